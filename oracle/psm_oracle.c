@@ -1,0 +1,709 @@
+/*
+ * psm_oracle.c — TEST INFRASTRUCTURE ONLY.  Plain, slow, fp64 CPU oracle of the PSM lattice
+ * Boltzmann hot path of arXiv 2502.20049 (Suffa et al.).  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference leg may load it.  The product path
+ * (paper_2502_20049_b200/) never links, imports or calls anything in this directory, and this
+ * file shares no code, header, table or helper with it.
+ *
+ * It runs the method itself, step by step, in the paper's notation:
+ *   Eq.(1)  LB update
+ *   Eq.(2)  SRT collision
+ *   Eq.(3)  equilibrium             PAPER.md:138-140  (u^2 term with "-", reading A1)
+ *   Eq.(4)  PSM update rule
+ *   Eq.(5)  B = eps
+ *   Eq.(6)  tau-weighted B
+ *   Eq.(7)-(9) SC1/SC2/SC3          PAPER.md:178-189  (SC2 in its literal printed form, A2)
+ *   Eq.(10)-(11) force / torque     PAPER.md:196-204  (returned with the sign ON the body, A6)
+ *   Sec. III geometry field + super-sampled fraction mapping, PAPER.md:299-321 (reading R1, A12)
+ * The readings taken where the paper is silent or garbled are listed in DESIGN.md §3
+ * (A1..A26); each use below names its reading.
+ *
+ * State convention (A10): f holds the Eq.(4) state, i.e. the PRE-collision populations
+ * f_i(x,t).  One step = collide every cell, then push f*_i(x) to x + c_i.
+ *
+ * Build: gcc -O2 -fopenmp -ffp-contract=off -shared -fPIC (no FMA contraction; explicit fma()
+ * only where reading A14 fixes it).  Parallelism: OpenMP over z planes only; every reduction is
+ * done per z-plane and then summed in plane order, so results do not depend on thread count.
+ *
+ * Parity status: every function here is pinned by a test in tests/test_oracle_*.py
+ * (DESIGN.md §4 lists the pin for each); none is "parity unpinned" except the absolute drag
+ * magnitude (P12(iii)), which the paper does not print.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_MAXB 16
+
+/* ---------------------------------------------------------------- stencils --
+ * Order is fixed by our ABI (lbmpy/waLBerla convention; the paper lists stencils only by name,
+ * PAPER.md:233).  Weights are the standard D3Q19/D3Q27 ones (sum 1, second moment c_s^2 = 1/3). */
+static const int C19[19][3] = {
+    {0, 0, 0},  {0, 1, 0},  {0, -1, 0}, {-1, 0, 0}, {1, 0, 0},  {0, 0, 1},   {0, 0, -1},
+    {-1, 1, 0}, {1, 1, 0},  {-1, -1, 0}, {1, -1, 0}, {0, 1, 1},  {0, -1, 1},  {-1, 0, 1},
+    {1, 0, 1},  {0, 1, -1}, {0, -1, -1}, {-1, 0, -1}, {1, 0, -1}};
+static const int C27x[8][3] = {{1, 1, 1},  {-1, 1, 1},  {1, -1, 1},  {-1, -1, 1},
+                               {1, 1, -1}, {-1, 1, -1}, {1, -1, -1}, {-1, -1, -1}};
+
+static void stencil_c(int Q, int i, int c[3]) {
+  const int* src = (i < 19) ? C19[i] : C27x[i - 19];
+  c[0] = src[0];
+  c[1] = src[1];
+  c[2] = src[2];
+  (void)Q;
+}
+
+static double stencil_w(int Q, int i) {
+  int c[3];
+  stencil_c(Q, i, c);
+  int n = abs(c[0]) + abs(c[1]) + abs(c[2]); /* 0 rest, 1 face, 2 edge, 3 corner */
+  if (Q == 19) {
+    if (n == 0) return 1.0 / 3.0;
+    if (n == 1) return 1.0 / 18.0;
+    return 1.0 / 36.0;
+  }
+  if (n == 0) return 8.0 / 27.0;
+  if (n == 1) return 2.0 / 27.0;
+  if (n == 2) return 1.0 / 54.0;
+  return 1.0 / 216.0;
+}
+
+/* i-bar: the direction with c_ibar = -c_i, found by search. */
+static int stencil_opp(int Q, int i) {
+  int c[3], d[3];
+  stencil_c(Q, i, c);
+  for (int j = 0; j < Q; ++j) {
+    stencil_c(Q, j, d);
+    if (d[0] == -c[0] && d[1] == -c[1] && d[2] == -c[2]) return j;
+  }
+  return -1;
+}
+
+/* Tables computed once from the definitions above (plain lookups in the per-cell loops). */
+static int TC[28][27][3], TOPP[28][27];
+static double TW[28][27];
+static int tables_ready = 0;
+static void tables_init(void) {
+  if (tables_ready) return;
+  for (int Q = 19; Q <= 27; Q += 8)
+    for (int i = 0; i < Q; ++i) {
+      stencil_c(Q, i, TC[Q][i]);
+      TW[Q][i] = stencil_w(Q, i);
+      TOPP[Q][i] = stencil_opp(Q, i);
+    }
+  tables_ready = 1;
+}
+
+void orc_stencil(int Q, int* c, double* w, int* opp) {
+  for (int i = 0; i < Q; ++i) {
+    stencil_c(Q, i, c + 3 * i);
+    w[i] = stencil_w(Q, i);
+    opp[i] = stencil_opp(Q, i);
+  }
+}
+
+/* ---------------------------------------------------------------------- Eq.(3) equilibrium --
+ * f_i^eq(u, rho) = w_i rho [1 + c_i.u / c_s^2 + (c_i.u)^2 / (2 c_s^4) - u^2 / (2 c_s^2)],
+ * c_s^2 = 1/3.  The printed "+ u^2/(2c_s^2)" is garbled: only "-" gives
+ * sum_i f_i^eq = rho (reading A1; pinned by P2). */
+static const double CS2 = 1.0 / 3.0;
+
+void orc_equilibrium(int Q, double rho, const double u[3], double* feq) {
+  double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+  for (int i = 0; i < Q; ++i) {
+    int c[3];
+    stencil_c(Q, i, c);
+    double cu = c[0] * u[0] + c[1] * u[1] + c[2] * u[2];
+    feq[i] = stencil_w(Q, i) * rho *
+             (1.0 + (cu / CS2 + (cu * cu) / (2.0 * CS2 * CS2) - uu / (2.0 * CS2)));
+  }
+}
+
+/* ------------------------------------------------------------------ Eq.(5) / Eq.(6): B(eps) --
+ * mode 0: B = eps.  mode 1: B = eps(tau-1/2) / ((1-eps) + (tau-1/2))
+ * (PAPER.md:159-161), evaluated in fp64 in exactly this operation order (reading A14). */
+double orc_weight_fraction(double eps, double tau, int mode) {
+  if (mode == 0) return eps;
+  return eps * (tau - 0.5) / ((1.0 - eps) + (tau - 0.5));
+}
+
+/* ------------------------------------------------------ one-cell collision, Eq.(2),(4),(7)-(9) --
+ * Computes f*_i = f_i + (1 - B) Omega^F_i + B Omega^S_i (Eq.(4)) for one cell, and
+ * m = B sum_i Omega^S_i c_i (the summand of Eq.(10)).  g is the test-only Guo body force (A-P12):
+ * u = (j + g/2)/rho and Omega^F gains (1 - 1/(2 tau)) w_i [(c_i - u)/c_s^2 + (c_i.u) c_i/c_s^4].g.
+ * Returns 0, or 1 if rho <= 0 or a value is non-finite (error rule of S:66/S:93). */
+int orc_collide_cell(int Q, const double* f, double tau, int sc, double B, const double us[3],
+                     const double g[3], double* fstar, double m[3]) {
+  tables_init();
+  double rho = 0.0, j[3] = {0.0, 0.0, 0.0};
+  for (int i = 0; i < Q; ++i) {
+    int c[3];
+    stencil_c(Q, i, c);
+    rho += f[i];
+    j[0] += f[i] * c[0];
+    j[1] += f[i] * c[1];
+    j[2] += f[i] * c[2];
+  }
+  m[0] = m[1] = m[2] = 0.0;
+  if (!(rho > 0.0) || !isfinite(rho)) {
+    for (int i = 0; i < Q; ++i) fstar[i] = f[i];
+    return 1;
+  }
+  double u[3];
+  for (int a = 0; a < 3; ++a) u[a] = (j[a] + 0.5 * g[a]) / rho; /* A4/A5: local pre-collision u */
+  double feq[27], fs[27], omF[27], omS[27];
+  orc_equilibrium(Q, rho, u, feq);
+  /* Eq.(2): Omega^F_i = -(1/tau)(f_i - f_i^eq) */
+  for (int i = 0; i < Q; ++i) {
+    omF[i] = -(f[i] - feq[i]) / tau;
+    if (g[0] != 0.0 || g[1] != 0.0 || g[2] != 0.0) {
+      int c[3];
+      stencil_c(Q, i, c);
+      double cu = c[0] * u[0] + c[1] * u[1] + c[2] * u[2];
+      double s = 0.0;
+      for (int a = 0; a < 3; ++a) s += ((c[a] - u[a]) / CS2 + cu * c[a] / (CS2 * CS2)) * g[a];
+      omF[i] += (1.0 - 1.0 / (2.0 * tau)) * stencil_w(Q, i) * s;
+    }
+  }
+  if (B > 0.0) {
+    orc_equilibrium(Q, rho, us, fs); /* f^eq(rho, u_s), rho = local rho (A3) */
+    for (int i = 0; i < Q; ++i) {
+      int ib = TOPP[Q][i];
+      if (sc == 1) /* Eq.(7) SC1 */
+        omS[i] = (f[ib] - feq[ib]) - (f[i] - fs[i]);
+      else if (sc == 2) /* Eq.(8) SC2, literal printed form with the missing ")" closed (A2) */
+        omS[i] = (fs[i] - f[i]) + (1.0 - 1.0 / tau) * (f[i] - fs[i]);
+      else /* Eq.(9) SC3 */
+        omS[i] = (f[ib] - fs[ib]) - (f[i] - fs[i]);
+    }
+    double sum[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < Q; ++i) {
+      int c[3];
+      stencil_c(Q, i, c);
+      fstar[i] = f[i] + (1.0 - B) * omF[i] + B * omS[i];
+      sum[0] += omS[i] * c[0];
+      sum[1] += omS[i] * c[1];
+      sum[2] += omS[i] * c[2];
+    }
+    m[0] = B * sum[0];
+    m[1] = B * sum[1];
+    m[2] = B * sum[2];
+  } else {
+    for (int i = 0; i < Q; ++i) fstar[i] = f[i] + omF[i]; /* Eq.(1) with Eq.(2) */
+  }
+  for (int i = 0; i < Q; ++i)
+    if (!isfinite(fstar[i])) return 1;
+  return 0;
+}
+
+/* --------------------------------------------------------------------------- pose (A13) -----
+ * Closed-form prescribed motion (one-way coupling): t_n = t_0 + n v, wrapped
+ * into [0, L) on periodic axes; Q_n = Rot(w/|w|, n|w|) Q_0 by Rodrigues' formula, host libm. */
+void orc_pose_advance(const double Q0[9], const double t0[3], const double v[3],
+                      const double w[3], int64_t n, const double L[3], const int periodic[3],
+                      double Qn[9], double tn[3]) {
+  for (int a = 0; a < 3; ++a) {
+    double t = t0[a] + (double)n * v[a];
+    if (periodic[a]) t = t - L[a] * floor(t / L[a]);
+    tn[a] = t;
+  }
+  double wn = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  if (wn > 0.0) {
+    double k[3] = {w[0] / wn, w[1] / wn, w[2] / wn};
+    double th = (double)n * wn, s = sin(th), c = cos(th);
+    double K[9] = {0, -k[2], k[1], k[2], 0, -k[0], -k[1], k[0], 0};
+    double K2[9];
+    for (int r = 0; r < 3; ++r)
+      for (int cc = 0; cc < 3; ++cc) {
+        double acc = 0.0;
+        for (int l = 0; l < 3; ++l) acc += K[3 * r + l] * K[3 * l + cc];
+        K2[3 * r + cc] = acc;
+      }
+    for (int e = 0; e < 9; ++e) R[e] += s * K[e] + (1.0 - c) * K2[e];
+  }
+  for (int r = 0; r < 3; ++r)
+    for (int cc = 0; cc < 3; ++cc) {
+      double acc = 0.0;
+      for (int l = 0; l < 3; ++l) acc += R[3 * r + l] * Q0[3 * l + cc];
+      Qn[3 * r + cc] = acc;
+    }
+}
+
+/* ------------------------------------------------------------ voxelizer (A15) --
+ * Geometry field G of a closed mesh, spacing h = 2^-s in the body frame,
+ * extent = mesh bbox padded by 2 LBM cells with an integer origin o_G (A17).  G[g] = 1 iff the
+ * sub-cell centre o_G + (g + 1/2) h is inside the mesh by ray parity along +x, decided exactly:
+ * vertices are snapped to the fixed-point grid 2^-(s+12) relative to o_G (sub-cell centres are
+ * then integers g*4096 + 2048), the (y,z) containment uses 2D edge functions with a top-left
+ * tie rule on the counter-clockwise-oriented projection, and a crossing counts iff it lies
+ * strictly at x > x_0 (sign of an exact int128 expression).  Degenerate projections count 0.
+ * Plain form: for every row (gy,gz), every triangle is tested; for each containing triangle the
+ * crossing is compared exactly with every sample of the row. */
+typedef __int128 i128;
+
+static int edge_inside(int64_t ay, int64_t az, int64_t by, int64_t bz, int64_t py, int64_t pz) {
+  /* E > 0 : P strictly left of a->b (inside for a CCW triangle).  Tie (E == 0): inside iff the
+   * edge is a "top" edge (horizontal, pointing to -y) or a "left" edge (pointing to -z). */
+  i128 e = (i128)(by - ay) * (i128)(pz - az) - (i128)(bz - az) * (i128)(py - ay);
+  if (e > 0) return 1;
+  if (e < 0) return 0;
+  int64_t dy = by - ay, dz = bz - az;
+  if (dz == 0 && dy < 0) return 1; /* top edge */
+  if (dz < 0) return 1;            /* left edge */
+  return 0;
+}
+
+int64_t orc_geometry_extent(const double* verts, int64_t nv, int s, double origin[3],
+                            int64_t dims[3]) {
+  for (int a = 0; a < 3; ++a) {
+    double lo = verts[a], hi = verts[a];
+    for (int64_t k = 1; k < nv; ++k) {
+      double x = verts[3 * k + a];
+      if (x < lo) lo = x;
+      if (x > hi) hi = x;
+    }
+    origin[a] = floor(lo) - 2.0;
+    dims[a] = ((int64_t)(ceil(hi) + 2.0 - origin[a])) << s;
+  }
+  return dims[0] * dims[1] * dims[2];
+}
+
+/* bits: [dims2][dims1][dims0] bytes (0/1), sized by orc_geometry_extent. */
+void orc_voxelize(const double* verts, int64_t nv, const int32_t* tris, int64_t nt, int s,
+                  uint8_t* bits) {
+  double origin[3];
+  int64_t dims[3];
+  orc_geometry_extent(verts, nv, s, origin, dims);
+  int64_t* V = (int64_t*)malloc(sizeof(int64_t) * 3 * (size_t)nv);
+  double scale = ldexp(1.0, s + 12);
+  for (int64_t k = 0; k < nv; ++k)
+    for (int a = 0; a < 3; ++a) V[3 * k + a] = llround((verts[3 * k + a] - origin[a]) * scale);
+  int64_t NX = dims[0];
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t row = 0; row < dims[1] * dims[2]; ++row) {
+    int64_t gy = row % dims[1], gz = row / dims[1];
+    int64_t Y0 = gy * 4096 + 2048, Z0 = gz * 4096 + 2048;
+    uint8_t* cnt = (uint8_t*)calloc((size_t)NX, 1);
+    for (int64_t t = 0; t < nt; ++t) {
+      const int64_t* A = V + 3 * (int64_t)tris[3 * t + 0];
+      const int64_t* Bv = V + 3 * (int64_t)tris[3 * t + 1];
+      const int64_t* Cv = V + 3 * (int64_t)tris[3 * t + 2];
+      /* projected signed area (2x) in the (y,z) plane */
+      i128 area = (i128)(Bv[1] - A[1]) * (i128)(Cv[2] - A[2]) -
+                  (i128)(Bv[2] - A[2]) * (i128)(Cv[1] - A[1]);
+      if (area == 0) continue;
+      const int64_t *P0 = A, *P1 = Bv, *P2 = Cv;
+      if (area < 0) { /* orient counter-clockwise */
+        P1 = Cv;
+        P2 = Bv;
+      }
+      if (!edge_inside(P0[1], P0[2], P1[1], P1[2], Y0, Z0)) continue;
+      if (!edge_inside(P1[1], P1[2], P2[1], P2[2], Y0, Z0)) continue;
+      if (!edge_inside(P2[1], P2[2], P0[1], P0[2], Y0, Z0)) continue;
+      /* plane normal n = (B-A) x (C-A) (original orientation; only the sign test below uses it) */
+      i128 e1[3] = {Bv[0] - A[0], Bv[1] - A[1], Bv[2] - A[2]};
+      i128 e2[3] = {Cv[0] - A[0], Cv[1] - A[1], Cv[2] - A[2]};
+      i128 n0 = e1[1] * e2[2] - e1[2] * e2[1];
+      i128 n1 = e1[2] * e2[0] - e1[0] * e2[2];
+      i128 n2 = e1[0] * e2[1] - e1[1] * e2[0];
+      /* crossing x* satisfies n.(X - A) = 0; x* - X0 = D / n0 with D = n.(A - P) */
+      for (int64_t gx = 0; gx < NX; ++gx) {
+        int64_t X0 = gx * 4096 + 2048;
+        i128 D = n0 * (i128)(A[0] - X0) + n1 * (i128)(A[1] - Y0) + n2 * (i128)(A[2] - Z0);
+        int right = (n0 > 0) ? (D > 0) : (D < 0);
+        if (right) cnt[gx] ^= 1;
+      }
+    }
+    uint8_t* dst = bits + row * NX;
+    for (int64_t gx = 0; gx < NX; ++gx) dst[gx] = cnt[gx];
+    free(cnt);
+  }
+  free(V);
+}
+
+/* ---------------------------------------------------------------------------- simulation ---- */
+typedef struct {
+  int present, kind, s; /* kind 0 sphere, 1 mesh */
+  double radius, rbound;
+  double Q[9], t[3], v[3], w[3];
+  double gorigin[3];
+  int64_t gdims[3];
+  uint8_t* gbits;
+} orc_body;
+
+typedef struct {
+  int nx, ny, nz, Q;
+  double tau;
+  int bc[3]; /* 0 periodic, 1 wall */
+  int sc, bmode;
+  double g[3];
+  double *f, *fnew;
+  double* B;
+  double* us;
+  uint8_t* id;
+  int32_t* cnt;
+  orc_body bodies[ORC_MAXB + 1];
+  double SF[ORC_MAXB + 1][3], ST[ORC_MAXB + 1][3], AF[ORC_MAXB + 1][3], AT[ORC_MAXB + 1][3];
+  int64_t step;
+  int64_t err_cell; /* -1 none */
+  int map_all_cells; /* 1: evaluate every cell for every body (no bbox restriction) */
+} orc_sim;
+
+static int64_t cidx(const orc_sim* S, int x, int y, int z) {
+  return ((int64_t)z * S->ny + y) * S->nx + x;
+}
+
+orc_sim* orc_create(int nx, int ny, int nz, int Q, double tau, const int bc[3], int sc,
+                    int bmode) {
+  tables_init();
+  orc_sim* S = (orc_sim*)calloc(1, sizeof(orc_sim));
+  S->nx = nx;
+  S->ny = ny;
+  S->nz = nz;
+  S->Q = Q;
+  S->tau = tau;
+  for (int a = 0; a < 3; ++a) S->bc[a] = bc[a];
+  S->sc = sc;
+  S->bmode = bmode;
+  int64_t N = (int64_t)nx * ny * nz;
+  S->f = (double*)calloc((size_t)(Q * N), sizeof(double));
+  S->fnew = (double*)calloc((size_t)(Q * N), sizeof(double));
+  S->B = (double*)calloc((size_t)N, sizeof(double));
+  S->us = (double*)calloc((size_t)(3 * N), sizeof(double));
+  S->id = (uint8_t*)calloc((size_t)N, 1);
+  S->cnt = (int32_t*)calloc((size_t)N, sizeof(int32_t));
+  S->err_cell = -1;
+  return S;
+}
+
+void orc_destroy(orc_sim* S) {
+  if (!S) return;
+  for (int b = 0; b <= ORC_MAXB; ++b) free(S->bodies[b].gbits);
+  free(S->f);
+  free(S->fnew);
+  free(S->B);
+  free(S->us);
+  free(S->id);
+  free(S->cnt);
+  free(S);
+}
+
+void orc_set_force(orc_sim* S, const double g[3]) {
+  for (int a = 0; a < 3; ++a) S->g[a] = g[a];
+}
+void orc_set_map_all_cells(orc_sim* S, int on) { S->map_all_cells = on; }
+
+void orc_init_equilibrium(orc_sim* S, const double* rho, const double* u) {
+  int64_t N = (int64_t)S->nx * S->ny * S->nz;
+  for (int64_t x = 0; x < N; ++x) {
+    double r = rho ? rho[x] : 1.0;
+    double uu[3] = {u ? u[x] : 0.0, u ? u[N + x] : 0.0, u ? u[2 * N + x] : 0.0};
+    double feq[27];
+    orc_equilibrium(S->Q, r, uu, feq);
+    for (int i = 0; i < S->Q; ++i) S->f[(int64_t)i * N + x] = feq[i];
+  }
+  S->step = 0;
+}
+
+void orc_set_pdfs(orc_sim* S, const double* f) {
+  memcpy(S->f, f, sizeof(double) * (size_t)S->Q * S->nx * S->ny * S->nz);
+}
+void orc_get_pdfs(const orc_sim* S, double* f) {
+  memcpy(f, S->f, sizeof(double) * (size_t)S->Q * S->nx * S->ny * S->nz);
+}
+
+/* rho and u = j / rho of the Eq.(4) state */
+void orc_get_velocity(const orc_sim* S, double* rho, double* u) {
+  int64_t N = (int64_t)S->nx * S->ny * S->nz;
+  for (int64_t x = 0; x < N; ++x) {
+    double r = 0, j[3] = {0, 0, 0};
+    for (int i = 0; i < S->Q; ++i) {
+      int c[3];
+      stencil_c(S->Q, i, c);
+      double fi = S->f[(int64_t)i * N + x];
+      r += fi;
+      j[0] += fi * c[0];
+      j[1] += fi * c[1];
+      j[2] += fi * c[2];
+    }
+    if (rho) rho[x] = r;
+    if (u)
+      for (int a = 0; a < 3; ++a) u[(int64_t)a * N + x] = j[a] / r;
+  }
+}
+
+/* Body setup.  Sphere: radius r, bounding radius r.  Mesh: voxelised once here,
+ * bounding radius = max |vertex| (body frame). */
+int orc_set_sphere(orc_sim* S, int id, double r, int s) {
+  if (id < 1 || id > ORC_MAXB) return -1;
+  orc_body* b = &S->bodies[id];
+  free(b->gbits);
+  memset(b, 0, sizeof(*b));
+  b->present = 1;
+  b->kind = 0;
+  b->s = s;
+  b->radius = r;
+  b->rbound = r;
+  b->Q[0] = b->Q[4] = b->Q[8] = 1.0;
+  return 0;
+}
+
+int orc_set_mesh(orc_sim* S, int id, const double* verts, int64_t nv, const int32_t* tris,
+                 int64_t nt, int s) {
+  if (id < 1 || id > ORC_MAXB) return -1;
+  orc_body* b = &S->bodies[id];
+  free(b->gbits);
+  memset(b, 0, sizeof(*b));
+  b->present = 1;
+  b->kind = 1;
+  b->s = s;
+  int64_t n = orc_geometry_extent(verts, nv, s, b->gorigin, b->gdims);
+  b->gbits = (uint8_t*)calloc((size_t)n, 1);
+  orc_voxelize(verts, nv, tris, nt, s, b->gbits);
+  double rb = 0.0;
+  for (int64_t k = 0; k < nv; ++k) {
+    double x = verts[3 * k], y = verts[3 * k + 1], z = verts[3 * k + 2];
+    double r = sqrt(x * x + y * y + z * z);
+    if (r > rb) rb = r;
+  }
+  b->rbound = rb;
+  b->Q[0] = b->Q[4] = b->Q[8] = 1.0;
+  return 0;
+}
+
+void orc_remove_body(orc_sim* S, int id) {
+  if (id < 1 || id > ORC_MAXB) return;
+  free(S->bodies[id].gbits);
+  memset(&S->bodies[id], 0, sizeof(orc_body));
+}
+
+int orc_get_geometry(const orc_sim* S, int id, double origin[3], int64_t dims[3],
+                     uint8_t* bits) {
+  const orc_body* b = &S->bodies[id];
+  if (!b->present || b->kind != 1) return -1;
+  for (int a = 0; a < 3; ++a) {
+    origin[a] = b->gorigin[a];
+    dims[a] = b->gdims[a];
+  }
+  if (bits) memcpy(bits, b->gbits, (size_t)(b->gdims[0] * b->gdims[1] * b->gdims[2]));
+  return 0;
+}
+
+void orc_set_pose(orc_sim* S, int id, const double Q[9], const double t[3], const double v[3],
+                  const double w[3]) {
+  orc_body* b = &S->bodies[id];
+  memcpy(b->Q, Q, sizeof(b->Q));
+  memcpy(b->t, t, sizeof(b->t));
+  memcpy(b->v, v, sizeof(b->v));
+  memcpy(b->w, w, sizeof(b->w));
+}
+
+/* Minimum image on a periodic axis of length L (A7). */
+static double mi(double d, double L, int periodic) {
+  if (!periodic) return d;
+  if (d >= 0.5 * L)
+    d -= L;
+  else if (d < -0.5 * L)
+    d += L;
+  return d;
+}
+
+/* Inside test of one sub-sample for body b, at world point p (reading R1, A12): the sample is
+ * mapped into the body frame, q = Q^T mi(p - t), with the fma order of A14. */
+static int sample_inside(const orc_sim* S, const orc_body* b, const double p[3]) {
+  double L[3] = {S->nx, S->ny, S->nz};
+  double d[3];
+  for (int a = 0; a < 3; ++a) d[a] = mi(p[a] - b->t[a], L[a], S->bc[a] == 0);
+  double q[3];
+  for (int a = 0; a < 3; ++a)
+    q[a] = fma(b->Q[6 + a], d[2], fma(b->Q[3 + a], d[1], b->Q[0 + a] * d[0]));
+  if (b->kind == 0) return fma(q[2], q[2], fma(q[1], q[1], q[0] * q[0])) <= b->radius * b->radius;
+  double hs = ldexp(1.0, b->s);
+  int64_t g[3];
+  for (int a = 0; a < 3; ++a) {
+    double x = floor((q[a] - b->gorigin[a]) * hs);
+    if (!(x >= 0.0) || x >= (double)b->gdims[a]) return 0; /* outside the field: outside (A17) */
+    g[a] = (int64_t)x;
+  }
+  return b->gbits[(g[2] * b->gdims[1] + g[1]) * b->gdims[0] + g[0]];
+}
+
+/* Fraction mapping: for each cell, eps_b = (#inside sub-samples)/2^(3s) over
+ * the 2^(3s) sub-cell centres (A16); the body with the largest eps wins, ties to the lower id
+ * (A18); B by Eq.(5)/(6); u_s = v + w x mi(x_c - t) (rigid motion). */
+void orc_map(orc_sim* S) {
+  double L[3] = {S->nx, S->ny, S->nz};
+#pragma omp parallel for schedule(static)
+  for (int z = 0; z < S->nz; ++z)
+    for (int y = 0; y < S->ny; ++y)
+      for (int x = 0; x < S->nx; ++x) {
+        int64_t c = cidx(S, x, y, z);
+        int best = 0, bestcnt = 0;
+        double xc[3] = {x + 0.5, y + 0.5, z + 0.5};
+        for (int id = 1; id <= ORC_MAXB; ++id) {
+          const orc_body* b = &S->bodies[id];
+          if (!b->present) continue;
+          if (!S->map_all_cells) { /* conservative bbox: |mi(x_c - t)|_a <= rbound + 1 per axis */
+            int in = 1;
+            for (int a = 0; a < 3; ++a)
+              if (fabs(mi(xc[a] - b->t[a], L[a], S->bc[a] == 0)) > b->rbound + 1.0) in = 0;
+            if (!in) continue;
+          }
+          int n = 1 << b->s, cnt = 0;
+          double h = ldexp(1.0, -b->s);
+          for (int gz = 0; gz < n; ++gz)
+            for (int gy = 0; gy < n; ++gy)
+              for (int gx = 0; gx < n; ++gx) {
+                double p[3] = {x + (gx + 0.5) * h, y + (gy + 0.5) * h, z + (gz + 0.5) * h};
+                cnt += sample_inside(S, b, p);
+              }
+          /* compare eps exactly: cnt / 8^s as a dyadic double */
+          double e = ldexp((double)cnt, -3 * b->s);
+          double eb = best ? ldexp((double)bestcnt, -3 * S->bodies[best].s) : 0.0;
+          if (cnt > 0 && e > eb) {
+            best = id;
+            bestcnt = cnt;
+          }
+        }
+        S->cnt[c] = bestcnt;
+        S->id[c] = (uint8_t)best;
+        int64_t N = (int64_t)S->nx * S->ny * S->nz;
+        if (best) {
+          const orc_body* b = &S->bodies[best];
+          double e = ldexp((double)bestcnt, -3 * b->s);
+          S->B[c] = orc_weight_fraction(e, S->tau, S->bmode);
+          double r[3];
+          for (int a = 0; a < 3; ++a) r[a] = mi(xc[a] - b->t[a], L[a], S->bc[a] == 0);
+          S->us[c] = b->v[0] + (b->w[1] * r[2] - b->w[2] * r[1]);
+          S->us[N + c] = b->v[1] + (b->w[2] * r[0] - b->w[0] * r[2]);
+          S->us[2 * N + c] = b->v[2] + (b->w[0] * r[1] - b->w[1] * r[0]);
+        } else {
+          S->B[c] = 0.0;
+          S->us[c] = S->us[N + c] = S->us[2 * N + c] = 0.0;
+        }
+      }
+}
+
+/* TEST-ONLY explicit fields (P4): B[N], us[3][N], id[N]. */
+void orc_set_fields(orc_sim* S, const double* B, const double* us, const uint8_t* id) {
+  int64_t N = (int64_t)S->nx * S->ny * S->nz;
+  memcpy(S->B, B, sizeof(double) * (size_t)N);
+  memcpy(S->us, us, sizeof(double) * 3 * (size_t)N);
+  memcpy(S->id, id, (size_t)N);
+  memset(S->cnt, 0, sizeof(int32_t) * (size_t)N);
+}
+
+void orc_get_fractions(const orc_sim* S, double* B, uint8_t* id, int32_t* cnt, double* us) {
+  int64_t N = (int64_t)S->nx * S->ny * S->nz;
+  if (B) memcpy(B, S->B, sizeof(double) * (size_t)N);
+  if (id) memcpy(id, S->id, (size_t)N);
+  if (cnt) memcpy(cnt, S->cnt, sizeof(int32_t) * (size_t)N);
+  if (us) memcpy(us, S->us, sizeof(double) * 3 * (size_t)N);
+}
+
+/* One time step n -> n+1 (DESIGN.md §3 "oracle step"): collide every cell with the current B,
+ * u_s, id fields (Eq.(4)), accumulate Eqs.(10)-(11), then push f*_i(x) to x + c_i (Eq.(1)); on a
+ * wall axis a population leaving the domain returns as f_ibar(x) (half-way bounce-back, A23).
+ * Returns 0, or 1 on an invalid state (first offending cell in cell order is recorded). */
+int orc_step(orc_sim* S) {
+  const int Q = S->Q, nx = S->nx, ny = S->ny, nz = S->nz;
+  const int64_t N = (int64_t)nx * ny * nz;
+  double L[3] = {nx, ny, nz};
+  double(*pSF)[ORC_MAXB + 1][3] = calloc((size_t)nz, sizeof(*pSF));
+  double(*pST)[ORC_MAXB + 1][3] = calloc((size_t)nz, sizeof(*pST));
+  double(*pAF)[ORC_MAXB + 1][3] = calloc((size_t)nz, sizeof(*pAF));
+  double(*pAT)[ORC_MAXB + 1][3] = calloc((size_t)nz, sizeof(*pAT));
+  int64_t* perr = (int64_t*)malloc(sizeof(int64_t) * (size_t)nz);
+#pragma omp parallel for schedule(static)
+  for (int z = 0; z < nz; ++z) {
+    perr[z] = -1;
+    for (int y = 0; y < ny; ++y)
+      for (int x = 0; x < nx; ++x) {
+        int64_t c = cidx(S, x, y, z);
+        double f[27], fs[27], m[3];
+        for (int i = 0; i < Q; ++i) f[i] = S->f[(int64_t)i * N + c];
+        double us[3] = {S->us[c], S->us[N + c], S->us[2 * N + c]};
+        double B = S->B[c];
+        int bad = orc_collide_cell(Q, f, S->tau, S->sc, B, us, S->g, fs, m);
+        if (bad && perr[z] < 0) perr[z] = c;
+        int id = S->id[c];
+        if (B > 0.0) {
+          double R[3] = {0, 0, 0};
+          if (id > 0) R[0] = S->bodies[id].t[0], R[1] = S->bodies[id].t[1],
+                      R[2] = S->bodies[id].t[2];
+          double xc[3] = {x + 0.5, y + 0.5, z + 0.5}, r[3];
+          for (int a = 0; a < 3; ++a) r[a] = mi(xc[a] - R[a], L[a], S->bc[a] == 0);
+          double tq[3] = {r[1] * m[2] - r[2] * m[1], r[2] * m[0] - r[0] * m[2],
+                          r[0] * m[1] - r[1] * m[0]};
+          for (int a = 0; a < 3; ++a) {
+            pSF[z][id][a] += m[a];
+            pST[z][id][a] += tq[a];
+            pAF[z][id][a] += fabs(m[a]);
+            pAT[z][id][a] += fabs(tq[a]);
+          }
+        }
+        /* stream (push) */
+        for (int i = 0; i < Q; ++i) {
+          int cc[3];
+          stencil_c(Q, i, cc);
+          int xn[3] = {x + cc[0], y + cc[1], z + cc[2]};
+          int n3[3] = {nx, ny, nz};
+          int wall = 0;
+          for (int a = 0; a < 3; ++a) {
+            if (xn[a] < 0 || xn[a] >= n3[a]) {
+              if (S->bc[a] == 1)
+                wall = 1;
+              else
+                xn[a] = (xn[a] + n3[a]) % n3[a];
+            }
+          }
+          if (wall)
+            S->fnew[(int64_t)TOPP[Q][i] * N + c] = fs[i];
+          else
+            S->fnew[(int64_t)i * N + cidx(S, xn[0], xn[1], xn[2])] = fs[i];
+        }
+      }
+  }
+  for (int id = 0; id <= ORC_MAXB; ++id)
+    for (int a = 0; a < 3; ++a) S->SF[id][a] = S->ST[id][a] = S->AF[id][a] = S->AT[id][a] = 0.0;
+  int err = 0;
+  for (int z = 0; z < nz; ++z) {
+    for (int id = 0; id <= ORC_MAXB; ++id)
+      for (int a = 0; a < 3; ++a) {
+        S->SF[id][a] += pSF[z][id][a];
+        S->ST[id][a] += pST[z][id][a];
+        S->AF[id][a] += pAF[z][id][a];
+        S->AT[id][a] += pAT[z][id][a];
+      }
+    if (!err && perr[z] >= 0) {
+      err = 1;
+      S->err_cell = perr[z];
+    }
+  }
+  free(pSF);
+  free(pST);
+  free(pAF);
+  free(pAT);
+  free(perr);
+  double* t = S->f;
+  S->f = S->fnew;
+  S->fnew = t;
+  S->step += 1;
+  return err;
+}
+
+int64_t orc_error_cell(const orc_sim* S) { return S->err_cell; }
+
+/* Force and torque ON body id (A6): F = -sum B sum_i Omega^S_i c_i (the printed Eq.(10) sum is
+ * the momentum the fluid gains), T = -sum B (x_c - R) x sum_i Omega^S_i c_i (Eq.(11), A7). */
+void orc_force_torque(const orc_sim* S, int id, double F[3], double T[3], double AF[3],
+                      double AT[3]) {
+  for (int a = 0; a < 3; ++a) {
+    F[a] = -S->SF[id][a];
+    T[a] = -S->ST[id][a];
+    if (AF) AF[a] = S->AF[id][a];
+    if (AT) AT[a] = S->AT[id][a];
+  }
+}

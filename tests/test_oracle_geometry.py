@@ -1,0 +1,223 @@
+"""Pins of the oracle's geometry path (P9-P10): super-sampled fraction mapping
+(reading R1) and the exact voxelizer (reading A15), against brute force and
+exact symmetries computed here independently."""
+import numpy as np
+import pytest
+
+import oracle
+import psm_inputs as pi
+
+
+def _brute_sphere_counts(shape, t, r, s):
+    """Independent numpy brute force: count sub-sample centres with |p - t|^2 <= r^2.
+    Coordinates are dyadic and t is a lattice vertex, so every square is exact."""
+    nz, ny, nx = shape
+    n = 1 << s
+    h = 2.0 ** -s
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    cnt = np.zeros(shape, np.int64)
+    for a in range(n):
+        for b in range(n):
+            for c in range(n):
+                d2 = ((x + (a + 0.5) * h - t[0]) ** 2 + (y + (b + 0.5) * h - t[1]) ** 2
+                      + (z + (c + 0.5) * h - t[2]) ** 2)
+                cnt += d2 <= r * r
+    return cnt
+
+
+@pytest.mark.parametrize("s,expect", [(0, 912.0), (1, 901.0), (2, 904.0), (3, 905.078125)])
+def test_p9_sphere_fraction_brute_force(s, expect):
+    """r = 6 centred at the lattice vertex (16,16,16) of a 32^3 box.  Sum of eps equals the
+    number of sub-sample centres inside the ball / 8^s (exact counts), and approaches
+    4/3 pi r^3 = 904.7787 within 1%."""
+    o = oracle.Oracle(32, 32, 32, 19, 0.8, (0, 0, 0), 1, 0)
+    o.set_sphere(1, 6.0, s)
+    o.set_pose(1, np.eye(3), (16.0, 16.0, 16.0))
+    o.map()
+    B, bid, cnt, _ = o.fractions()
+    ref = _brute_sphere_counts((32, 32, 32), (16.0, 16.0, 16.0), 6.0, s)
+    assert np.array_equal(cnt, ref)
+    assert cnt.sum() / 8 ** s == expect
+    assert abs(expect / (4 / 3 * np.pi * 216) - 1) < 0.01
+    assert np.array_equal(B, cnt / 8.0 ** s)  # direct mode: B = eps exactly (Eq.(5))
+    assert np.array_equal(bid, (cnt > 0).astype(np.uint8))
+    if s == 2:
+        assert (cnt == 64).sum() == 672 and (cnt > 0).sum() == 1136
+
+
+def test_p9_bbox_restriction_is_conservative():
+    o = oracle.Oracle(24, 20, 28, 19, 0.8, (0, 0, 0), 1, 1)
+    o.set_sphere(1, 5.3, 1)
+    Q = pi.rotation_about([1, -1, 2], 0.7)
+    o.set_pose(1, Q, (22.3, 1.7, 14.2))  # wraps across x and y periodic boundaries
+    o.map()
+    a = o.fractions()
+    o.set_map_all_cells(True)
+    o.map()
+    b = o.fractions()
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    assert a[2].sum() > 0
+
+
+def test_p9_translating_sphere_sequence():
+    """c2 geometry: r=6, s=2, start (32,32,32), v = (1/32,0,0) (dyadic, poses exact).  Sum eps
+    for n = 0..7 is periodic with period 8, and cnt(x, n+32) = cnt(x - e_x, n) exactly."""
+    expect = [904, 904.4375, 904.5, 904.375, 904.6875, 904.375, 904.5, 904.4375]
+    o = oracle.Oracle(128, 64, 64, 19, 0.575, (0, 1, 1), 2, 1)
+    o.set_sphere(1, 6.0, 2)
+    cnts = {}
+    for n in list(range(9)) + [32]:
+        t = (32.0 + n / 32.0, 32.0, 32.0)
+        o.set_pose(1, np.eye(3), t, (1 / 32, 0, 0))
+        o.map()
+        _, _, cnt, _ = o.fractions()
+        cnts[n] = cnt
+        if n < 8:
+            assert cnt.sum() / 64 == expect[n]
+            ref = _brute_sphere_counts((64, 64, 128), t, 6.0, 2)
+            assert np.array_equal(cnt, ref)
+    assert cnts[8].sum() == cnts[0].sum()
+    assert np.array_equal(cnts[32], np.roll(cnts[0], 1, axis=2))
+
+
+# ------------------------------------------------------------------------------ mesh / P10 ---
+def test_p10_aligned_cube_s0_has_64_inside():
+    v, t = pi.box_mesh([-2, -2, -2], [2, 2, 2])
+    o = oracle.Oracle(16, 16, 16, 19, 0.8, (0, 0, 0), 1, 0)
+    o.set_mesh(1, v, t, 0)
+    o.set_pose(1, np.eye(3), (8.0, 8.0, 8.0))
+    o.map()
+    _, bid, cnt, _ = o.fractions()
+    assert cnt.sum() == 64 and np.all(cnt[6:10, 6:10, 6:10] == 1)
+
+
+@pytest.mark.parametrize("s", [0, 1, 2])
+def test_p10_orientation_flip_leaves_bits_unchanged(s):
+    v, t = pi.propeller_mesh(n_blades=3, scale=0.1, n_st=6, n_pts=12, hub_seg=12)
+    o1, b1 = oracle.voxelize(v, t, s)
+    o2, b2 = oracle.voxelize(v, t[:, ::-1], s)
+    assert np.array_equal(o1, o2) and np.array_equal(b1, b2)
+    assert b1.sum() > 0
+
+
+def _downsample(bits, s):
+    n = 1 << s
+    gz, gy, gx = bits.shape
+    return bits.reshape(gz // n, n, gy // n, n, gx // n, n).sum(axis=(1, 3, 5))
+
+
+@pytest.mark.parametrize("s", [0, 1, 2])
+def test_p10_identity_pose_equals_downsampled_geometry(s):
+    v, t = pi.propeller_mesh(n_blades=3, scale=0.1, n_st=8, n_pts=16, hub_seg=16)
+    origin, bits = oracle.voxelize(v, t, s)
+    down = _downsample(bits.astype(np.int64), s)
+    o = oracle.Oracle(32, 32, 32, 19, 0.8, (0, 0, 0), 1, 0)
+    o.set_mesh(1, v, t, s)
+    tpos = np.array([16.0, 15.0, 17.0])
+    o.set_pose(1, np.eye(3), tpos)
+    o.map()
+    _, _, cnt, _ = o.fractions()
+    lo = (tpos + origin).astype(int)  # world cell of geometry brick (0,0,0)
+    gz, gy, gx = down.shape
+    window = cnt[lo[2]:lo[2] + gz, lo[1]:lo[1] + gy, lo[0]:lo[0] + gx]
+    assert np.array_equal(window, down)
+    assert cnt.sum() == down.sum()
+
+
+@pytest.mark.parametrize("axis,k", [(0, 1), (1, 1), (2, 1), (2, 2), (0, 3)])
+def test_p10_rot90_is_an_exact_permutation(axis, k):
+    """Q with entries in {0, +-1} about a lattice vertex t: the count field at pose Q equals the
+    identity-pose field re-indexed by x'_c = t + Q^T (x_c - t) (exact transform)."""
+    v, tr = pi.propeller_mesh(n_blades=3, scale=0.1, n_st=8, n_pts=16, hub_seg=16)
+    n = 32
+    tpos = np.array([16.0, 16.0, 16.0])
+    o = oracle.Oracle(n, n, n, 19, 0.8, (0, 0, 0), 1, 0)
+    o.set_mesh(1, v, tr, 1)
+    o.set_pose(1, np.eye(3), tpos)
+    o.map()
+    c0 = o.fractions()[2]
+    R = pi.rot90(axis, k)
+    o.set_pose(1, R, tpos)
+    o.map()
+    cR = o.fractions()[2]
+    z, y, x = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    xc = np.stack([x, y, z], 0).reshape(3, -1) + 0.5
+    xp = tpos[:, None] + R.T @ (xc - tpos[:, None]) - 0.5
+    xp = np.rint(xp).astype(int) % n
+    perm = c0[xp[2], xp[1], xp[0]].reshape(n, n, n)
+    assert np.array_equal(cR, perm)
+    assert cR.sum() == c0.sum() > 0
+
+
+def test_p10_mesh_box_matches_analytic_box_at_generic_pose():
+    """A 12-triangle box mapped at a generic rotation equals the analytic box tested at the
+    geometry-cell centre each sub-sample falls in (the paper's lookup)."""
+    a = 3.3
+    v, tr = pi.box_mesh([-a, -a, -a], [a, a, a])
+    s = 1
+    o = oracle.Oracle(20, 20, 20, 19, 0.8, (0, 0, 0), 1, 0)
+    o.set_mesh(1, v, tr, s)
+    Q = pi.rotation_about([0.3, -0.5, 0.8], 0.61)
+    tpos = np.array([10.2, 9.7, 10.05])
+    o.set_pose(1, Q, tpos)
+    o.map()
+    cnt = o.fractions()[2]
+    origin, _ = oracle.voxelize(v, tr, s)
+    h = 2.0 ** -s
+    nsub = 1 << s
+    ref = np.zeros_like(cnt)
+    amb = np.zeros(cnt.shape, bool)
+    off = (np.arange(nsub) + 0.5) * h
+    z, y, x = np.meshgrid(np.arange(20), np.arange(20), np.arange(20), indexing="ij")
+    for gz in off:
+        for gy in off:
+            for gx in off:
+                p = np.stack([x + gx, y + gy, z + gz], 0).reshape(3, -1)
+                q = Q.T @ (p - tpos[:, None])
+                g = np.floor((q - origin[:, None]) / h)
+                frac = (q - origin[:, None]) / h - g
+                cen = origin[:, None] + (g + 0.5) * h
+                inside = np.all(np.abs(cen) < a, axis=0)
+                near = np.any(np.abs(np.abs(cen) - a) < 1e-9, axis=0) | np.any(
+                    (frac < 1e-9) | (frac > 1 - 1e-9), axis=0)
+                ref += inside.reshape(cnt.shape)
+                amb |= near.reshape(cnt.shape)
+    assert amb.mean() < 0.01
+    assert np.array_equal(cnt[~amb], ref[~amb])
+    # the geometry field represents the box by whole sub-cells: side 14 h = 7 (centres |c| < a)
+    assert abs(cnt.sum() / 8 - 7.0 ** 3) / 7.0 ** 3 < 0.02
+
+
+def _winding_number(points, verts, tris):
+    """Generalised winding number (sum of solid angles / 4 pi, Van Oosterom-Strackee)."""
+    A = verts[tris[:, 0]]
+    B = verts[tris[:, 1]]
+    Cc = verts[tris[:, 2]]
+    out = np.zeros(len(points))
+    for k in range(0, len(points), 2048):
+        P = points[k:k + 2048, None, :]
+        a, b, c = A[None] - P, B[None] - P, Cc[None] - P
+        la, lb, lc = (np.linalg.norm(x, axis=2) for x in (a, b, c))
+        det = np.einsum("pti,pti->pt", a, np.cross(b, c))
+        den = (la * lb * lc + np.einsum("pti,pti->pt", a, b) * lc
+               + np.einsum("pti,pti->pt", b, c) * la + np.einsum("pti,pti->pt", c, a) * lb)
+        out[k:k + 2048] = (2 * np.arctan2(det, den)).sum(1) / (4 * np.pi)
+    return out
+
+
+def test_p10_voxelizer_matches_winding_number_on_sphere_mesh():
+    v, tr = pi.uv_sphere_mesh(3.7, 10, 20)
+    s = 1
+    origin, bits = oracle.voxelize(v, tr, s)
+    gz, gy, gx = bits.shape
+    h = 2.0 ** -s
+    z, y, x = np.meshgrid(np.arange(gz), np.arange(gy), np.arange(gx), indexing="ij")
+    pts = np.stack([x, y, z], -1).reshape(-1, 3) * h + origin + 0.5 * h
+    wn = _winding_number(pts, v, tr)
+    sure = np.abs(wn - np.rint(wn)) < 1e-6
+    assert sure.mean() > 0.99
+    assert np.array_equal(bits.reshape(-1)[sure], np.rint(wn[sure]).astype(np.uint8))
+    # inside volume ~ polyhedron volume (divergence theorem)
+    vol = np.einsum("ij,ij->i", v[tr[:, 0]], np.cross(v[tr[:, 1]], v[tr[:, 2]])).sum() / 6
+    assert abs(bits.sum() * h ** 3 / vol - 1) < 0.05
