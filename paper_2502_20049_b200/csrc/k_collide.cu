@@ -1,0 +1,343 @@
+// k_collide.cu — fused PSM stream-collide (arXiv 2502.20049, Eq.(4)) with the
+// SRT fluid operator (Eq.(2)-(3)), the solid operators SC1/SC2/SC3
+// (Eqs.(7)-(9)), B(eps) by Eq.(5)/(6) and the per-body
+// force/torque partials of Eqs.(10)-(11), for sm_100a.
+//
+// One thread per cell, one 32x4x2 tile per 256-thread block, SoA f[q][z][y][x] (x fastest):
+// every direction plane is read and written with coalesced 32-wide rows.  The kernel is
+// HBM-bound (2*Q*S bytes per cell update); the PSM work is confined to tiles whose
+// flag the mapping kernel set, so fluid tiles run the plain SRT path and never touch the solid
+// words.  Streaming patterns (reading A10):
+//   PAT 0  two-array pull : f_i(x) = A_i(x - c_i)  (wall: A_ibar(x)); write B_i(x) = f*_i(x)
+//   PAT 1  AA even step   : f_i(x) = A[i][x];                      write A[ibar][x] = f*_i
+//   PAT 2  AA odd step    : f_i(x) = A[ibar][x - c_i] (wall: A[i][x]);
+//                           write A[i][x + c_i] = f*_i (wall: A[ibar][x])
+#include "psm_device.cuh"
+#include "psm_internal.h"
+
+namespace psm {
+
+template <int Q, typename T>
+__device__ __forceinline__ T feq_q(int q, T rho, T ux, T uy, T uz, T usq15) {
+  // w rho [1 + 3 c.u + 4.5 (c.u)^2 - 1.5 u.u]  (Eq.(3) with c_s^2 = 1/3, "-" sign: reading A1)
+  const T cu = T(stc_x(q)) * ux + T(stc_y(q)) * uy + T(stc_z(q)) * uz;
+  return T(stc_w<Q>(q)) * rho * (T(1) - usq15 + cu * (T(3) + T(4.5) * cu));
+}
+
+template <int Q, typename T>
+__device__ __forceinline__ T guo_q(int q, T ux, T uy, T uz, const T g[3], T pref) {
+  // (1 - 1/(2 tau)) w_i [3 (c_i - u) + 9 (c_i.u) c_i] . g   (test-only forcing)
+  const T cx = T(stc_x(q)), cy = T(stc_y(q)), cz = T(stc_z(q));
+  const T cu = cx * ux + cy * uy + cz * uz;
+  const T s = (T(3) * (cx - ux) + T(9) * cu * cx) * g[0] + (T(3) * (cy - uy) + T(9) * cu * cy) * g[1] +
+              (T(3) * (cz - uz) + T(9) * cu * cz) * g[2];
+  return pref * T(stc_w<Q>(q)) * s;
+}
+
+__device__ __forceinline__ double weight_fraction(double e, double tau, int mode) {
+  // Eq.(6) in fp64, fixed operation order (bit-exact with the method definition, A14)
+  if (mode == 0) return e;
+  const double a = __dsub_rn(tau, 0.5);
+  return __ddiv_rn(__dmul_rn(e, a), __dadd_rn(__dsub_rn(1.0, e), a));
+}
+
+// Deterministic per-tile reduction of the Eq.(10)-(11) summands: the (at most) two smallest
+// body ids present in the tile get a slot each (fixed warp-butterfly + fixed warp order), a third
+// or later body in the same tile falls back to fp64 atomics in `overflow` (never happens unless
+// bodies overlap one tile).  Slot layout: [id, v[0..11]].  Called by every thread of the block.
+__device__ __forceinline__ void tile_partial_reduce(int myid, const double* v, double* out,
+                                                    double* overflow) {
+  __shared__ unsigned s_min[kTileCells / 32];
+  __shared__ unsigned s_ids[2];
+  __shared__ double s_red[kTileCells / 32][kSlotVals];
+  const int tid = threadIdx.x + kTileX * (threadIdx.y + kTileY * threadIdx.z);
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kTileCells / 32;
+  unsigned ids[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const unsigned key = (myid && (s == 0 || (unsigned)myid != ids[0])) ? (unsigned)myid
+                                                                         : 0xFFFFFFFFu;
+    const unsigned k = __reduce_min_sync(0xFFFFFFFFu, key);
+    if (lane == 0) s_min[warp] = k;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned mm = s_min[0];
+      for (int w = 1; w < NW; ++w) mm = min(mm, s_min[w]);
+      s_ids[s] = mm;
+    }
+    __syncthreads();
+    ids[s] = s_ids[s];
+  }
+#pragma unroll 1
+  for (int s = 0; s < 2; ++s) {
+    if (ids[s] == 0xFFFFFFFFu) {
+      if (tid == 0) out[s * (1 + kSlotVals)] = 0.0;
+      continue;
+    }
+#pragma unroll
+    for (int k = 0; k < kSlotVals; ++k) {
+      double a = ((unsigned)myid == ids[s]) ? v[k] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+      if (lane == 0) s_red[warp][k] = a;
+    }
+    __syncthreads();
+    if (tid < kSlotVals) {
+      double acc = s_red[0][tid];
+      for (int w = 1; w < NW; ++w) acc += s_red[w][tid];
+      out[s * (1 + kSlotVals) + 1 + tid] = acc;
+    }
+    if (tid == 0) out[s * (1 + kSlotVals)] = (double)ids[s];
+    __syncthreads();
+  }
+  if (myid && (unsigned)myid != ids[0] && (unsigned)myid != ids[1]) {
+    for (int k = 0; k < kSlotVals; ++k) atomicAdd(overflow + myid * kSlotVals + k, v[k]);
+  }
+}
+
+template <int Q, typename T, int PAT, bool FORCE, bool DBG>
+__global__ void __launch_bounds__(kTileCells)
+    k_collide(const __grid_constant__ CollideParams p) {
+  const Geom& G = p.g;
+  const int x = blockIdx.x * kTileX + threadIdx.x;
+  const int y = blockIdx.y * kTileY + threadIdx.y;
+  const int z = blockIdx.z * kTileZ + threadIdx.z;
+  const bool act = (x < G.nx) && (y < G.ny) && (z < G.nzl);
+  const int tile = (blockIdx.z * G.gy + blockIdx.y) * G.gx + blockIdx.x;
+  const bool solid_tile = DBG ? true : (p.tile_flag[tile] != 0);
+
+  const int nx = G.nx, ny = G.ny;
+  const int xc = act ? x : 0, yc = act ? y : 0, zc = act ? z : 0;
+  const int zs = zc + G.zghost;  // storage plane
+  // source coordinate for a population with velocity component d is (coord - d)
+  int sx_p = xc - 1, sx_m = xc + 1, sy_p = yc - 1, sy_m = yc + 1, sz_p = zs - 1, sz_m = zs + 1;
+  bool ox_p = false, ox_m = false, oy_p = false, oy_m = false, oz_p = false, oz_m = false;
+  if (sx_p < 0) { if (G.wall[0]) ox_p = true; else sx_p += nx; }
+  if (sx_m >= nx) { if (G.wall[0]) ox_m = true; else sx_m -= nx; }
+  if (sy_p < 0) { if (G.wall[1]) oy_p = true; else sy_p += ny; }
+  if (sy_m >= ny) { if (G.wall[1]) oy_m = true; else sy_m -= ny; }
+  if (G.zghost) {
+    const int zg = G.z0 + zc;
+    if (G.wall[2]) { oz_p = (zg == 0); oz_m = (zg == G.nz_global - 1); }
+  } else {
+    if (sz_p < 0) { if (G.wall[2]) oz_p = true; else sz_p += G.nzl; }
+    if (sz_m >= G.nzl) { if (G.wall[2]) oz_m = true; else sz_m -= G.nzl; }
+  }
+  const int self = (zs * ny + yc) * nx + xc;
+  const long long qs = G.qstride;
+
+  T f[Q];
+  {
+    const T* A = static_cast<const T*>(p.src);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int cx = stc_x(q), cy = stc_y(q), cz = stc_z(q);
+      const int sx = cx > 0 ? sx_p : (cx < 0 ? sx_m : xc);
+      const int sy = cy > 0 ? sy_p : (cy < 0 ? sy_m : yc);
+      const int sz = cz > 0 ? sz_p : (cz < 0 ? sz_m : zs);
+      const bool out = (cx > 0 ? ox_p : (cx < 0 ? ox_m : false)) ||
+                       (cy > 0 ? oy_p : (cy < 0 ? oy_m : false)) ||
+                       (cz > 0 ? oz_p : (cz < 0 ? oz_m : false));
+      const int src = (sz * ny + sy) * nx + sx;
+      T v = T(0);
+      if (act) {
+        if (PAT == 0) {
+          v = out ? __ldg(A + stc_opp(q) * qs + self) : __ldg(A + q * qs + src);
+        } else if (PAT == 1) {
+          v = A[q * qs + self];
+        } else {
+          v = out ? A[q * qs + self] : A[stc_opp(q) * qs + src];
+        }
+      }
+      f[q] = v;
+    }
+  }
+
+  // moments of the pre-collision state
+  T rho = T(0), jx = T(0), jy = T(0), jz = T(0);
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    rho += f[q];
+    if (stc_x(q) > 0) jx += f[q]; else if (stc_x(q) < 0) jx -= f[q];
+    if (stc_y(q) > 0) jy += f[q]; else if (stc_y(q) < 0) jy -= f[q];
+    if (stc_z(q) > 0) jz += f[q]; else if (stc_z(q) < 0) jz -= f[q];
+  }
+  if (act && !(rho > T(0) && rho < T(INFINITY))) {
+    const long long cell =
+        ((long long)(G.z0 + z) * G.ny + y) * (long long)G.nx + x;
+    const long long ncell = (long long)G.nz_global * G.ny * G.nx;
+    atomicMin(p.err, (unsigned long long)(p.step * ncell + cell));
+  }
+  const T ir = act ? T(1) / rho : T(0);
+  T gl[3] = {T(p.gforce[0]), T(p.gforce[1]), T(p.gforce[2])};
+  const T ux = FORCE ? (jx + T(0.5) * gl[0]) * ir : jx * ir;
+  const T uy = FORCE ? (jy + T(0.5) * gl[1]) * ir : jy * ir;
+  const T uz = FORCE ? (jz + T(0.5) * gl[2]) * ir : jz * ir;
+  const T usq15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
+  const T om = T(p.omega);
+  const T gpref = T(1) - T(0.5) * om;
+
+  if (!solid_tile) {
+    // plain SRT: f* = f + omega (f^eq - f)   (Eq.(1) with Eq.(2))
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      T o = om * (feq_q<Q, T>(q, rho, ux, uy, uz, usq15) - f[q]);
+      if (FORCE) o += guo_q<Q, T>(q, ux, uy, uz, gl, gpref);
+      f[q] = f[q] + o;
+    }
+  } else {
+    // ---- PSM cell: B, u_s from the solid word (or the test-only dense fields) ----
+    int id = 0;
+    double Bd = 0.0;
+    double usd[3] = {0.0, 0.0, 0.0};
+    double r[3] = {0.0, 0.0, 0.0};
+    if (act) {
+      if (DBG) {
+        const long long c = ((long long)z * ny + y) * nx + x;
+        Bd = p.dbg_B[c];
+        id = p.dbg_id[c];
+        const long long N = (long long)G.nzl * ny * nx;
+        usd[0] = p.dbg_us[c];
+        usd[1] = p.dbg_us[N + c];
+        usd[2] = p.dbg_us[2 * N + c];
+      } else {
+        const uint32_t w = p.word[((long long)z * ny + y) * nx + x];
+        id = (int)(w >> 16);
+        if (id) {
+          const int cnt = (int)(w & 0xFFFFu);
+          const double e = ldexp((double)cnt, -3 * p.bodies[id].s);
+          Bd = weight_fraction(e, p.tau, p.bmode);
+        }
+      }
+      if (id) {
+        const BodyKin& b = p.bodies[id];
+        const double L[3] = {(double)nx, (double)ny, (double)G.nz_global};
+        const double xcen[3] = {x + 0.5, y + 0.5, (double)(G.z0 + z) + 0.5};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) r[a] = min_image(xcen[a] - b.t[a], L[a], !G.wall[a]);
+        if (!DBG) {
+          usd[0] = b.v[0] + (b.w[1] * r[2] - b.w[2] * r[1]);
+          usd[1] = b.v[1] + (b.w[2] * r[0] - b.w[0] * r[2]);
+          usd[2] = b.v[2] + (b.w[0] * r[1] - b.w[1] * r[0]);
+        }
+      }
+    }
+    double m[3] = {0.0, 0.0, 0.0};
+    if (Bd > 0.0) {
+      const T B = T(Bd), B1 = T(1) - T(Bd);
+      const T sux = T(usd[0]), suy = T(usd[1]), suz = T(usd[2]);
+      const T susq15 = T(1.5) * (sux * sux + suy * suy + suz * suz);
+      T msx = T(0), msy = T(0), msz = T(0);
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        const int j = stc_opp(i);
+        if (j < i) continue;  // each (i, ibar) pair once
+        const T fi = f[i], fj = f[j];
+        const T ei = feq_q<Q, T>(i, rho, ux, uy, uz, usq15);
+        const T ej = feq_q<Q, T>(j, rho, ux, uy, uz, usq15);
+        const T si = feq_q<Q, T>(i, rho, sux, suy, suz, susq15);
+        const T sj = feq_q<Q, T>(j, rho, sux, suy, suz, susq15);
+        T oFi = om * (ei - fi), oFj = om * (ej - fj);
+        if (FORCE) {
+          oFi += guo_q<Q, T>(i, ux, uy, uz, gl, gpref);
+          oFj += guo_q<Q, T>(j, ux, uy, uz, gl, gpref);
+        }
+        T oSi, oSj;
+        if (p.sc == 1) {         // Eq.(7)
+          oSi = (fj - ej) - (fi - si);
+          oSj = (fi - ei) - (fj - sj);
+        } else if (p.sc == 2) {  // Eq.(8) == -(f_i - f^eq_i(rho,u_s))/tau (reading A2)
+          oSi = om * (si - fi);
+          oSj = om * (sj - fj);
+        } else {                 // Eq.(9)
+          oSi = (fj - sj) - (fi - si);
+          oSj = (fi - si) - (fj - sj);
+        }
+        f[i] = fi + B1 * oFi + B * oSi;
+        if (j != i) f[j] = fj + B1 * oFj + B * oSj;
+        if (j != i) {
+          const T d = oSi - oSj;  // c_j = -c_i
+          msx += T(stc_x(i)) * d;
+          msy += T(stc_y(i)) * d;
+          msz += T(stc_z(i)) * d;
+        }
+      }
+      m[0] = Bd * (double)msx;
+      m[1] = Bd * (double)msy;
+      m[2] = Bd * (double)msz;
+    } else {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        T o = om * (feq_q<Q, T>(q, rho, ux, uy, uz, usq15) - f[q]);
+        if (FORCE) o += guo_q<Q, T>(q, ux, uy, uz, gl, gpref);
+        f[q] = f[q] + o;
+      }
+    }
+    // ---- per-body F/T partial of this tile (deterministic block reduction) ----
+    double v[kSlotVals];
+    v[0] = m[0]; v[1] = m[1]; v[2] = m[2];
+    v[3] = r[1] * m[2] - r[2] * m[1];
+    v[4] = r[2] * m[0] - r[0] * m[2];
+    v[5] = r[0] * m[1] - r[1] * m[0];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) v[6 + a] = fabs(v[a]);
+    const int myid = (Bd > 0.0) ? id : 0;
+    tile_partial_reduce(myid, v, p.partial + (size_t)tile * 2 * (1 + kSlotVals), p.overflow);
+  }
+
+  if (act) {
+    T* Aout = static_cast<T*>(p.dst);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (PAT == 0) {
+        __stcs(Aout + q * qs + self, f[q]);
+      } else if (PAT == 1) {
+        Aout[stc_opp(q) * qs + self] = f[q];
+      } else {
+        // destination x + c_q == source position of the opposite direction
+        const int cx = stc_x(q), cy = stc_y(q), cz = stc_z(q);
+        const int dx = cx > 0 ? sx_m : (cx < 0 ? sx_p : xc);
+        const int dy = cy > 0 ? sy_m : (cy < 0 ? sy_p : yc);
+        const int dz = cz > 0 ? sz_m : (cz < 0 ? sz_p : zs);
+        const bool out = (cx > 0 ? ox_m : (cx < 0 ? ox_p : false)) ||
+                         (cy > 0 ? oy_m : (cy < 0 ? oy_p : false)) ||
+                         (cz > 0 ? oz_m : (cz < 0 ? oz_p : false));
+        if (out)
+          Aout[stc_opp(q) * qs + self] = f[q];
+        else
+          Aout[q * qs + (dz * ny + dy) * nx + dx] = f[q];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ launcher ---
+template <int Q, typename T>
+static cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool dbg,
+                            cudaStream_t st) {
+  dim3 grid(p.g.gx, p.g.gy, p.g.gz), block(kTileX, kTileY, kTileZ);
+  if (dbg) {
+    if (force) k_collide<Q, T, 0, true, true><<<grid, block, 0, st>>>(p);
+    else k_collide<Q, T, 0, false, true><<<grid, block, 0, st>>>(p);
+  } else if (force) {
+    k_collide<Q, T, 0, true, false><<<grid, block, 0, st>>>(p);
+  } else if (pat == 0) {
+    k_collide<Q, T, 0, false, false><<<grid, block, 0, st>>>(p);
+  } else if (pat == 1) {
+    k_collide<Q, T, 1, false, false><<<grid, block, 0, st>>>(p);
+  } else {
+    k_collide<Q, T, 2, false, false><<<grid, block, 0, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_collide(int Q, bool fp64, const CollideParams& p, int pat, bool force,
+                           bool dbg, cudaStream_t st) {
+  if (Q == 19) return fp64 ? launch_t<19, double>(p, pat, force, dbg, st)
+                           : launch_t<19, float>(p, pat, force, dbg, st);
+  return fp64 ? launch_t<27, double>(p, pat, force, dbg, st)
+              : launch_t<27, float>(p, pat, force, dbg, st);
+}
+
+}  // namespace psm

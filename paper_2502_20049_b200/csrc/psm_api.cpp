@@ -1,0 +1,1127 @@
+// psm_api.cpp — C ABI of the B200 PSM hot path (include/psm.h).  Host orchestration only:
+// validation, memory layout, closed-form pose advance (host fp64 libm, reading A13),
+// remap-box planning, the per-step launch sequence, NCCL halo exchange and force/torque
+// allreduce.  Every arithmetic step of the method runs in the sm_100a kernels (k_*.cu).
+#include "psm.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "psm_device.cuh"
+#include "psm_host.h"
+#include "psm_internal.h"
+
+using namespace psm;
+
+namespace {
+
+constexpr int kFtChunks = 296;           // 2 x 148 SMs, pass-1 blocks of the F/T reduction
+constexpr size_t kStageBudget = 256ull << 20;
+constexpr size_t kGeomCapBytes = 1ull << 30;
+
+struct Body {
+  bool present = false;
+  int kind = 0, s = 0;
+  double radius = 0, rbound = 0;
+  // mesh geometry field (device)
+  double o[3] = {0, 0, 0};
+  int64_t dims[3] = {0, 0, 0};
+  int words = 1;
+  unsigned long long* d_bits = nullptr;
+  uint8_t* d_mask = nullptr;
+  // prescribed motion: pose at step0, closed-form advance
+  double Q0[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, t0[3] = {0, 0, 0};
+  double v[3] = {0, 0, 0}, w[3] = {0, 0, 0};
+  int64_t step0 = 0;
+  bool moving = false;
+  // pose of the current mapping
+  double Qc[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, tc[3] = {0, 0, 0};
+  int64_t mapped_step = -1;
+  bool has_box = false;
+  int64_t box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};  // last mapped box (global, unwrapped)
+};
+
+struct Box {
+  int64_t lo[3], hi[3];  // global cells, [lo, hi), already wrapped into the domain
+};
+
+}  // namespace
+
+struct psm_ctx {
+  psm_grid grid{};
+  int Q = 19;
+  double tau = 0.8;
+  psm_options opt{};
+  int rank = 0, world = 1;
+  int64_t z0 = 0, nzl = 0;
+  Geom geom{};
+  int64_t ncell_local = 0, ntiles = 0;
+  size_t S = 8;
+  // device memory
+  void* mem = nullptr;
+  size_t mem_bytes = 0;
+  bool own_mem = false, bound = false;
+  void* A[2] = {nullptr, nullptr};
+  int cur = 0;
+  uint32_t* word = nullptr;
+  uint8_t* tile_flag = nullptr;
+  double* partial = nullptr;
+  double* overflow = nullptr;
+  unsigned long long* err = nullptr;
+  double* ft_scratch = nullptr;
+  double* ft_out = nullptr;
+  int* ft_ids = nullptr;
+  double* stage = nullptr;
+  size_t stage_bytes = 0;
+  double* pinned = nullptr;  // host staging (ft + err)
+  // test-only dense fields
+  double *dbg_B = nullptr, *dbg_us = nullptr;
+  uint8_t* dbg_id = nullptr;
+  bool dbg = false;
+  Body bodies[kMaxBodies + 1];
+  int64_t step = 0;
+  double ft[kMaxBodies + 1][kSlotVals] = {};
+  bool ft_valid = false;
+  cudaStream_t st = nullptr;
+  ncclComm_t comm = nullptr;
+  std::string err_msg;
+  int64_t launches = 0;
+  bool prof = false;
+  std::vector<std::array<cudaEvent_t, 2>> ev[PSM_NUM_PHASES];
+  double prof_ms[PSM_NUM_PHASES] = {};
+  int64_t prof_cnt[PSM_NUM_PHASES] = {};
+};
+
+static std::string g_last_error;
+
+#define FAIL(ctx, code, msg)                  \
+  do {                                        \
+    std::string _m = (msg);                   \
+    if (ctx) (ctx)->err_msg = _m;             \
+    g_last_error = _m;                        \
+    return (code);                            \
+  } while (0)
+
+#define CUDA_TRY(ctx, expr)                                                             \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      FAIL(ctx, PSM_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+  } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                             \
+  do {                                                                                  \
+    ncclResult_t _r = (expr);                                                           \
+    if (_r != ncclSuccess)                                                              \
+      FAIL(ctx, PSM_E_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));        \
+  } while (0)
+
+// ---------------------------------------------------------------------------- helpers ------
+static void rodrigues(const double w[3], double n, const double Q0[9], double out[9]) {
+  // Q_n = Rot(w/|w|, n|w|) Q_0 (A13: host libm sin/cos)
+  const double wn = std::sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  if (wn > 0.0) {
+    const double k[3] = {w[0] / wn, w[1] / wn, w[2] / wn};
+    const double th = n * wn, s = std::sin(th), c = 1.0 - std::cos(th);
+    const double K[9] = {0, -k[2], k[1], k[2], 0, -k[0], -k[1], k[0], 0};
+    for (int r = 0; r < 3; ++r)
+      for (int cc = 0; cc < 3; ++cc) {
+        double k2 = 0.0;
+        for (int l = 0; l < 3; ++l) k2 += K[3 * r + l] * K[3 * l + cc];
+        R[3 * r + cc] += s * K[3 * r + cc] + c * k2;
+      }
+  }
+  for (int r = 0; r < 3; ++r)
+    for (int cc = 0; cc < 3; ++cc) {
+      double acc = 0.0;
+      for (int l = 0; l < 3; ++l) acc += R[3 * r + l] * Q0[3 * l + cc];
+      out[3 * r + cc] = acc;
+    }
+}
+
+static double extent(const psm_ctx* c, int a) {
+  return (double)(a == 0 ? c->grid.nx : (a == 1 ? c->grid.ny : c->grid.nz));
+}
+
+static void pose_at(const psm_ctx* c, const Body& b, int64_t step, double Q[9], double t[3]) {
+  const double n = (double)(step - b.step0);
+  for (int a = 0; a < 3; ++a) {
+    double x = b.t0[a] + n * b.v[a];
+    if (c->grid.bc[a] == PSM_PERIODIC) {
+      const double L = extent(c, a);
+      x = x - L * std::floor(x / L);
+    }
+    t[a] = x;
+  }
+  rodrigues(b.w, n, b.Q0, Q);
+}
+
+static void body_box(const psm_ctx* c, const Body& b, const double t[3], int64_t lo[3],
+                     int64_t hi[3]) {
+  (void)c;
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = (int64_t)std::floor(t[a] - b.rbound - 1.0);
+    hi[a] = (int64_t)std::floor(t[a] + b.rbound + 1.0) + 1;
+  }
+}
+
+// split [lo, hi) on axis a into in-domain pieces
+static int axis_pieces(const psm_ctx* c, int a, int64_t lo, int64_t hi, int64_t out[2][2]) {
+  const int64_t L = (int64_t)extent(c, a);
+  if (c->grid.bc[a] != PSM_PERIODIC) {
+    lo = std::max<int64_t>(lo, 0);
+    hi = std::min<int64_t>(hi, L);
+    if (hi <= lo) return 0;
+    out[0][0] = lo;
+    out[0][1] = hi;
+    return 1;
+  }
+  if (hi - lo >= L) {
+    out[0][0] = 0;
+    out[0][1] = L;
+    return 1;
+  }
+  int64_t l = ((lo % L) + L) % L, len = hi - lo;
+  if (l + len <= L) {
+    out[0][0] = l;
+    out[0][1] = l + len;
+    return 1;
+  }
+  out[0][0] = l;
+  out[0][1] = L;
+  out[1][0] = 0;
+  out[1][1] = l + len - L;
+  return 2;
+}
+
+static void add_box(const psm_ctx* c, const int64_t lo[3], const int64_t hi[3],
+                    std::vector<Box>& boxes) {
+  int64_t px[2][2], py[2][2], pz[2][2];
+  const int nxp = axis_pieces(c, 0, lo[0], hi[0], px);
+  const int nyp = axis_pieces(c, 1, lo[1], hi[1], py);
+  const int nzp = axis_pieces(c, 2, lo[2], hi[2], pz);
+  for (int i = 0; i < nxp; ++i)
+    for (int j = 0; j < nyp; ++j)
+      for (int k = 0; k < nzp; ++k) {
+        Box b;
+        b.lo[0] = px[i][0]; b.hi[0] = px[i][1];
+        b.lo[1] = py[j][0]; b.hi[1] = py[j][1];
+        b.lo[2] = pz[k][0]; b.hi[2] = pz[k][1];
+        boxes.push_back(b);
+      }
+}
+
+// region to remap for body b moving to pose t: hull of the old and new boxes if they overlap
+// (after the periodic shift that brings them closest), both boxes otherwise
+static void remap_region(const psm_ctx* c, Body& b, const double t[3], std::vector<Box>& boxes) {
+  int64_t lo[3], hi[3];
+  body_box(c, b, t, lo, hi);
+  if (b.has_box) {
+    bool overlap = true;
+    int64_t slo[3], shi[3];
+    for (int a = 0; a < 3; ++a) {
+      int64_t shift = 0;
+      if (c->grid.bc[a] == PSM_PERIODIC) {
+        const int64_t L = (int64_t)extent(c, a);
+        const double dc = 0.5 * ((lo[a] + hi[a]) - (b.box_lo[a] + b.box_hi[a]));
+        shift = -(int64_t)std::llround(dc / (double)L) * L;
+      }
+      slo[a] = lo[a] + shift;
+      shi[a] = hi[a] + shift;
+      if (slo[a] >= b.box_hi[a] || shi[a] <= b.box_lo[a]) overlap = false;
+    }
+    if (overlap) {
+      int64_t ulo[3], uhi[3];
+      for (int a = 0; a < 3; ++a) {
+        ulo[a] = std::min(slo[a], b.box_lo[a]);
+        uhi[a] = std::max(shi[a], b.box_hi[a]);
+      }
+      add_box(c, ulo, uhi, boxes);
+    } else {
+      add_box(c, b.box_lo, b.box_hi, boxes);
+      add_box(c, lo, hi, boxes);
+    }
+  } else {
+    add_box(c, lo, hi, boxes);
+  }
+  for (int a = 0; a < 3; ++a) {
+    b.box_lo[a] = lo[a];
+    b.box_hi[a] = hi[a];
+  }
+  b.has_box = true;
+}
+
+static cudaError_t record(psm_ctx* c, int phase, int which) {
+  if (!c->prof) return cudaSuccess;
+  if (which == 0) {
+    std::array<cudaEvent_t, 2> e{};
+    cudaError_t r = cudaEventCreate(&e[0]);
+    if (r != cudaSuccess) return r;
+    r = cudaEventCreate(&e[1]);
+    if (r != cudaSuccess) return r;
+    c->ev[phase].push_back(e);
+  }
+  return cudaEventRecord(c->ev[phase].back()[which], c->st);
+}
+
+// ------------------------------------------------------------------------- memory plan -----
+struct Plan {
+  size_t off_A0, off_A1, off_word, off_flag, off_partial, off_overflow, off_err, off_scratch,
+      off_ftout, off_ids, off_stage, stage_bytes, total;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static Plan make_plan(const psm_ctx* c) {
+  Plan p{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  const size_t arr = (size_t)c->Q * (size_t)c->geom.qstride * c->S;
+  p.off_A0 = take(arr);
+  p.off_A1 = (c->opt.pattern == PSM_TWO_ARRAY) ? take(arr) : 0;
+  p.off_word = take((size_t)c->ncell_local * 4);
+  p.off_flag = take((size_t)c->ntiles);
+  p.off_partial = take((size_t)c->ntiles * 2 * (1 + kSlotVals) * 8);
+  p.off_overflow = take((kMaxBodies + 1) * kSlotVals * 8);
+  p.off_err = take(8);
+  p.off_scratch = take((size_t)kFtChunks * kMaxBodies * kSlotVals * 8);
+  p.off_ftout = take(kMaxBodies * kSlotVals * 8);
+  p.off_ids = take(kMaxBodies * 4);
+  const size_t plane = (size_t)c->grid.nx * c->grid.ny * 8;
+  const size_t per = plane * (size_t)c->Q;
+  size_t planes = std::max<size_t>(3, kStageBudget / per);
+  planes = std::min<size_t>(planes, (size_t)c->nzl + 2);
+  p.stage_bytes = planes * per;
+  p.off_stage = take(p.stage_bytes);
+  p.total = off;
+  return p;
+}
+
+static psm_status ensure_pinned(psm_ctx* c);
+
+static psm_status bind(psm_ctx* c, void* mem, size_t bytes) {
+  psm_status ps = ensure_pinned(c);
+  if (ps != PSM_OK) return ps;
+  Plan p = make_plan(c);
+  if (bytes < p.total)
+    FAIL(c, PSM_E_OOM, "bound buffer has " + std::to_string(bytes) + " bytes, need " +
+                           std::to_string(p.total));
+  char* m = static_cast<char*>(mem);
+  c->mem = mem;
+  c->mem_bytes = bytes;
+  c->A[0] = m + p.off_A0;
+  c->A[1] = (c->opt.pattern == PSM_TWO_ARRAY) ? (void*)(m + p.off_A1) : nullptr;
+  c->word = reinterpret_cast<uint32_t*>(m + p.off_word);
+  c->tile_flag = reinterpret_cast<uint8_t*>(m + p.off_flag);
+  c->partial = reinterpret_cast<double*>(m + p.off_partial);
+  c->overflow = reinterpret_cast<double*>(m + p.off_overflow);
+  c->err = reinterpret_cast<unsigned long long*>(m + p.off_err);
+  c->ft_scratch = reinterpret_cast<double*>(m + p.off_scratch);
+  c->ft_out = reinterpret_cast<double*>(m + p.off_ftout);
+  c->ft_ids = reinterpret_cast<int*>(m + p.off_ids);
+  c->stage = reinterpret_cast<double*>(m + p.off_stage);
+  c->stage_bytes = p.stage_bytes;
+  CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->st));
+  CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->st));
+  CUDA_TRY(c, cudaMemsetAsync(c->overflow, 0, (kMaxBodies + 1) * kSlotVals * 8, c->st));
+  CUDA_TRY(c, cudaMemsetAsync(c->err, 0xFF, 8, c->st));
+  c->bound = true;
+  return PSM_OK;
+}
+
+static psm_status ensure_pinned(psm_ctx* c) {
+  if (c->pinned) return PSM_OK;
+  if (cudaMallocHost(&c->pinned, (kMaxBodies + 2) * kSlotVals * 8) != cudaSuccess) {
+    cudaGetLastError();
+    c->pinned = nullptr;
+    FAIL(c, PSM_E_OOM, "cudaMallocHost failed");
+  }
+  return PSM_OK;
+}
+
+static psm_status ensure_mem(psm_ctx* c) {
+  psm_status ps = ensure_pinned(c);
+  if (ps != PSM_OK) return ps;
+  if (c->bound) return PSM_OK;
+  Plan p = make_plan(c);
+  void* m = nullptr;
+  if (cudaMalloc(&m, p.total) != cudaSuccess) {
+    cudaGetLastError();
+    FAIL(c, PSM_E_OOM, "cudaMalloc of " + std::to_string(p.total) + " bytes failed");
+  }
+  c->own_mem = true;
+  return bind(c, m, p.total);
+}
+
+static psm_status halo(psm_ctx* c, void* arr) {
+  // two-array pull: ship the c_z = +1 populations of the top plane up and the c_z = -1
+  // populations of the bottom plane down, straight from/into the SoA planes (no packing)
+  if (c->world == 1) return PSM_OK;
+  if (record(c, 3, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+  const int P = c->world, r = c->rank;
+  const bool zwall = c->grid.bc[2] == PSM_WALL;
+  const int up = (r + 1) % P, down = (r - 1 + P) % P;
+  const bool has_up = !(zwall && r == P - 1), has_down = !(zwall && r == 0);
+  const size_t plane = (size_t)c->grid.nx * c->grid.ny;
+  const ncclDataType_t dt = (c->opt.prec == PSM_F64) ? ncclFloat64 : ncclFloat32;
+  char* base = static_cast<char*>(arr);
+  auto ptr = [&](int q, int64_t zs) {
+    return base + ((size_t)q * (size_t)c->geom.qstride + (size_t)zs * plane) * c->S;
+  };
+  NCCL_TRY(c, ncclGroupStart());
+  for (int q = 0; q < c->Q; ++q) {
+    const int cz = stc_z(q);
+    if (cz > 0) {
+      if (has_up) NCCL_TRY(c, ncclSend(ptr(q, c->nzl), plane, dt, up, c->comm, c->st));
+      if (has_down) NCCL_TRY(c, ncclRecv(ptr(q, 0), plane, dt, down, c->comm, c->st));
+    } else if (cz < 0) {
+      if (has_down) NCCL_TRY(c, ncclSend(ptr(q, 1), plane, dt, down, c->comm, c->st));
+      if (has_up) NCCL_TRY(c, ncclRecv(ptr(q, c->nzl + 1), plane, dt, up, c->comm, c->st));
+    }
+  }
+  NCCL_TRY(c, ncclGroupEnd());
+  if (record(c, 3, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+  return PSM_OK;
+}
+
+static void fill_kin(const psm_ctx* c, CollideParams& p, int64_t step) {
+  for (int id = 0; id <= kMaxBodies; ++id) {
+    BodyKin& k = p.bodies[id];
+    std::memset(&k, 0, sizeof(k));
+    const Body& b = c->bodies[id];
+    if (!b.present) continue;
+    double Q[9], t[3];
+    pose_at(c, b, step, Q, t);
+    (void)Q;
+    (void)t;
+    for (int a = 0; a < 3; ++a) {
+      k.t[a] = b.tc[a];  // pose of the current mapping (remapped before this collide)
+      k.v[a] = b.v[a];
+      k.w[a] = b.w[a];
+    }
+    k.s = b.s;
+    k.present = 1;
+  }
+}
+
+static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
+  MapParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.g = c->geom;
+  mp.word = c->word;
+  mp.tile_flag = c->tile_flag;
+  for (int id = 1; id <= kMaxBodies; ++id) {
+    const Body& b = c->bodies[id];
+    BodyGeo& g = mp.bodies[id];
+    if (!b.present) continue;
+    std::memcpy(g.Q, b.Qc, sizeof(g.Q));
+    std::memcpy(g.t, b.tc, sizeof(g.t));
+    g.rb1 = b.rbound + 1.0;
+    g.r2 = b.radius * b.radius;
+    for (int a = 0; a < 3; ++a) {
+      g.o[a] = b.o[a];
+      g.dims_b[a] = (int)b.dims[a];
+    }
+    g.kind = b.kind;
+    g.s = b.s;
+    g.words = b.words;
+    g.present = 1;
+    g.bits = b.d_bits;
+    g.mask = b.d_mask;
+  }
+  // boxes -> local tile boxes, launched in batches of kMaxBoxes
+  std::vector<MapBox> tb;
+  for (const Box& b : boxes) {
+    const int64_t zlo = std::max<int64_t>(b.lo[2], c->z0) - c->z0;
+    const int64_t zhi = std::min<int64_t>(b.hi[2], c->z0 + c->nzl) - c->z0;
+    if (zhi <= zlo || b.hi[0] <= b.lo[0] || b.hi[1] <= b.lo[1]) continue;
+    MapBox m;
+    m.t0[0] = (int)(b.lo[0] / kTileX);
+    m.n[0] = (int)((b.hi[0] - 1) / kTileX + 1 - m.t0[0]);
+    m.t0[1] = (int)(b.lo[1] / kTileY);
+    m.n[1] = (int)((b.hi[1] - 1) / kTileY + 1 - m.t0[1]);
+    m.t0[2] = (int)(zlo / kTileZ);
+    m.n[2] = (int)((zhi - 1) / kTileZ + 1 - m.t0[2]);
+    m.first = 0;
+    tb.push_back(m);
+  }
+  if (record(c, 0, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+  for (size_t i = 0; i < tb.size(); i += kMaxBoxes) {
+    const size_t nb = std::min<size_t>(kMaxBoxes, tb.size() - i);
+    int total = 0;
+    for (size_t k = 0; k < nb; ++k) {
+      mp.box[k] = tb[i + k];
+      mp.box[k].first = total;
+      total += mp.box[k].n[0] * mp.box[k].n[1] * mp.box[k].n[2];
+    }
+    mp.nbox = (int)nb;
+    mp.ntiles = total;
+    CUDA_TRY(c, launch_map(mp, c->st));
+    c->launches += 1;
+  }
+  if (record(c, 0, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+  return PSM_OK;
+}
+
+// remap the given bodies at the pose of `step` (or all present bodies if ids empty)
+static psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
+  std::vector<Box> boxes;
+  for (int id : ids) {
+    Body& b = c->bodies[id];
+    if (!b.present) continue;
+    double Q[9], t[3];
+    if (b.moving) {
+      pose_at(c, b, step, Q, t);
+    } else {
+      std::memcpy(Q, b.Q0, sizeof(Q));
+      std::memcpy(t, b.t0, sizeof(t));
+    }
+    std::memcpy(b.Qc, Q, sizeof(Q));
+    std::memcpy(b.tc, t, sizeof(t));
+    remap_region(c, b, t, boxes);
+    b.mapped_step = step;
+  }
+  if (boxes.empty()) return PSM_OK;
+  if (c->dbg) {  // leaving the debug field mode: the words are authoritative again
+    c->dbg = false;
+    CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->st));
+    psm_status s = PSM_OK;
+    std::vector<Box> all;
+    for (int id = 1; id <= kMaxBodies; ++id)
+      if (c->bodies[id].present && c->bodies[id].has_box)
+        add_box(c, c->bodies[id].box_lo, c->bodies[id].box_hi, all);
+    CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->st));
+    s = run_map(c, all);
+    if (s != PSM_OK) return s;
+  }
+  return run_map(c, boxes);
+}
+
+static psm_status state_write(psm_ctx* c, const double* host, int mode) {
+  // mode 0: f [Q][N] host; 1: rho/u host (rho or u may be NULL -> defaults); 2: uniform rest
+  psm_status s = ensure_mem(c);
+  if (s != PSM_OK) return s;
+  const size_t plane = (size_t)c->grid.nx * c->grid.ny;
+  const int nvals = mode == 0 ? c->Q : 4;
+  const size_t per = plane * (size_t)nvals * 8;
+  const int64_t cap = (int64_t)(c->stage_bytes / per);  // planes in staging
+  const bool ghost = c->geom.zghost != 0;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(c->nzl, cap - 2));
+  void* arr = c->A[c->opt.pattern == PSM_TWO_ARRAY ? c->cur : 0];
+  std::vector<double> tmp;
+  for (int64_t za = 0; za < c->nzl; za += chunk) {
+    const int64_t zb = std::min<int64_t>(c->nzl, za + chunk);
+    StateParams p{};
+    p.g = c->geom;
+    p.A = arr;
+    p.stage = c->stage;
+    p.za = (int)za;
+    p.zb = (int)zb;
+    p.pattern = c->opt.pattern == PSM_AA ? 1 : 0;
+    p.mode = mode;
+    p.ghosts = ghost ? 1 : 0;
+    if (mode != 2) {
+      // staging planes cover the readers of slots in [za, zb): local planes [za-1, zb+1)
+      int64_t s0 = za - 1, s1 = zb + 1;
+      if (ghost || c->opt.pattern == PSM_AA) {
+        s0 = std::max<int64_t>(0, s0);
+        s1 = std::min<int64_t>(c->nzl, s1);
+      }
+      if (!ghost && c->opt.pattern != PSM_AA && c->grid.bc[2] == PSM_WALL) {
+        s0 = std::max<int64_t>(0, s0);
+        s1 = std::min<int64_t>(c->nzl, s1);
+      }
+      int64_t ns = s1 - s0;
+      if (ns > c->nzl) {  // small periodic grid: the whole slab once
+        s0 = 0;
+        ns = c->nzl;
+      }
+      p.stage_z0 = (int)s0;
+      p.stage_nz = (int)ns;
+      // gather host planes (wrapped) into a contiguous pinned-free host buffer, then H2D
+      tmp.assign((size_t)(ns * plane * nvals), 0.0);
+      const size_t N = (size_t)c->nzl * plane;
+      if (mode == 0)
+        for (int v = 0; v < nvals; ++v)
+          for (int64_t k = 0; k < ns; ++k) {
+            const int64_t zl = ((s0 + k) % c->nzl + c->nzl) % c->nzl;
+            std::memcpy(&tmp[((size_t)v * ns + k) * plane], host + (size_t)v * N + (size_t)zl * plane,
+                        plane * 8);
+          }
+      if (mode == 1) {
+        // host points to a 2-element array {rho, u} packed by the caller
+        const double* const* ru = reinterpret_cast<const double* const*>(host);
+        for (int64_t k = 0; k < ns; ++k) {
+          const int64_t zl = ((s0 + k) % c->nzl + c->nzl) % c->nzl;
+          for (size_t i = 0; i < plane; ++i) {
+            const size_t src = (size_t)zl * plane + i;
+            tmp[((size_t)0 * ns + k) * plane + i] = ru[0] ? ru[0][src] : 1.0;
+            for (int a = 0; a < 3; ++a)
+              tmp[((size_t)(a + 1) * ns + k) * plane + i] = ru[1] ? ru[1][a * N + src] : 0.0;
+          }
+        }
+      }
+      CUDA_TRY(c, cudaMemcpyAsync(c->stage, tmp.data(), tmp.size() * 8, cudaMemcpyHostToDevice,
+                                  c->st));
+    }
+    CUDA_TRY(c, launch_write_state(c->Q, c->opt.prec == PSM_F64, p, c->st));
+    c->launches += 1;
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));  // tmp is reused by the next chunk
+  }
+  c->step = 0;
+  c->ft_valid = false;
+  return PSM_OK;
+}
+
+static psm_status state_read(psm_ctx* c, double* f, double* rho, double* u) {
+  psm_status s = ensure_mem(c);
+  if (s != PSM_OK) return s;
+  const size_t plane = (size_t)c->grid.nx * c->grid.ny;
+  const int mode = f ? 0 : 1;
+  const int nvals = mode == 0 ? c->Q : 4;
+  const size_t per = plane * (size_t)nvals * 8;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(c->nzl,
+                                                              (int64_t)(c->stage_bytes / per)));
+  const void* arr = (c->opt.pattern == PSM_TWO_ARRAY) ? c->A[c->cur] : c->A[0];
+  const size_t N = (size_t)c->nzl * plane;
+  std::vector<double> tmp;
+  for (int64_t za = 0; za < c->nzl; za += chunk) {
+    const int64_t zb = std::min<int64_t>(c->nzl, za + chunk);
+    StateParams p{};
+    p.g = c->geom;
+    p.A = const_cast<void*>(arr);
+    p.stage = c->stage;
+    p.za = (int)za;
+    p.zb = (int)zb;
+    p.stage_z0 = (int)za;
+    p.stage_nz = (int)(zb - za);
+    p.pattern = c->opt.pattern == PSM_AA ? 1 : 0;
+    p.odd = (int)(c->step & 1);
+    p.mode = mode;
+    CUDA_TRY(c, launch_read_state(c->Q, c->opt.prec == PSM_F64, p, c->st));
+    c->launches += 1;
+    const size_t nz = (size_t)(zb - za);
+    tmp.resize(nz * plane * nvals);
+    CUDA_TRY(c, cudaMemcpyAsync(tmp.data(), c->stage, tmp.size() * 8, cudaMemcpyDeviceToHost,
+                                c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    for (int v = 0; v < nvals; ++v) {
+      const double* src = &tmp[(size_t)v * nz * plane];
+      if (mode == 0) {
+        std::memcpy(f + (size_t)v * N + (size_t)za * plane, src, nz * plane * 8);
+      } else if (v == 0) {
+        if (rho) std::memcpy(rho + (size_t)za * plane, src, nz * plane * 8);
+      } else if (u) {
+        std::memcpy(u + (size_t)(v - 1) * N + (size_t)za * plane, src, nz * plane * 8);
+      }
+    }
+  }
+  return PSM_OK;
+}
+
+// ----------------------------------------------------------------------------- ABI --------
+extern "C" {
+
+psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
+                      const psm_options* opt, psm_ctx** out) {
+  if (!grid || !opt || !out) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null argument");
+  *out = nullptr;
+  if (!(tau > 0.5) || !std::isfinite(tau))
+    FAIL((psm_ctx*)nullptr, PSM_E_ARG, "tau must be finite and > 1/2 (Eq.(2): nu = (tau-1/2)/3)");
+  if (stencil != PSM_D3Q19 && stencil != PSM_D3Q27)
+    FAIL((psm_ctx*)nullptr, PSM_E_ARG, "stencil must be 19 or 27");
+  if (grid->nx < 1 || grid->ny < 1 || grid->nz < 1)
+    FAIL((psm_ctx*)nullptr, PSM_E_ARG, "grid extents must be >= 1");
+  for (int a = 0; a < 3; ++a)
+    if (grid->bc[a] != PSM_PERIODIC && grid->bc[a] != PSM_WALL)
+      FAIL((psm_ctx*)nullptr, PSM_E_ARG, "bad boundary kind");
+  if ((opt->prec != PSM_F64 && opt->prec != PSM_F32) ||
+      (opt->pattern != PSM_TWO_ARRAY && opt->pattern != PSM_AA) || opt->sc < 1 || opt->sc > 3 ||
+      (opt->bmode != PSM_B_DIRECT && opt->bmode != PSM_B_WEIGHTED))
+    FAIL((psm_ctx*)nullptr, PSM_E_ARG, "bad option enum");
+  const int world = opt->world < 1 ? 1 : opt->world;
+  if (opt->rank < 0 || opt->rank >= world) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "bad rank");
+  if (grid->nz < world) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "nz < world");
+  const bool force = opt->body_force[0] != 0.0 || opt->body_force[1] != 0.0 ||
+                     opt->body_force[2] != 0.0;
+  if (force && opt->pattern == PSM_AA)
+    FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "body force needs PSM_TWO_ARRAY");
+  if (world > 1 && opt->pattern == PSM_AA)
+    FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "multi-rank runs need PSM_TWO_ARRAY");
+  if (world > 1 && !opt->nccl_unique_id)
+    FAIL((psm_ctx*)nullptr, PSM_E_ARG, "world > 1 needs an ncclUniqueId");
+  psm_ctx* c = new (std::nothrow) psm_ctx();
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_OOM, "host allocation failed");
+  c->grid = *grid;
+  c->Q = (int)stencil;
+  c->tau = tau;
+  c->opt = *opt;
+  c->rank = opt->rank;
+  c->world = world;
+  c->S = opt->prec == PSM_F64 ? 8 : 4;
+  c->z0 = (grid->nz * c->rank) / world;
+  c->nzl = (grid->nz * (c->rank + 1)) / world - c->z0;
+  c->st = static_cast<cudaStream_t>(opt->cuda_stream);
+  Geom& g = c->geom;
+  g.nx = (int)grid->nx;
+  g.ny = (int)grid->ny;
+  g.nzl = (int)c->nzl;
+  g.nz_global = (int)grid->nz;
+  g.z0 = (int)c->z0;
+  g.zghost = world > 1 ? 1 : 0;
+  for (int a = 0; a < 3; ++a) g.wall[a] = grid->bc[a] == PSM_WALL;
+  g.qstride = (long long)(c->nzl + 2 * g.zghost) * grid->ny * grid->nx;
+  g.gx = (int)((grid->nx + kTileX - 1) / kTileX);
+  g.gy = (int)((grid->ny + kTileY - 1) / kTileY);
+  g.gz = (int)((c->nzl + kTileZ - 1) / kTileZ);
+  if (g.qstride >= (1ll << 31) || grid->nx >= (1 << 30) || grid->ny > 65535 * kTileY ||
+      c->nzl > 65535 * kTileZ) {
+    delete c;
+    FAIL((psm_ctx*)nullptr, PSM_E_ARG, "local slab too large for 32-bit in-plane indexing");
+  }
+  c->ncell_local = (int64_t)c->nzl * grid->ny * grid->nx;
+  c->ntiles = (int64_t)g.gx * g.gy * g.gz;
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, opt->nccl_unique_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, c->rank);
+    if (r != ncclSuccess) {
+      std::string m = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      delete c;
+      FAIL((psm_ctx*)nullptr, PSM_E_NCCL, m);
+    }
+  }
+  *out = c;
+  return PSM_OK;
+}
+
+psm_status psm_destroy(psm_ctx* c) {
+  if (!c) return PSM_OK;
+  cudaStreamSynchronize(c->st);
+  for (int id = 0; id <= kMaxBodies; ++id) {
+    cudaFree(c->bodies[id].d_bits);
+    cudaFree(c->bodies[id].d_mask);
+  }
+  cudaFree(c->dbg_B);
+  cudaFree(c->dbg_us);
+  cudaFree(c->dbg_id);
+  if (c->own_mem) cudaFree(c->mem);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  for (int ph = 0; ph < PSM_NUM_PHASES; ++ph)
+    for (auto& e : c->ev[ph]) {
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+  return PSM_OK;
+}
+
+psm_status psm_required_bytes(const psm_ctx* c, size_t* bytes) {
+  if (!c || !bytes) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null argument");
+  *bytes = make_plan(c).total;
+  return PSM_OK;
+}
+
+psm_status psm_bind_memory(psm_ctx* c, void* dev_ptr, size_t bytes) {
+  if (!c || !dev_ptr) FAIL(c, PSM_E_ARG, "null argument");
+  if (c->bound) FAIL(c, PSM_E_STATE, "memory already bound");
+  if (reinterpret_cast<uintptr_t>(dev_ptr) & 255) FAIL(c, PSM_E_ARG, "dev_ptr not 256-aligned");
+  return bind(c, dev_ptr, bytes);
+}
+
+psm_status psm_local_extent(const psm_ctx* c, int64_t* z0, int64_t* nz_local) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  if (z0) *z0 = c->z0;
+  if (nz_local) *nz_local = c->nzl;
+  return PSM_OK;
+}
+
+psm_status psm_init_equilibrium(psm_ctx* c, const double* rho, const double* u) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  if (!rho && !u) return state_write(c, nullptr, 2);
+  const double* ru[2] = {rho, u};
+  return state_write(c, reinterpret_cast<const double*>(ru), 1);
+}
+
+psm_status psm_write_pdfs(psm_ctx* c, const double* f) {
+  if (!c || !f) FAIL(c, PSM_E_ARG, "null argument");
+  return state_write(c, f, 0);
+}
+
+psm_status psm_read_pdfs(psm_ctx* c, double* f) {
+  if (!c || !f) FAIL(c, PSM_E_ARG, "null argument");
+  return state_read(c, f, nullptr, nullptr);
+}
+
+psm_status psm_read_velocity(psm_ctx* c, double* rho, double* u) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  if (!rho && !u) return PSM_OK;
+  return state_read(c, nullptr, rho, u);
+}
+
+psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const psm_pose* pose,
+                        const psm_velocity* vel) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  if (id < 1 || id > kMaxBodies) FAIL(c, PSM_E_ARG, "body id must be in 1..16");
+  psm_status st = ensure_mem(c);
+  if (st != PSM_OK) return st;
+  Body& b = c->bodies[id];
+  if (!shape && !b.present) FAIL(c, PSM_E_ARG, "new body needs a shape");
+  if (!pose) FAIL(c, PSM_E_ARG, "pose required");
+  // pose validation: orthonormal, det = +1
+  const double* Q = pose->Q;
+  double dev = 0.0;
+  for (int r = 0; r < 3; ++r)
+    for (int cc = 0; cc < 3; ++cc) {
+      double acc = 0.0;
+      for (int l = 0; l < 3; ++l) acc += Q[3 * l + r] * Q[3 * l + cc];
+      dev = std::max(dev, std::fabs(acc - (r == cc ? 1.0 : 0.0)));
+    }
+  const double det = Q[0] * (Q[4] * Q[8] - Q[5] * Q[7]) - Q[1] * (Q[3] * Q[8] - Q[5] * Q[6]) +
+                     Q[2] * (Q[3] * Q[7] - Q[4] * Q[6]);
+  if (!(dev <= 1e-9) || !(det > 0.0)) FAIL(c, PSM_E_POSE, "pose matrix is not a rotation");
+  for (int a = 0; a < 3; ++a)
+    if (!std::isfinite(pose->t[a])) FAIL(c, PSM_E_POSE, "non-finite translation");
+  if (shape) {
+    if (shape->s < 0 || shape->s > 3) FAIL(c, PSM_E_ARG, "s must be in 0..3");
+    Body nb;
+    nb.kind = shape->kind;
+    nb.s = shape->s;
+    if (shape->kind == PSM_SPHERE) {
+      if (!(shape->radius > 0.0) || !std::isfinite(shape->radius))
+        FAIL(c, PSM_E_ARG, "sphere radius must be > 0");
+      nb.radius = shape->radius;
+      nb.rbound = shape->radius;
+    } else if (shape->kind == PSM_MESH) {
+      std::string why;
+      if (!shape->verts || !shape->tris ||
+          check_mesh(shape->verts, shape->nverts, shape->tris, shape->ntris, &why) != 0)
+        FAIL(c, PSM_E_MESH, why.empty() ? std::string("null mesh arrays") : why);
+      geometry_extent(shape->verts, shape->nverts, shape->s, nb.o, nb.dims);
+      const double bits = (double)nb.dims[0] * nb.dims[1] * nb.dims[2] * std::ldexp(1.0, 3 * shape->s);
+      if (bits / 8.0 > (double)kGeomCapBytes)
+        FAIL(c, PSM_E_OOM, "geometry field exceeds the 1 GiB cap (reduce s)");
+      double rb = 0.0;
+      for (int64_t k = 0; k < shape->nverts; ++k) {
+        const double* v = shape->verts + 3 * k;
+        rb = std::max(rb, std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]));
+      }
+      nb.rbound = rb;
+      std::vector<uint8_t> field, mask;
+      std::vector<unsigned long long> words;
+      voxelize_mesh(shape->verts, shape->nverts, shape->tris, shape->ntris, shape->s, nb.o,
+                    nb.dims, field);
+      pack_bricks(field, shape->s, nb.dims, words, mask, &nb.words);
+      CUDA_TRY(c, cudaMalloc(&nb.d_bits, words.size() * 8));
+      CUDA_TRY(c, cudaMalloc(&nb.d_mask, mask.size()));
+      CUDA_TRY(c, cudaMemcpy(nb.d_bits, words.data(), words.size() * 8, cudaMemcpyHostToDevice));
+      CUDA_TRY(c, cudaMemcpy(nb.d_mask, mask.data(), mask.size(), cudaMemcpyHostToDevice));
+    } else {
+      FAIL(c, PSM_E_ARG, "unknown shape kind");
+    }
+    for (int a = 0; a < 3; ++a)
+      if (c->grid.bc[a] == PSM_PERIODIC && nb.rbound + 1.0 >= 0.5 * extent(c, a))
+        FAIL(c, PSM_E_ARG, "body bounding radius + 1 must be < half a periodic extent");
+    // keep the previous mapped box so the old footprint gets cleared
+    nb.has_box = b.has_box;
+    for (int a = 0; a < 3; ++a) {
+      nb.box_lo[a] = b.box_lo[a];
+      nb.box_hi[a] = b.box_hi[a];
+    }
+    cudaStreamSynchronize(c->st);
+    cudaFree(b.d_bits);
+    cudaFree(b.d_mask);
+    b = nb;
+  }
+  b.present = true;
+  std::memcpy(b.Q0, pose->Q, sizeof(b.Q0));
+  std::memcpy(b.t0, pose->t, sizeof(b.t0));
+  for (int a = 0; a < 3; ++a) {
+    b.v[a] = vel ? vel->v[a] : 0.0;
+    b.w[a] = vel ? vel->omega[a] : 0.0;
+  }
+  b.moving = false;
+  for (int a = 0; a < 3; ++a)
+    if (b.v[a] != 0.0 || b.w[a] != 0.0) b.moving = true;
+  b.step0 = c->step;
+  c->ft_valid = false;
+  return remap(c, std::vector<int>{id}, c->step);
+}
+
+psm_status psm_remove_body(psm_ctx* c, int32_t id) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  if (id < 1 || id > kMaxBodies) FAIL(c, PSM_E_ARG, "body id must be in 1..16");
+  Body& b = c->bodies[id];
+  if (!b.present) return PSM_OK;
+  std::vector<Box> boxes;
+  if (b.has_box) add_box(c, b.box_lo, b.box_hi, boxes);
+  cudaStreamSynchronize(c->st);
+  cudaFree(b.d_bits);
+  cudaFree(b.d_mask);
+  b = Body();
+  return run_map(c, boxes);
+}
+
+psm_status psm_map_fractions(psm_ctx* c) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  psm_status st = ensure_mem(c);
+  if (st != PSM_OK) return st;
+  std::vector<int> ids;
+  for (int id = 1; id <= kMaxBodies; ++id)
+    if (c->bodies[id].present) ids.push_back(id);
+  return remap(c, ids, c->step);
+}
+
+psm_status psm_step(psm_ctx* c, int64_t n) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  if (n < 0) FAIL(c, PSM_E_ARG, "n < 0");
+  psm_status st = ensure_mem(c);
+  if (st != PSM_OK) return st;
+  if (n == 0) return PSM_OK;
+  const bool fp64 = c->opt.prec == PSM_F64;
+  const bool force = c->opt.body_force[0] != 0.0 || c->opt.body_force[1] != 0.0 ||
+                     c->opt.body_force[2] != 0.0;
+  CollideParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.g = c->geom;
+  p.word = c->word;
+  p.tile_flag = c->tile_flag;
+  p.partial = c->partial;
+  p.overflow = c->overflow;
+  p.err = c->err;
+  p.dbg_B = c->dbg_B;
+  p.dbg_us = c->dbg_us;
+  p.dbg_id = c->dbg_id;
+  p.tau = c->tau;
+  p.omega = 1.0 / c->tau;
+  for (int a = 0; a < 3; ++a) p.gforce[a] = c->opt.body_force[a];
+  p.sc = c->opt.sc;
+  p.bmode = c->opt.bmode;
+  CUDA_TRY(c, cudaMemsetAsync(c->overflow, 0, (kMaxBodies + 1) * kSlotVals * 8, c->st));
+  for (int64_t k = 0; k < n; ++k) {
+    // 1. closed-form pose advance + remap of the bodies that moved
+    std::vector<int> moved;
+    for (int id = 1; id <= kMaxBodies; ++id) {
+      const Body& b = c->bodies[id];
+      if (b.present && b.moving && b.mapped_step != c->step) moved.push_back(id);
+    }
+    if (!moved.empty() && !c->dbg) {
+      st = remap(c, moved, c->step);
+      if (st != PSM_OK) return st;
+    }
+    // 2. fused PSM stream-collide (Eq.(4)) + F/T partials
+    if (k == n - 1)
+      CUDA_TRY(c, cudaMemsetAsync(c->overflow, 0, (kMaxBodies + 1) * kSlotVals * 8, c->st));
+    fill_kin(c, p, c->step);
+    p.step = c->step;
+    int pat = 0;
+    if (c->opt.pattern == PSM_TWO_ARRAY) {
+      p.src = c->A[c->cur];
+      p.dst = c->A[c->cur ^ 1];
+    } else {
+      p.src = c->A[0];
+      p.dst = c->A[0];
+      pat = (c->step & 1) ? 2 : 1;
+    }
+    if (record(c, 1, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+    CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, c->st));
+    c->launches += 1;
+    if (record(c, 1, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+    if (c->opt.pattern == PSM_TWO_ARRAY) c->cur ^= 1;
+    // 3. halo exchange of the freshly written array (world > 1)
+    st = halo(c, c->opt.pattern == PSM_TWO_ARRAY ? c->A[c->cur] : c->A[0]);
+    if (st != PSM_OK) return st;
+    c->step += 1;
+  }
+  // 4. force/torque of the last step: deterministic two-pass reduction, then allreduce
+  std::vector<int> ids;
+  for (int id = 1; id <= kMaxBodies; ++id)
+    if (c->bodies[id].present) ids.push_back(id);
+  if (c->dbg) {
+    ids.clear();
+    for (int id = 1; id <= kMaxBodies; ++id) ids.push_back(id);
+  }
+  const int nb = (int)ids.size();
+  if (record(c, 2, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+  if (nb > 0) {
+    int* hid = reinterpret_cast<int*>(c->pinned + kMaxBodies * kSlotVals);
+    for (int i = 0; i < nb; ++i) hid[i] = ids[i];
+    CUDA_TRY(c, cudaMemcpyAsync(c->ft_ids, hid, nb * 4, cudaMemcpyHostToDevice, c->st));
+    CUDA_TRY(c, launch_ft_reduce(c->tile_flag, c->partial, (int)c->ntiles, c->overflow,
+                                 c->ft_ids, nb, c->ft_scratch, kFtChunks, c->ft_out, c->st));
+    c->launches += 2;
+    if (c->world > 1)
+      NCCL_TRY(c, ncclAllReduce(c->ft_out, c->ft_out, (size_t)nb * kSlotVals, ncclFloat64,
+                                ncclSum, c->comm, c->st));
+    CUDA_TRY(c, cudaMemcpyAsync(c->pinned, c->ft_out, (size_t)nb * kSlotVals * 8,
+                                cudaMemcpyDeviceToHost, c->st));
+  }
+  if (record(c, 2, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+  unsigned long long* herr =
+      reinterpret_cast<unsigned long long*>(c->pinned + (kMaxBodies + 1) * kSlotVals);
+  CUDA_TRY(c, cudaMemcpyAsync(herr, c->err, 8, cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  std::memset(c->ft, 0, sizeof(c->ft));
+  for (int i = 0; i < nb; ++i)
+    std::memcpy(c->ft[ids[i]], c->pinned + (size_t)i * kSlotVals, kSlotVals * 8);
+  c->ft_valid = true;
+  if (*herr != ~0ull) {
+    const long long ncell = (long long)c->grid.nx * c->grid.ny * c->grid.nz;
+    const long long stp = (long long)(*herr / (unsigned long long)ncell);
+    const long long cell = (long long)(*herr % (unsigned long long)ncell);
+    const long long x = cell % c->grid.nx, y = (cell / c->grid.nx) % c->grid.ny,
+                    z = cell / (c->grid.nx * c->grid.ny);
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "invalid state (rho <= 0 or non-finite) at step %lld, cell "
+                  "(%lld,%lld,%lld)", stp, x, y, z);
+    CUDA_TRY(c, cudaMemsetAsync(c->err, 0xFF, 8, c->st));
+    FAIL(c, PSM_E_STATE, buf);
+  }
+  return PSM_OK;
+}
+
+psm_status psm_force_torque(psm_ctx* c, int32_t id, double F[3], double T[3], double aF[3],
+                            double aT[3]) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  if (id < 1 || id > kMaxBodies) FAIL(c, PSM_E_ARG, "body id must be in 1..16");
+  if (!c->ft_valid) FAIL(c, PSM_E_STATE, "no step has run since the last state change");
+  // the partials hold the momentum the fluid gains (printed Eqs.(10)-(11)); on the body: minus
+  for (int a = 0; a < 3; ++a) {
+    if (F) F[a] = -c->ft[id][a];
+    if (T) T[a] = -c->ft[id][3 + a];
+    if (aF) aF[a] = c->ft[id][6 + a];
+    if (aT) aT[a] = c->ft[id][9 + a];
+  }
+  return PSM_OK;
+}
+
+psm_status psm_read_fractions(psm_ctx* c, double* B, uint8_t* id, int32_t* cnt) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  psm_status st = ensure_mem(c);
+  if (st != PSM_OK) return st;
+  const size_t plane = (size_t)c->grid.nx * c->grid.ny;
+  const size_t per = plane * (8 + 1 + 4);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(c->nzl,
+                                                              (int64_t)(c->stage_bytes / per)));
+  for (int64_t za = 0; za < c->nzl; za += chunk) {
+    const int64_t zb = std::min<int64_t>(c->nzl, za + chunk);
+    const size_t nz = (size_t)(zb - za);
+    FracParams p{};
+    p.g = c->geom;
+    p.word = c->word;
+    p.B = c->stage;
+    p.cnt = reinterpret_cast<int32_t*>(c->stage + nz * plane);
+    p.id = reinterpret_cast<uint8_t*>(p.cnt + nz * plane);
+    p.za = (int)za;
+    p.zb = (int)zb;
+    p.tau = c->tau;
+    p.bmode = c->opt.bmode;
+    for (int i = 0; i <= kMaxBodies; ++i) p.s[i] = c->bodies[i].s;
+    CUDA_TRY(c, launch_read_fractions(p, c->st));
+    c->launches += 1;
+    if (B)
+      CUDA_TRY(c, cudaMemcpyAsync(B + za * plane, p.B, nz * plane * 8, cudaMemcpyDeviceToHost,
+                                  c->st));
+    if (cnt)
+      CUDA_TRY(c, cudaMemcpyAsync(cnt + za * plane, p.cnt, nz * plane * 4,
+                                  cudaMemcpyDeviceToHost, c->st));
+    if (id)
+      CUDA_TRY(c, cudaMemcpyAsync(id + za * plane, p.id, nz * plane, cudaMemcpyDeviceToHost,
+                                  c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  }
+  return PSM_OK;
+}
+
+psm_status psm_debug_set_fields(psm_ctx* c, const double* B, const double* us,
+                                const uint8_t* id) {
+  if (!c || !B || !us || !id) FAIL(c, PSM_E_ARG, "null argument");
+  if (c->opt.pattern != PSM_TWO_ARRAY) FAIL(c, PSM_E_UNSUPPORTED, "debug fields need TWO_ARRAY");
+  psm_status st = ensure_mem(c);
+  if (st != PSM_OK) return st;
+  const size_t N = (size_t)c->ncell_local;
+  if (!c->dbg_B) {
+    CUDA_TRY(c, cudaMalloc(&c->dbg_B, N * 8));
+    CUDA_TRY(c, cudaMalloc(&c->dbg_us, 3 * N * 8));
+    CUDA_TRY(c, cudaMalloc(&c->dbg_id, N));
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->dbg_B, B, N * 8, cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->dbg_us, us, 3 * N * 8, cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->dbg_id, id, N, cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 1, (size_t)c->ntiles, c->st));
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  c->dbg = true;
+  return PSM_OK;
+}
+
+psm_status psm_get_step(const psm_ctx* c, int64_t* step) {
+  if (!c || !step) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null argument");
+  *step = c->step;
+  return PSM_OK;
+}
+
+psm_status psm_launch_count(const psm_ctx* c, int64_t* launches) {
+  if (!c || !launches) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null argument");
+  *launches = c->launches;
+  return PSM_OK;
+}
+
+psm_status psm_profile(psm_ctx* c, int32_t enable) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  c->prof = enable != 0;
+  return PSM_OK;
+}
+
+psm_status psm_profile_read(psm_ctx* c, double ms[PSM_NUM_PHASES],
+                            int64_t count[PSM_NUM_PHASES]) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  for (int ph = 0; ph < PSM_NUM_PHASES; ++ph) {
+    for (auto& e : c->ev[ph]) {
+      float t = 0.f;
+      CUDA_TRY(c, cudaEventElapsedTime(&t, e[0], e[1]));
+      c->prof_ms[ph] += t;
+      c->prof_cnt[ph] += 1;
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+    c->ev[ph].clear();
+    if (ms) ms[ph] = c->prof_ms[ph];
+    if (count) count[ph] = c->prof_cnt[ph];
+    c->prof_ms[ph] = 0.0;
+    c->prof_cnt[ph] = 0;
+  }
+  return PSM_OK;
+}
+
+int32_t psm_nccl_id_bytes(void) { return (int32_t)sizeof(ncclUniqueId); }
+
+psm_status psm_nccl_get_unique_id(void* out128) {
+  if (!out128) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null argument");
+  ncclUniqueId id;
+  NCCL_TRY((psm_ctx*)nullptr, ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  return PSM_OK;
+}
+
+const char* psm_last_error(const psm_ctx* c) {
+  if (c) return c->err_msg.c_str();
+  return g_last_error.c_str();
+}
+
+}  // extern "C"

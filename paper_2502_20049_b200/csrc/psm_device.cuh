@@ -1,0 +1,134 @@
+// psm_device.cuh — device-side definitions of the B200 PSM hot path (arXiv 2502.20049).
+//
+// Stencils, storage layout and kernel parameter blocks shared by the .cu files of the product
+// library.  Nothing here is shared with oracle/ (which has its own tables and arithmetic).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace psm {
+
+constexpr int kMaxBodies = 16;   // PSM_MAX_BODIES
+constexpr int kTileX = 32;       // one warp along x (coalesced SoA rows)
+constexpr int kTileY = 4;
+constexpr int kTileZ = 2;
+constexpr int kTileCells = kTileX * kTileY * kTileZ;  // 256 threads = one collide/map block
+constexpr int kMaxBoxes = 64;    // remap boxes per launch
+constexpr int kSlotVals = 12;    // F/T partial: m[3], (x_c-R) x m [3], |m| [3], |(x_c-R) x m| [3]
+
+// ------------------------------------------------------------------------------ stencils ----
+// Direction order of DESIGN.md §2.1 (lbmpy/waLBerla convention; PAPER.md:233 names the sets).
+__host__ __device__ constexpr int stc_x(int i) {
+  constexpr int t[27] = {0, 0, 0, -1, 1, 0, 0, -1, 1, -1, 1, 0, 0, -1, 1, 0, 0, -1, 1,
+                         1, -1, 1, -1, 1, -1, 1, -1};
+  return t[i];
+}
+__host__ __device__ constexpr int stc_y(int i) {
+  constexpr int t[27] = {0, 1, -1, 0, 0, 0, 0, 1, 1, -1, -1, 1, -1, 0, 0, 1, -1, 0, 0,
+                         1, 1, -1, -1, 1, 1, -1, -1};
+  return t[i];
+}
+__host__ __device__ constexpr int stc_z(int i) {
+  constexpr int t[27] = {0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, 1, 1, 1, -1, -1, -1, -1,
+                         1, 1, 1, 1, -1, -1, -1, -1};
+  return t[i];
+}
+// opposite direction index (c_opp = -c)
+__host__ __device__ constexpr int stc_opp(int i) {
+  constexpr int t[27] = {0, 2, 1, 4, 3, 6, 5, 10, 9, 8, 7, 16, 15, 18, 17, 12, 11, 14, 13,
+                         26, 25, 24, 23, 22, 21, 20, 19};
+  return t[i];
+}
+// weights: D3Q19 1/3, 1/18, 1/36; D3Q27 8/27, 2/27, 1/54, 1/216
+template <int Q>
+__host__ __device__ constexpr double stc_w(int i) {
+  int n = (stc_x(i) != 0) + (stc_y(i) != 0) + (stc_z(i) != 0);
+  if (Q == 19) return n == 0 ? 1.0 / 3.0 : (n == 1 ? 1.0 / 18.0 : 1.0 / 36.0);
+  return n == 0 ? 8.0 / 27.0 : (n == 1 ? 2.0 / 27.0 : (n == 2 ? 1.0 / 54.0 : 1.0 / 216.0));
+}
+
+// ------------------------------------------------------------------------- body tables -----
+// What the collide kernel needs per body: rigid velocity u_s = v + w x mi(x_c - t) and the
+// fraction weighting (s, tau-weighted or direct).
+struct BodyKin {
+  double t[3], v[3], w[3];
+  int s;        // super-sampling exponent (eps = cnt * 2^-3s)
+  int present;
+};
+
+// What the mapping kernel needs per body.
+struct BodyGeo {
+  double Q[9];      // body -> world, row major; sample maps to q = Q^T mi(p - t)
+  double t[3];
+  double rb1;       // bounding radius + 1 (conservative cell filter |mi(x_c - t)|_a <= rb1)
+  double r2;        // sphere: r*r
+  double o[3];      // mesh: geometry-field origin (body frame, integer valued)
+  int dims_b[3];    // mesh: field extent in bricks (LBM cells)
+  int kind;         // 0 sphere, 1 mesh
+  int s;
+  int words;        // uint64 words per brick = max(1, 8^s / 64)
+  int present;
+  const unsigned long long* bits;  // [brick][words]
+  const uint8_t* mask;             // [brick]: 1 dilated-all-in, 2 dilated-all-out, 0 otherwise
+};
+
+// ---------------------------------------------------------------------- launch params -----
+struct Geom {
+  int nx, ny, nzl;        // local extents
+  int nz_global;
+  int z0;                 // global z of local plane 0
+  int zghost;             // 1: ghost planes at local z = -1 and nzl (world > 1)
+  int wall[3];            // 1 = half-way bounce-back wall on this axis
+  long long qstride;      // elements between consecutive direction planes
+  int gx, gy, gz;         // tile grid
+};
+
+struct CollideParams {
+  Geom g;
+  const void* src;        // two-array: read array;   AA: the single array
+  void* dst;              // two-array: write array;  AA: same as src
+  const uint32_t* word;   // solid word per local cell: cnt | id << 16 (0 = fluid)
+  const uint8_t* tile_flag;
+  double* partial;        // [tile][2 slots][1 + kSlotVals] (slot id stored as double)
+  double* overflow;       // [kMaxBodies+1][kSlotVals] atomics for a 3rd+ body in a tile
+  unsigned long long* err;  // first (step, cell) with rho <= 0 or non-finite
+  const double* dbg_B;    // DBG: B [cell]
+  const double* dbg_us;   // DBG: u_s [3][cell]
+  const uint8_t* dbg_id;  // DBG: id [cell]
+  double tau, omega;      // omega = 1/tau
+  double gforce[3];       // test-only Guo force
+  int sc;                 // 1, 2, 3
+  int bmode;              // 0 direct, 1 weighted
+  long long step;         // for the error word
+  BodyKin bodies[kMaxBodies + 1];
+};
+
+struct MapBox {
+  int t0[3];   // first tile (local tile coords)
+  int n[3];    // tiles per axis
+  int first;   // prefix sum of tiles before this box
+};
+
+struct MapParams {
+  Geom g;
+  uint32_t* word;
+  uint8_t* tile_flag;
+  int nbox;
+  int ntiles;
+  MapBox box[kMaxBoxes];
+  BodyGeo bodies[kMaxBodies + 1];
+};
+
+#if defined(__CUDACC__)
+// minimum image on a periodic axis (same tie rule as the method definition)
+__device__ __forceinline__ double min_image(double d, double L, bool periodic) {
+  if (!periodic) return d;
+  if (d >= 0.5 * L)
+    d = __dsub_rn(d, L);
+  else if (d < -0.5 * L)
+    d = __dadd_rn(d, L);
+  return d;
+}
+#endif
+
+}  // namespace psm

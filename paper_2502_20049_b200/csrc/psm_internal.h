@@ -1,0 +1,54 @@
+// psm_internal.h — host-side launchers of the sm_100a kernels (product library only).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "psm_device.cuh"
+
+namespace psm {
+
+// k_collide.cu
+cudaError_t launch_collide(int Q, bool fp64, const CollideParams& p, int pat, bool force,
+                           bool dbg, cudaStream_t st);
+
+// k_map.cu
+cudaError_t launch_map(const MapParams& p, cudaStream_t st);
+
+// k_state.cu — conversions between the Eq.(4) state and the storage pattern, z-chunked.
+struct StateParams {
+  Geom g;
+  void* A;               // PDF storage (pattern-specific layout)
+  double* stage;         // fp64 staging buffer
+  int za, zb;            // local planes [za, zb) handled by this launch
+  int stage_z0;          // local z of staging plane 0 (write: za - 1; read: za)
+  int stage_nz;          // planes in the staging buffer
+  int pattern;           // 0 pull, 1 AA
+  int odd;               // AA: current step count is odd
+  int mode;              // write: 0 = f from stage [Q][planes], 1 = feq from rho,u stage
+                         //        [4][planes], 2 = uniform rho=1,u=0; read: 0 = f, 1 = rho,u
+  int ghosts;            // write: also fill the ghost planes adjacent to [za, zb)
+};
+cudaError_t launch_write_state(int Q, bool fp64, const StateParams& p, cudaStream_t st);
+cudaError_t launch_read_state(int Q, bool fp64, const StateParams& p, cudaStream_t st);
+
+// fractions readback: words -> B (fp64), id, cnt for local planes [za, zb)
+struct FracParams {
+  Geom g;
+  const uint32_t* word;
+  double* B;
+  uint8_t* id;
+  int32_t* cnt;
+  int za, zb;
+  double tau;
+  int bmode;
+  int s[kMaxBodies + 1];
+};
+cudaError_t launch_read_fractions(const FracParams& p, cudaStream_t st);
+
+// force/torque: two-pass deterministic reduction over the tile partials of one step
+cudaError_t launch_ft_reduce(const uint8_t* tile_flag, const double* partial, int ntiles,
+                             const double* overflow, const int* ids, int nb, double* scratch,
+                             int nchunks, double* out, cudaStream_t st);
+
+}  // namespace psm

@@ -1,0 +1,94 @@
+"""CPU checks of the C-ABI boundary: the library loads, exports every symbol include/psm.h
+declares, and host-side validation returns the documented error codes (no GPU needed: these
+calls fail before touching the device)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2502_20049_b200 as psm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "psm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(psm_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = psm.load()
+    names = _declared()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(psm.EXPORTED)
+
+
+def test_struct_layouts_match_header():
+    # psm_options: 4 int32 + 3 double + 2 int32 + 2 pointers
+    assert C.sizeof(psm.psm_grid) == 3 * 8 + 3 * 4 + 4
+    assert C.sizeof(psm.psm_options) == 16 + 24 + 8 + 16
+    assert C.sizeof(psm.psm_pose) == 12 * 8
+    assert C.sizeof(psm.psm_velocity) == 6 * 8
+    assert C.sizeof(psm.psm_shape) == 8 + 8 + 8 + 8 + 8 + 8
+    assert psm.load().psm_nccl_id_bytes() == 128
+
+
+def _opts(**kw):
+    o = dict(prec=psm.PSM_F64, pattern=psm.PSM_TWO_ARRAY, sc=1, bmode=1, rank=0, world=1)
+    o.update(kw)
+    return psm.psm_options(o["prec"], o["pattern"], o["sc"], o["bmode"],
+                           (C.c_double * 3)(*o.get("force", (0, 0, 0))), o["rank"], o["world"],
+                           None, None)
+
+
+def _grid(nx=8, ny=8, nz=8, bc=(0, 0, 0)):
+    return psm.psm_grid(nx, ny, nz, (C.c_int32 * 3)(*bc))
+
+
+@pytest.mark.parametrize("tau", [0.5, 0.2, float("nan"), float("inf")])
+def test_create_rejects_bad_tau(tau):
+    with pytest.raises(psm.PSMError) as e:
+        psm.psm_create(_grid(), 19, tau, _opts())
+    assert e.value.code == psm.PSM_E_ARG
+
+
+def test_create_validation_codes():
+    cases = [
+        (dict(), _grid(0, 8, 8), 19, psm.PSM_E_ARG),
+        (dict(), _grid(), 15, psm.PSM_E_ARG),
+        (dict(sc=4), _grid(), 19, psm.PSM_E_ARG),
+        (dict(prec=7), _grid(), 19, psm.PSM_E_ARG),
+        (dict(pattern=psm.PSM_AA, force=(1e-5, 0, 0)), _grid(), 19, psm.PSM_E_UNSUPPORTED),
+        (dict(world=2, rank=0), _grid(), 19, psm.PSM_E_UNSUPPORTED if False else psm.PSM_E_ARG),
+        (dict(world=2, rank=2), _grid(), 19, psm.PSM_E_ARG),
+        (dict(), _grid(8, 8, 8, (0, 3, 0)), 19, psm.PSM_E_ARG),
+    ]
+    for kw, g, q, code in cases:
+        with pytest.raises(psm.PSMError) as e:
+            psm.psm_create(g, q, 0.8, _opts(**kw))
+        assert e.value.code == code, (kw, e.value)
+
+
+def test_create_succeeds_host_only_and_reports_layout():
+    ctx = psm.psm_create(_grid(40, 12, 10), 19, 0.7, _opts())
+    try:
+        z0, nzl = psm.psm_local_extent(ctx)
+        assert (z0, nzl) == (0, 10)
+        nbytes = psm.psm_required_bytes(ctx)
+        # two fp64 PDF arrays dominate: 2 * 19 * N * 8
+        assert nbytes >= 2 * 19 * 40 * 12 * 10 * 8
+    finally:
+        psm.psm_destroy(ctx)
+
+
+def test_simulation_refuses_to_run_without_cuda():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        psm.Simulation(8, 8, 8)

@@ -1,0 +1,234 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star, DESIGN.md §4 P15): fp64 max|df| <= 1e-12 after 100 steps;
+force/torque |dF_a| <= 1e-10 * max(|F_a|, A_F,a) (A_F = sum |m| componentwise); fp32 vs the fp64
+oracle <= 2e-5; fractions (count, id, B) bit-exact in both precisions.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import psm_inputs as pi
+
+pytestmark = pytest.mark.gpu
+
+F64_TOL = 1e-12
+F32_TOL = 2e-5
+FT_REL = 1e-10
+
+
+def _sim(**kw):
+    import paper_2502_20049_b200 as psm
+    return psm.Simulation(**kw)
+
+
+def _ft_close(g, o, rel=FT_REL):
+    Fg, Tg, aFg, aTg = g
+    Fo, To, aFo, aTo = o
+    okF = np.all(np.abs(Fg - Fo) <= rel * np.maximum(np.abs(Fo), aFo) + 1e-300)
+    okT = np.all(np.abs(Tg - To) <= rel * np.maximum(np.abs(To), aTo) + 1e-300)
+    return okF and okT, (Fg, Fo, Tg, To, aFo, aTo)
+
+
+def _run_pair(nx, ny, nz, Q, tau, bc, sc, bmode, prec, pattern, bodies, steps, seed,
+              u0=(0.05, 0.0, 0.0), ft_every=True, force=(0.0, 0.0, 0.0)):
+    """bodies: list of dicts (id, kind, r | mesh, s, pose(k) -> (Q, t), v, w).  Explicit poses
+    are passed every step to both sides (reading A13)."""
+    shape = (nz, ny, nx)
+    rho, u = pi.perturbed_flow(shape, seed, u0=u0)
+    o = oracle.Oracle(nx, ny, nz, Q, tau, bc, sc, bmode)
+    o.set_force(force)
+    g = _sim(nx=nx, ny=ny, nz=nz, Q=Q, tau=tau, bc=bc, prec=prec, pattern=pattern, sc=sc,
+             bmode=bmode, body_force=force)
+    o.init_equilibrium(rho, u)
+    g.init_equilibrium(rho, u)
+    for b in bodies:
+        Qp, tp = b["pose"](0)
+        if b["kind"] == "sphere":
+            o.set_sphere(b["id"], b["r"], b["s"])
+            g.set_sphere(b["id"], b["r"], b["s"], Qp, tp, b.get("v", (0, 0, 0)),
+                         b.get("w", (0, 0, 0)))
+        else:
+            o.set_mesh(b["id"], b["verts"], b["tris"], b["s"])
+            g.set_mesh(b["id"], b["verts"], b["tris"], b["s"], Qp, tp, b.get("v", (0, 0, 0)),
+                       b.get("w", (0, 0, 0)))
+        o.set_pose(b["id"], Qp, tp, b.get("v", (0, 0, 0)), b.get("w", (0, 0, 0)))
+    worst_ft = 0.0
+    for k in range(steps):
+        for b in bodies:
+            Qp, tp = b["pose"](k)
+            o.set_pose(b["id"], Qp, tp, b.get("v", (0, 0, 0)), b.get("w", (0, 0, 0)))
+            if k > 0:
+                g.set_pose(b["id"], Qp, tp, b.get("v", (0, 0, 0)), b.get("w", (0, 0, 0)))
+        o.map()
+        if k == 0 or k == steps - 1:
+            Bo, ido, co, _ = o.fractions()
+            Bg, idg, cg = g.fractions()
+            assert np.array_equal(co, cg), f"count mismatch at step {k}: {(co != cg).sum()} cells"
+            assert np.array_equal(ido, idg)
+            assert np.array_equal(Bo, Bg)
+        o.step(1)
+        g.step(1)
+        if ft_every or k == steps - 1:
+            for b in bodies:
+                ok, info = _ft_close(g.force_torque(b["id"]), o.force_torque(b["id"]))
+                assert ok, (k, info)
+    return o, g
+
+
+def _static(Q=np.eye(3), t=(16.0, 16.0, 16.0)):
+    return lambda k: (Q, t)
+
+
+@pytest.mark.parametrize("sc", [1, 2, 3])
+@pytest.mark.parametrize("bmode", [0, 1])
+def test_c1_stationary_sphere_fp64_100_steps(sc, bmode):
+    """BASELINE config c1: D3Q19 fp64, 32^3 periodic, sphere r=6 at (16,16,16), tau=0.8, s=2."""
+    c = pi.CONFIGS["c1"]
+    o, g = _run_pair(32, 32, 32, 19, 0.8, (0, 0, 0), sc, bmode, "f64", "two_array",
+                     [dict(id=1, kind="sphere", r=6.0, s=2, pose=_static())], 100, c["seed"])
+    d = np.max(np.abs(o.pdfs() - g.pdfs()))
+    assert d <= F64_TOL, d
+
+
+@pytest.mark.parametrize("pattern", ["two_array", "aa"])
+@pytest.mark.parametrize("Q", [19, 27])
+def test_ragged_walls_rotating_mesh(pattern, Q):
+    """Ragged grid (not a multiple of the 32x4x2 tile), y/z walls, a rotating + translating mesh
+    body remapped every step: fp64 parity, fractions bit-exact, F/T every step."""
+    v, tr = pi.propeller_mesh(n_blades=3, scale=0.07, n_st=8, n_pts=16, hub_seg=16)
+    w = np.array([0.0, 0.0, 0.03])
+    vv = np.array([0.02, 0.0, 0.0])
+    Q0 = pi.rotation_about([1, 1, 0], 0.4)
+
+    def pose(k):
+        Qk, tk = oracle.pose_advance(Q0, [20.3, 10.6, 9.2], vv, w, k, [45, 21, 19], [1, 0, 0])
+        return Qk, tk
+
+    o, g = _run_pair(45, 21, 19, Q, 0.65, (0, 1, 1), 1, 1, "f64", pattern,
+                     [dict(id=3, kind="mesh", verts=v, tris=tr, s=1, pose=pose, v=vv, w=w)], 40,
+                     77, u0=(0.02, 0.01, 0.0))
+    d = np.max(np.abs(o.pdfs() - g.pdfs()))
+    assert d <= F64_TOL, d
+
+
+def test_c2_translating_sphere_channel_fp64_and_fp32():
+    """BASELINE config c2 geometry: 128x64x64, x periodic, y/z walls, sphere r=6 translating at
+    v=(1/32,0,0), tau=0.575, SC2, weighted B; 100 steps (explicit dyadic poses)."""
+    c = pi.CONFIGS["c2"]
+    v = np.array(c["v"])
+    body = dict(id=1, kind="sphere", r=6.0, s=2, v=v,
+                pose=lambda k: (np.eye(3), tuple(np.array(c["t"]) + k * v)))
+    o, g = _run_pair(128, 64, 64, 19, 0.575, (0, 1, 1), 2, 1, "f64", "two_array", [body], 100,
+                     c["seed"], u0=(0.0, 0.0, 0.0), ft_every=False)
+    ref = o.pdfs()
+    d = np.max(np.abs(ref - g.pdfs()))
+    assert d <= F64_TOL, d
+    # fp32 variant of the same run: <= 2e-5 against the fp64 oracle, fractions bit-exact
+    g32 = _sim(nx=128, ny=64, nz=64, Q=19, tau=0.575, bc=(0, 1, 1), prec="f32", sc=2, bmode=1)
+    rho, u = pi.perturbed_flow((64, 64, 128), c["seed"], u0=(0.0, 0.0, 0.0))
+    g32.init_equilibrium(rho, u)
+    g32.set_sphere(1, 6.0, 2, np.eye(3), c["t"], v)
+    for k in range(100):
+        if k > 0:
+            g32.set_pose(1, np.eye(3), tuple(np.array(c["t"]) + k * v), v)
+        g32.step(1)
+    d32 = np.max(np.abs(ref - g32.pdfs()))
+    assert d32 <= F32_TOL, d32
+    Bo, ido, co, _ = o.fractions()
+    assert np.array_equal(g32.fractions()[2], co)
+
+
+def test_internal_pose_advance_matches_explicit_poses():
+    """psm_step(n) advancing a translating body itself (dyadic velocity: exact poses) gives the
+    same state and fractions as feeding the poses explicitly."""
+    c = pi.CONFIGS["c2"]
+    v = np.array(c["v"])
+    a = _sim(nx=128, ny=64, nz=64, Q=19, tau=0.575, bc=(0, 1, 1), sc=2, bmode=1)
+    b = _sim(nx=128, ny=64, nz=64, Q=19, tau=0.575, bc=(0, 1, 1), sc=2, bmode=1)
+    for s in (a, b):
+        s.init_equilibrium()
+        s.set_sphere(1, 6.0, 2, np.eye(3), c["t"], v)
+    a.step(40)
+    for k in range(40):
+        if k > 0:
+            b.set_pose(1, np.eye(3), tuple(np.array(c["t"]) + k * v), v)
+        b.step(1)
+    assert np.array_equal(a.pdfs(), b.pdfs())
+    assert a.step_count == 40
+    fa, fb = a.force_torque(1), b.force_torque(1)
+    assert np.array_equal(fa[0], fb[0])
+
+
+@pytest.mark.parametrize("Q", [19, 27])
+def test_two_array_and_aa_give_the_same_state(Q):
+    v, tr = pi.propeller_mesh(n_blades=4, scale=0.08, n_st=8, n_pts=16, hub_seg=16)
+    w = (0.02, -0.01, 0.0)
+    runs = []
+    for pattern in ("two_array", "aa"):
+        s = _sim(nx=48, ny=40, nz=36, Q=Q, tau=0.7, bc=(0, 0, 0), pattern=pattern, sc=1)
+        rho, u = pi.perturbed_flow((36, 40, 48), 5)
+        s.init_equilibrium(rho, u)
+        s.set_mesh(2, v, tr, 1, np.eye(3), (24.0, 20.0, 18.0), (0.01, 0, 0), w)
+        for n in (1, 6, 10):  # odd and even step counts
+            s.step(n)
+        runs.append((s.pdfs(), s.force_torque(2)))
+    d = np.max(np.abs(runs[0][0] - runs[1][0]))
+    assert d <= 1e-15, d
+    assert np.allclose(runs[0][1][0], runs[1][1][0], rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("sc", [1, 2, 3])
+def test_debug_fields_random_B(sc):
+    """Random B in [0,1] and u_s through psm_debug_set_fields (P4 on the GPU)."""
+    shape = (11, 9, 37)
+    n = int(np.prod(shape))
+    rho, u = pi.perturbed_flow(shape, 21)
+    B = pi.random_unit(22, n).reshape(shape)
+    B[B < 0.3] = 0.0
+    us = 0.05 * pi.uniform_pm1(23, 3 * n).reshape((3,) + shape)
+    bid = np.where(B > 0, 1 + (np.arange(n).reshape(shape) % 3), 0).astype(np.uint8)
+    o = oracle.Oracle(37, 9, 11, 19, 0.9, (0, 0, 0), sc, 1)
+    g = _sim(nx=37, ny=9, nz=11, Q=19, tau=0.9, sc=sc, bmode=1)
+    o.init_equilibrium(rho, u)
+    g.init_equilibrium(rho, u)
+    o.set_fields(B, us, bid)
+    g.debug_set_fields(B, us, bid)
+    for _ in range(5):
+        o.step(1)
+        g.step(1)
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+    for b in (1, 2, 3):
+        ok, info = _ft_close(g.force_torque(b), o.force_torque(b))
+        assert ok, info
+
+
+def test_body_force_with_sphere_and_walls():
+    g0 = (2e-5, 1e-6, 0.0)
+    body = dict(id=1, kind="sphere", r=4.0, s=1, pose=_static(t=(12.0, 10.0, 8.0)))
+    o, g = _run_pair(24, 20, 16, 19, 0.8, (0, 1, 0), 2, 1, "f64", "two_array", [body], 60, 9,
+                     u0=(0.0, 0.0, 0.0), force=g0)
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+
+
+def test_error_word_reports_invalid_state():
+    import paper_2502_20049_b200 as psm
+    s = _sim(nx=32, ny=8, nz=8)
+    f = np.broadcast_to(oracle.stencil(19)[1][:, None, None, None], (19, 8, 8, 32)).copy()
+    f[:, 3, 2, 5] = -1.0  # rho < 0 at cell (5, 2, 3)
+    s.write_pdfs(f)
+    with pytest.raises(psm.PSMError) as e:
+        s.step(1)
+    assert e.value.code == psm.PSM_E_STATE
+    assert "(5,2,3)" in str(e.value)
+
+
+def test_write_read_roundtrip_and_equilibrium():
+    s = _sim(nx=35, ny=6, nz=5, bc=(0, 1, 1), Q=27)
+    f = pi.random_pdfs(27, (5, 6, 35), 3, w=oracle.stencil(27)[1])
+    s.write_pdfs(f)
+    assert np.array_equal(s.pdfs(), f)
+    rho, u = pi.perturbed_flow((5, 6, 35), 4)
+    s.init_equilibrium(rho, u)
+    r2, u2 = s.velocity()
+    assert np.allclose(r2, rho, atol=1e-14) and np.allclose(u2, u, atol=1e-14)
