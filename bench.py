@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 PSM hot path (arXiv 2502.20049): MLUPS and % of the HBM roofline.
+
+Default workload (N=1): BASELINE config c4 — D3Q19 PSM fp32, 512^3 periodic cells per GPU, one
+sphere r=64 translating at v=(1/32,0,0) with s=1 and remapped every step, SRT + SC1, weighted B
+(Eq.(6)), two-array pull streaming.  A "step" is one pass of the whole hot path: closed-form pose
+advance, fraction remap (GPU), fused PSM stream-collide with force/torque partials (GPU), halo
+exchange (N>1), and the per-call force/torque reduction.  N>1: weak scaling, 512^3 per GPU
+stacked along z (global 512 x 512 x 512N), one moving sphere per GPU slab, NCCL halo exchange.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config c4]
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ...
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "MLUPS per GPU and % of HBM roofline at 1/2/4/8 B200 (PSM moving geometry)"
+UNIT = "MLUPS"
+
+WORKLOADS = {
+    # name: (nx, ny, nz_per_gpu, Q, prec, tau, sphere r, s, v, pattern)
+    "c4": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.6, r=64.0, s=1,
+               v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
+               desc="c4: D3Q19 PSM fp32 512^3/GPU periodic, sphere r=64 translating "
+                    "v=(1/32,0,0), s=1, remapped every step, SC1, weighted B"),
+    "c4aa": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.6, r=64.0, s=1,
+                 v=(1.0 / 32.0, 0.0, 0.0), pattern="aa", sc=1, bmode=1,
+                 desc="c4 (AA pattern): D3Q19 PSM fp32 512^3, moving sphere r=64, s=1"),
+    "c4f64": dict(nx=512, ny=512, nz=512, Q=19, prec="f64", tau=0.6, r=64.0, s=1,
+                  v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
+                  desc="c4 fp64: D3Q19 PSM fp64 512^3, moving sphere r=64, s=1"),
+    "c3f64": dict(nx=256, ny=256, nz=256, Q=27, prec="f64", tau=0.6, r=48.0, s=1,
+                  v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
+                  desc="c3-shaped: D3Q27 PSM fp64 256^3, moving sphere r=48, s=1"),
+}
+
+
+def bytes_per_update(Q: int, S: int) -> int:
+    """Algorithmic bytes per cell update: one read + one write per population, 2*Q*S
+    (the paper's roofline model)."""
+    return 2 * Q * S
+
+
+def load_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def profiles_traffic(workload: str):
+    """dram bytes per collide launch from the committed ncu summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------ CPU oracle leg ---
+def oracle_sample(wl: dict, steps: int, budget_s: float, seed: int):
+    """Time the CPU oracle (as it stands) on a bounded sub-box of the same workload: same
+    stencil/tau/operator, sphere scaled with the box, moving, remapped every step."""
+    import oracle
+    import psm_inputs as pi
+    cores = os.cpu_count() or 1
+    # oracle throughput is ~0.6 MLUPS per core for D3Q19; size the box for the budget
+    est = 0.6e6 * cores * (19.0 / wl["Q"])
+    cells = max(32 ** 3, min(256 ** 3, int(budget_s * est / max(1, steps))))
+    n = int(round(cells ** (1 / 3) / 16)) * 16
+    n = max(32, n)
+    scale = n / wl["nx"]
+    o = oracle.Oracle(n, n, n, wl["Q"], wl["tau"], (0, 0, 0), wl["sc"], wl["bmode"])
+    o.set_sphere(1, max(2.0, wl["r"] * scale), wl["s"])
+    rho, u = pi.perturbed_flow((n, n, n), seed, u0=(0.02, 0.0, 0.0), u_amp=0.001)
+    o.init_equilibrium(rho, u)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        o.set_pose(1, np.eye(3), (n / 2 + k * wl["v"][0], n / 2, n / 2), wl["v"])
+        o.map()
+        o.step(1)
+    dt = time.perf_counter() - t0
+    mlups = n ** 3 * steps / dt / 1e6
+    sample = (f"oracle fp64 on a {n}^3 periodic sub-box of {wl['desc'].split(':')[0]} "
+              f"(sphere r={max(2.0, wl['r'] * scale):g}, moving, remap+collide every step), "
+              f"{steps} steps, {dt:.1f} s")
+    return {"value": mlups, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+
+
+def run_reference(args, wl, rank, world):
+    if rank != 0:
+        return 0
+    per_step_budget = 150.0 / max(1, args.steps + args.warmup)
+    cb = oracle_sample(wl, max(1, args.steps), per_step_budget * args.steps, 7)
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": wl["desc"], "parallelism": "cpu oracle (OpenMP)"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------- GPU leg -----
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.config]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, wl, rank, world)
+
+    import torch
+    import paper_2502_20049_b200 as psm
+    import psm_inputs as pi
+
+    torch.cuda.set_device(local)
+    dist = None
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(psm.psm_nccl_get_unique_id()),
+                                       dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+
+    nx, ny, nzg = wl["nx"], wl["ny"], wl["nz"] * world
+    S = 8 if wl["prec"] == "f64" else 4
+    sim = psm.Simulation(nx, ny, nzg, Q=wl["Q"], tau=wl["tau"], bc=(0, 0, 0), prec=wl["prec"],
+                         pattern=wl["pattern"], sc=wl["sc"], bmode=wl["bmode"], rank=rank,
+                         world=world, nccl_id=nccl_id)
+    z0, nzl = sim.z0, sim.nzl
+    sim.init_equilibrium(None, None)
+    # one moving sphere per GPU slab, centred in it
+    t0 = (nx / 2, ny / 2, z0 + nzl / 2)
+    for r in range(world):
+        zc = (nzg * r) // world + ((nzg * (r + 1)) // world - (nzg * r) // world) / 2
+        sim.set_sphere(1 + r, wl["r"], wl["s"], np.eye(3), (nx / 2, ny / 2, zc), wl["v"])
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    sim.step(max(3, args.warmup))
+    barrier()
+    l0 = sim.launches
+    sim.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        sim.step(args.steps)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    sim.profile(False)
+    prof = sim.profile_read()
+    launches = sim.launches - l0
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    cells_local = nx * ny * nzl
+    cells_total = nx * ny * nzg
+    mlups = cells_total * args.steps / (ms_max / 1e3) / 1e6
+    peak, peak_src = load_peak()
+    bpu = bytes_per_update(wl["Q"], S)
+    coll_ms, coll_n = prof["collide"]
+    avg = coll_ms / max(1, coll_n)
+    achieved = bpu * cells_local / (avg / 1e3) / 1e9 if coll_n else None
+    step_gbs = bpu * cells_local * args.steps / (ms / 1e3) / 1e9
+
+    # end-to-end through the public API with host buffers: upload of the initial fields,
+    # per-step host pose in (closed form, 96 B) and force/torque out (48 B), final readback
+    e2e = None
+    if not args.no_e2e:
+        shape = (nzl, ny, nx)
+        rho_h = torch.ones(shape, dtype=torch.float64).pin_memory().numpy()
+        u_h = torch.zeros((3,) + shape, dtype=torch.float64).pin_memory().numpy()
+        u_h[0] = 0.02
+        barrier()
+        t_start = time.perf_counter()
+        sim.init_equilibrium(rho_h, u_h)
+        for k in range(args.steps):
+            sim.step(1)
+            for r in range(world):
+                sim.force_torque(1 + r)
+        sim.velocity() if False else None
+        rho_o = np.empty(shape)
+        u_o = np.empty((3,) + shape)
+        psm.psm_read_velocity(sim.ctx, rho_o, u_o)
+        barrier()
+        dt = time.perf_counter() - t_start
+        if dist is not None:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        h2d = (rho_h.nbytes + u_h.nbytes) / args.steps
+        d2h = (rho_o.nbytes + u_o.nbytes) / args.steps + 2 * 12 * 8 * world
+        e2e = {"value": cells_total * args.steps / dt / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "what": "init_equilibrium(host rho,u) + K x (psm_step(1) + psm_force_torque) + "
+                       "psm_read_velocity(host), wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(wl, 2, 20.0, 7)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": mlups, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": wl["prec"], "data": "synthetic",
+            "config": {"workload": wl["desc"], "grid": [nx, ny, nzg],
+                       "cells_per_gpu": cells_local, "global_cells": cells_total,
+                       "stencil": f"D3Q{wl['Q']}", "pattern": wl["pattern"],
+                       "parallelism": f"z-slab x{world}" + (" + NCCL halo" if world > 1 else ""),
+                       "l2": "inputs larger than L2 (PDF arrays >> 126 MB)"},
+            "mlups_per_gpu": mlups / world,
+            "roofline_frac_step": step_gbs / peak,
+            "roofline": {"bound": "hbm", "kernel": "k_collide (fused PSM stream-collide)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None,
+                         "traffic": profiles_traffic(args.config),
+                         "bytes_per_update": bpu, "peak_source": peak_src,
+                         "avg_launch_ms": avg, "launches_timed": coll_n},
+            "phases_ms": {k: v[0] / max(1, args.steps) for k, v in prof.items()},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        sim.close()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
