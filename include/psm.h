@@ -70,12 +70,14 @@ typedef struct {
   double body_force[3];  /* constant Guo body force on the fluid part, TEST-ONLY (default 0); */
                          /* only supported with PSM_TWO_ARRAY                               */
   int32_t rank, world;   /* z-slab decomposition: this rank of `world` (world >= 1)         */
-  const void* nccl_unique_id; /* 128-byte ncclUniqueId shared by all ranks; NULL iff world==1 */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId (fresh per context) shared by all ranks; NULL iff world==1 */
   void* cuda_stream;     /* cudaStream_t to enqueue on (e.g. torch's current stream); NULL = */
                          /* the legacy default stream                                       */
 } psm_options;
 
-/* Create a context.  Host-only: validates and plans the layout; no device memory yet.
+/* Create a context.  Host-only: validates and plans the layout; no device memory yet.  With
+ * world > 1 the NCCL communicator is created at the first device call (bind/alloc), which is
+ * collective: every rank must reach it.  Rank r owns global z in [r*nz/world, (r+1)*nz/world).
  * Errors: PSM_E_ARG if tau <= 1/2 or non-finite (Eq.(2): tau is the relaxation time and the
  * viscosity (tau-1/2)/3 must be positive), any extent < 1, nz < world, or an unknown enum;
  * PSM_E_UNSUPPORTED for body_force with PSM_AA or world > 1 with PSM_AA.

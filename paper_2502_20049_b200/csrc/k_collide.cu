@@ -96,7 +96,12 @@ __device__ __forceinline__ void tile_partial_reduce(int myid, const double* v, d
   }
 }
 
-template <int Q, typename T, int PAT, bool FORCE, bool DBG>
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+  return __ldg(p);
+}
+
+template <int Q, typename T, int PAT, bool WALLS, bool FORCE, bool DBG>
 __global__ void __launch_bounds__(kTileCells)
     k_collide(const __grid_constant__ CollideParams p) {
   const Geom& G = p.g;
@@ -108,68 +113,76 @@ __global__ void __launch_bounds__(kTileCells)
   const bool solid_tile = DBG ? true : (p.tile_flag[tile] != 0);
 
   const int nx = G.nx, ny = G.ny;
+  const int plane = nx * ny;
+  // inactive (ragged-tail) threads alias cell (0,0,0): their loads stay in bounds, no stores
   const int xc = act ? x : 0, yc = act ? y : 0, zc = act ? z : 0;
   const int zs = zc + G.zghost;  // storage plane
-  // source coordinate for a population with velocity component d is (coord - d)
-  int sx_p = xc - 1, sx_m = xc + 1, sy_p = yc - 1, sy_m = yc + 1, sz_p = zs - 1, sz_m = zs + 1;
-  bool ox_p = false, ox_m = false, oy_p = false, oy_m = false, oz_p = false, oz_m = false;
-  if (sx_p < 0) { if (G.wall[0]) ox_p = true; else sx_p += nx; }
-  if (sx_m >= nx) { if (G.wall[0]) ox_m = true; else sx_m -= nx; }
-  if (sy_p < 0) { if (G.wall[1]) oy_p = true; else sy_p += ny; }
-  if (sy_m >= ny) { if (G.wall[1]) oy_m = true; else sy_m -= ny; }
+  const int self = zs * plane + yc * nx + xc;
+
+  // Offsets (elements) from `self` to the SOURCE of a population with velocity component
+  // d = -1, 0, +1 along each axis (the source is at coordinate - d), wrapped on periodic axes;
+  // OUT* flags mark a source beyond a wall (half-way bounce-back, reading A23/A10).
+  int OX[3] = {1, 0, -1}, OY[3] = {nx, 0, -nx}, OZ[3] = {plane, 0, -plane};
+  bool OUTX[3] = {false, false, false}, OUTY[3] = {false, false, false},
+       OUTZ[3] = {false, false, false};
+  if (xc == 0) { if (WALLS && G.wall[0]) OUTX[2] = true; else OX[2] = nx - 1; }
+  if (xc == nx - 1) { if (WALLS && G.wall[0]) OUTX[0] = true; else OX[0] = 1 - nx; }
+  if (yc == 0) { if (WALLS && G.wall[1]) OUTY[2] = true; else OY[2] = (ny - 1) * nx; }
+  if (yc == ny - 1) { if (WALLS && G.wall[1]) OUTY[0] = true; else OY[0] = (1 - ny) * nx; }
   if (G.zghost) {
-    const int zg = G.z0 + zc;
-    if (G.wall[2]) { oz_p = (zg == 0); oz_m = (zg == G.nz_global - 1); }
+    if (WALLS && G.wall[2]) {
+      const int zg = G.z0 + zc;
+      OUTZ[2] = (zg == 0);
+      OUTZ[0] = (zg == G.nz_global - 1);
+    }
   } else {
-    if (sz_p < 0) { if (G.wall[2]) oz_p = true; else sz_p += G.nzl; }
-    if (sz_m >= G.nzl) { if (G.wall[2]) oz_m = true; else sz_m -= G.nzl; }
+    if (zc == 0) { if (WALLS && G.wall[2]) OUTZ[2] = true; else OZ[2] = (G.nzl - 1) * plane; }
+    if (zc == G.nzl - 1) { if (WALLS && G.wall[2]) OUTZ[0] = true; else OZ[0] = (1 - G.nzl) * plane; }
   }
-  const int self = (zs * ny + yc) * nx + xc;
+  int RB[3][3];  // self + OY[cy] + OZ[cz]
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) RB[a][b] = self + OY[a] + OZ[b];
   const long long qs = G.qstride;
 
+  // ---- gather the pre-collision populations f_i(x) ----
   T f[Q];
   {
     const T* A = static_cast<const T*>(p.src);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      const int cx = stc_x(q), cy = stc_y(q), cz = stc_z(q);
-      const int sx = cx > 0 ? sx_p : (cx < 0 ? sx_m : xc);
-      const int sy = cy > 0 ? sy_p : (cy < 0 ? sy_m : yc);
-      const int sz = cz > 0 ? sz_p : (cz < 0 ? sz_m : zs);
-      const bool out = (cx > 0 ? ox_p : (cx < 0 ? ox_m : false)) ||
-                       (cy > 0 ? oy_p : (cy < 0 ? oy_m : false)) ||
-                       (cz > 0 ? oz_p : (cz < 0 ? oz_m : false));
-      const int src = (sz * ny + sy) * nx + sx;
-      T v = T(0);
-      if (act) {
-        if (PAT == 0) {
-          v = out ? __ldg(A + stc_opp(q) * qs + self) : __ldg(A + q * qs + src);
-        } else if (PAT == 1) {
-          v = A[q * qs + self];
-        } else {
-          v = out ? A[q * qs + self] : A[stc_opp(q) * qs + src];
-        }
+      const int cx = stc_x(q) + 1, cy = stc_y(q) + 1, cz = stc_z(q) + 1;
+      const int src = RB[cy][cz] + OX[cx];
+      const bool out = WALLS && (OUTX[cx] || OUTY[cy] || OUTZ[cz]);
+      if (PAT == 0) {
+        const T* ptr = out ? (A + stc_opp(q) * qs + self) : (A + q * qs + src);
+        f[q] = ld_stream(ptr);
+      } else if (PAT == 1) {
+        f[q] = A[q * qs + self];
+      } else {
+        const T* ptr = out ? (A + q * qs + self) : (A + stc_opp(q) * qs + src);
+        f[q] = *ptr;
       }
-      f[q] = v;
     }
   }
 
-  // moments of the pre-collision state
-  T rho = T(0), jx = T(0), jy = T(0), jz = T(0);
+  // ---- moments ----
+  T rho = f[0], jx = T(0), jy = T(0), jz = T(0);
 #pragma unroll
-  for (int q = 0; q < Q; ++q) {
+  for (int q = 1; q < Q; ++q) {
     rho += f[q];
     if (stc_x(q) > 0) jx += f[q]; else if (stc_x(q) < 0) jx -= f[q];
     if (stc_y(q) > 0) jy += f[q]; else if (stc_y(q) < 0) jy -= f[q];
     if (stc_z(q) > 0) jz += f[q]; else if (stc_z(q) < 0) jz -= f[q];
   }
   if (act && !(rho > T(0) && rho < T(INFINITY))) {
-    const long long cell =
-        ((long long)(G.z0 + z) * G.ny + y) * (long long)G.nx + x;
+    const long long cell = ((long long)(G.z0 + z) * G.ny + y) * (long long)G.nx + x;
     const long long ncell = (long long)G.nz_global * G.ny * G.nx;
     atomicMin(p.err, (unsigned long long)(p.step * ncell + cell));
   }
-  const T ir = act ? T(1) / rho : T(0);
+  T ir;
+  if constexpr (sizeof(T) == 4) ir = __frcp_rn(rho); else ir = T(1) / rho;
   T gl[3] = {T(p.gforce[0]), T(p.gforce[1]), T(p.gforce[2])};
   const T ux = FORCE ? (jx + T(0.5) * gl[0]) * ir : jx * ir;
   const T uy = FORCE ? (jy + T(0.5) * gl[1]) * ir : jy * ir;
@@ -179,12 +192,30 @@ __global__ void __launch_bounds__(kTileCells)
   const T gpref = T(1) - T(0.5) * om;
 
   if (!solid_tile) {
-    // plain SRT: f* = f + omega (f^eq - f)   (Eq.(1) with Eq.(2))
+    // plain SRT, f* = f + omega (f^eq - f)  (Eq.(1) with Eq.(2)); pairs (i, ibar) share
+    // f^eq_i = w rho (a + b), f^eq_ibar = w rho (a - b), a = 1 - 1.5 u.u + 4.5 (c.u)^2, b = 3 c.u
+    const T base = T(1) - usq15;
+    {
+      T o0 = om * (T(stc_w<Q>(0)) * rho * base - f[0]);
+      if (FORCE) o0 += guo_q<Q, T>(0, ux, uy, uz, gl, gpref);
+      f[0] = f[0] + o0;
+    }
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      T o = om * (feq_q<Q, T>(q, rho, ux, uy, uz, usq15) - f[q]);
-      if (FORCE) o += guo_q<Q, T>(q, ux, uy, uz, gl, gpref);
-      f[q] = f[q] + o;
+    for (int i = 1; i < Q; ++i) {
+      const int j = stc_opp(i);
+      if (j < i) continue;
+      const T cu = T(stc_x(i)) * ux + T(stc_y(i)) * uy + T(stc_z(i)) * uz;
+      const T wr = T(stc_w<Q>(i)) * rho;
+      const T a = wr * (base + T(4.5) * cu * cu);
+      const T b = wr * (T(3) * cu);
+      T oi = om * ((a + b) - f[i]);
+      T oj = om * ((a - b) - f[j]);
+      if (FORCE) {
+        oi += guo_q<Q, T>(i, ux, uy, uz, gl, gpref);
+        oj += guo_q<Q, T>(j, ux, uy, uz, gl, gpref);
+      }
+      f[i] = f[i] + oi;
+      f[j] = f[j] + oj;
     }
   } else {
     // ---- PSM cell: B, u_s from the solid word (or the test-only dense fields) ----
@@ -255,8 +286,8 @@ __global__ void __launch_bounds__(kTileCells)
           oSj = (fi - si) - (fj - sj);
         }
         f[i] = fi + B1 * oFi + B * oSi;
-        if (j != i) f[j] = fj + B1 * oFj + B * oSj;
         if (j != i) {
+          f[j] = fj + B1 * oFj + B * oSj;
           const T d = oSi - oSj;  // c_j = -c_i
           msx += T(stc_x(i)) * d;
           msy += T(stc_y(i)) * d;
@@ -286,6 +317,7 @@ __global__ void __launch_bounds__(kTileCells)
     tile_partial_reduce(myid, v, p.partial + (size_t)tile * 2 * (1 + kSlotVals), p.overflow);
   }
 
+  // ---- scatter ----
   if (act) {
     T* Aout = static_cast<T*>(p.dst);
 #pragma unroll
@@ -296,17 +328,10 @@ __global__ void __launch_bounds__(kTileCells)
         Aout[stc_opp(q) * qs + self] = f[q];
       } else {
         // destination x + c_q == source position of the opposite direction
-        const int cx = stc_x(q), cy = stc_y(q), cz = stc_z(q);
-        const int dx = cx > 0 ? sx_m : (cx < 0 ? sx_p : xc);
-        const int dy = cy > 0 ? sy_m : (cy < 0 ? sy_p : yc);
-        const int dz = cz > 0 ? sz_m : (cz < 0 ? sz_p : zs);
-        const bool out = (cx > 0 ? ox_m : (cx < 0 ? ox_p : false)) ||
-                         (cy > 0 ? oy_m : (cy < 0 ? oy_p : false)) ||
-                         (cz > 0 ? oz_m : (cz < 0 ? oz_p : false));
-        if (out)
-          Aout[stc_opp(q) * qs + self] = f[q];
-        else
-          Aout[q * qs + (dz * ny + dy) * nx + dx] = f[q];
+        const int cx = 1 - stc_x(q), cy = 1 - stc_y(q), cz = 1 - stc_z(q);
+        const bool out = WALLS && (OUTX[cx] || OUTY[cy] || OUTZ[cz]);
+        T* ptr = out ? (Aout + stc_opp(q) * qs + self) : (Aout + q * qs + RB[cy][cz] + OX[cx]);
+        *ptr = f[q];
       }
     }
   }
@@ -317,17 +342,19 @@ template <int Q, typename T>
 static cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool dbg,
                             cudaStream_t st) {
   dim3 grid(p.g.gx, p.g.gy, p.g.gz), block(kTileX, kTileY, kTileZ);
-  if (dbg) {
-    if (force) k_collide<Q, T, 0, true, true><<<grid, block, 0, st>>>(p);
-    else k_collide<Q, T, 0, false, true><<<grid, block, 0, st>>>(p);
-  } else if (force) {
-    k_collide<Q, T, 0, true, false><<<grid, block, 0, st>>>(p);
+  const bool walls = p.g.wall[0] || p.g.wall[1] || p.g.wall[2];
+  if (dbg || force) {
+    if (dbg && force) k_collide<Q, T, 0, true, true, true><<<grid, block, 0, st>>>(p);
+    else if (dbg) k_collide<Q, T, 0, true, false, true><<<grid, block, 0, st>>>(p);
+    else k_collide<Q, T, 0, true, true, false><<<grid, block, 0, st>>>(p);
   } else if (pat == 0) {
-    k_collide<Q, T, 0, false, false><<<grid, block, 0, st>>>(p);
+    if (walls) k_collide<Q, T, 0, true, false, false><<<grid, block, 0, st>>>(p);
+    else k_collide<Q, T, 0, false, false, false><<<grid, block, 0, st>>>(p);
   } else if (pat == 1) {
-    k_collide<Q, T, 1, false, false><<<grid, block, 0, st>>>(p);
+    k_collide<Q, T, 1, false, false, false><<<grid, block, 0, st>>>(p);
   } else {
-    k_collide<Q, T, 2, false, false><<<grid, block, 0, st>>>(p);
+    if (walls) k_collide<Q, T, 2, true, false, false><<<grid, block, 0, st>>>(p);
+    else k_collide<Q, T, 2, false, false, false><<<grid, block, 0, st>>>(p);
   }
   return cudaGetLastError();
 }

@@ -93,6 +93,7 @@ struct psm_ctx {
   bool ft_valid = false;
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
+  unsigned char nccl_id[128] = {};
   std::string err_msg;
   int64_t launches = 0;
   bool prof = false;
@@ -313,8 +314,12 @@ static Plan make_plan(const psm_ctx* c) {
 
 static psm_status ensure_pinned(psm_ctx* c);
 
+static psm_status ensure_comm(psm_ctx* c);
+
 static psm_status bind(psm_ctx* c, void* mem, size_t bytes) {
   psm_status ps = ensure_pinned(c);
+  if (ps != PSM_OK) return ps;
+  ps = ensure_comm(c);
   if (ps != PSM_OK) return ps;
   Plan p = make_plan(c);
   if (bytes < p.total)
@@ -353,8 +358,20 @@ static psm_status ensure_pinned(psm_ctx* c) {
   return PSM_OK;
 }
 
+static psm_status ensure_comm(psm_ctx* c) {
+  // the communicator is created at the first device call, so psm_create stays host-only
+  if (c->world == 1 || c->comm) return PSM_OK;
+  ncclUniqueId id;
+  static_assert(sizeof(id) == sizeof(c->nccl_id), "ncclUniqueId size");
+  std::memcpy(&id, c->nccl_id, sizeof(id));
+  NCCL_TRY(c, ncclCommInitRank(&c->comm, c->world, id, c->rank));
+  return PSM_OK;
+}
+
 static psm_status ensure_mem(psm_ctx* c) {
   psm_status ps = ensure_pinned(c);
+  if (ps != PSM_OK) return ps;
+  ps = ensure_comm(c);
   if (ps != PSM_OK) return ps;
   if (c->bound) return PSM_OK;
   Plan p = make_plan(c);
@@ -695,16 +712,7 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   }
   c->ncell_local = (int64_t)c->nzl * grid->ny * grid->nx;
   c->ntiles = (int64_t)g.gx * g.gy * g.gz;
-  if (world > 1) {
-    ncclUniqueId id;
-    std::memcpy(&id, opt->nccl_unique_id, sizeof(id));
-    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, c->rank);
-    if (r != ncclSuccess) {
-      std::string m = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
-      delete c;
-      FAIL((psm_ctx*)nullptr, PSM_E_NCCL, m);
-    }
-  }
+  if (world > 1) std::memcpy(c->nccl_id, opt->nccl_unique_id, sizeof(c->nccl_id));
   *out = c;
   return PSM_OK;
 }
