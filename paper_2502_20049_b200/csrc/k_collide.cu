@@ -25,7 +25,7 @@ __device__ __forceinline__ T feq_q(int q, T rho, T ux, T uy, T uz, T usq15) {
 }
 
 template <int Q, typename T>
-__device__ __forceinline__ T guo_q(int q, T ux, T uy, T uz, const T g[3], T pref) {
+__device__ __forceinline__ T guo_q(int q, T ux, T uy, T uz, const T (&g)[3], T pref) {
   // (1 - 1/(2 tau)) w_i [3 (c_i - u) + 9 (c_i.u) c_i] . g   (test-only forcing)
   const T cx = T(stc_x(q)), cy = T(stc_y(q)), cz = T(stc_z(q));
   const T cu = cx * ux + cy * uy + cz * uz;
@@ -93,6 +93,60 @@ __device__ __forceinline__ void tile_partial_reduce(int myid, const double* v, d
   }
   if (myid && (unsigned)myid != ids[0] && (unsigned)myid != ids[1]) {
     for (int k = 0; k < kSlotVals; ++k) atomicAdd(overflow + myid * kSlotVals + k, v[k]);
+  }
+}
+
+// explicitly rounded arithmetic: the fluid update must give the same bits wherever it runs
+// (fluid tiles, B = 0 cells of PSM tiles, every slab decomposition)
+__device__ __forceinline__ float rfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double rfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+
+// c_i . u with compile-time c (adds/subtracts only)
+template <typename T>
+__device__ __forceinline__ T cdot(int q, T ux, T uy, T uz) {
+  T r = T(0);
+  bool first = true;
+  if (stc_x(q)) { r = stc_x(q) > 0 ? ux : -ux; first = false; }
+  if (stc_y(q)) { r = first ? (stc_y(q) > 0 ? uy : -uy) : (stc_y(q) > 0 ? radd(r, uy) : rsub(r, uy)); first = false; }
+  if (stc_z(q)) { r = first ? (stc_z(q) > 0 ? uz : -uz) : (stc_z(q) > 0 ? radd(r, uz) : rsub(r, uz)); }
+  return r;
+}
+
+// Plain SRT for one cell, f* = f + omega (f^eq - f) (Eq.(1) with Eq.(2)-(3)), pairs (i, ibar)
+// sharing f^eq_i = a + b, f^eq_ibar = a - b with a = w rho (1 - 1.5 u.u + 4.5 (c.u)^2),
+// b = 3 w rho c.u.  Every operation is explicitly rounded.
+template <int Q, typename T, bool FORCE>
+__device__ __forceinline__ void srt_update(T (&f)[Q], T rho, T ux, T uy, T uz, T om,
+                                           const T (&gl)[3], T gpref) {
+  const T usq = rfma(uz, uz, rfma(uy, uy, rmul(ux, ux)));
+  const T base = rsub(T(1), rmul(T(1.5), usq));
+  {
+    T o0 = rmul(om, rsub(rmul(rmul(T(stc_w<Q>(0)), rho), base), f[0]));
+    if (FORCE) o0 = radd(o0, guo_q<Q, T>(0, ux, uy, uz, gl, gpref));
+    f[0] = radd(f[0], o0);
+  }
+#pragma unroll
+  for (int i = 1; i < Q; ++i) {
+    const int j = stc_opp(i);
+    if (j < i) continue;
+    const T cu = cdot<T>(i, ux, uy, uz);
+    const T wr = rmul(T(stc_w<Q>(i)), rho);
+    const T a = rmul(wr, rfma(rmul(T(4.5), cu), cu, base));
+    const T b = rmul(wr, rmul(T(3), cu));
+    T oi = rmul(om, rsub(radd(a, b), f[i]));
+    T oj = rmul(om, rsub(rsub(a, b), f[j]));
+    if (FORCE) {
+      oi = radd(oi, guo_q<Q, T>(i, ux, uy, uz, gl, gpref));
+      oj = radd(oj, guo_q<Q, T>(j, ux, uy, uz, gl, gpref));
+    }
+    f[i] = radd(f[i], oi);
+    f[j] = radd(f[j], oj);
   }
 }
 
@@ -183,40 +237,16 @@ __global__ void __launch_bounds__(kTileCells)
   }
   T ir;
   if constexpr (sizeof(T) == 4) ir = __frcp_rn(rho); else ir = T(1) / rho;
-  T gl[3] = {T(p.gforce[0]), T(p.gforce[1]), T(p.gforce[2])};
-  const T ux = FORCE ? (jx + T(0.5) * gl[0]) * ir : jx * ir;
-  const T uy = FORCE ? (jy + T(0.5) * gl[1]) * ir : jy * ir;
-  const T uz = FORCE ? (jz + T(0.5) * gl[2]) * ir : jz * ir;
+  const T gl[3] = {T(p.gforce[0]), T(p.gforce[1]), T(p.gforce[2])};
+  const T ux = FORCE ? rmul(rfma(T(0.5), gl[0], jx), ir) : rmul(jx, ir);
+  const T uy = FORCE ? rmul(rfma(T(0.5), gl[1], jy), ir) : rmul(jy, ir);
+  const T uz = FORCE ? rmul(rfma(T(0.5), gl[2], jz), ir) : rmul(jz, ir);
   const T usq15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
   const T om = T(p.omega);
   const T gpref = T(1) - T(0.5) * om;
 
   if (!solid_tile) {
-    // plain SRT, f* = f + omega (f^eq - f)  (Eq.(1) with Eq.(2)); pairs (i, ibar) share
-    // f^eq_i = w rho (a + b), f^eq_ibar = w rho (a - b), a = 1 - 1.5 u.u + 4.5 (c.u)^2, b = 3 c.u
-    const T base = T(1) - usq15;
-    {
-      T o0 = om * (T(stc_w<Q>(0)) * rho * base - f[0]);
-      if (FORCE) o0 += guo_q<Q, T>(0, ux, uy, uz, gl, gpref);
-      f[0] = f[0] + o0;
-    }
-#pragma unroll
-    for (int i = 1; i < Q; ++i) {
-      const int j = stc_opp(i);
-      if (j < i) continue;
-      const T cu = T(stc_x(i)) * ux + T(stc_y(i)) * uy + T(stc_z(i)) * uz;
-      const T wr = T(stc_w<Q>(i)) * rho;
-      const T a = wr * (base + T(4.5) * cu * cu);
-      const T b = wr * (T(3) * cu);
-      T oi = om * ((a + b) - f[i]);
-      T oj = om * ((a - b) - f[j]);
-      if (FORCE) {
-        oi += guo_q<Q, T>(i, ux, uy, uz, gl, gpref);
-        oj += guo_q<Q, T>(j, ux, uy, uz, gl, gpref);
-      }
-      f[i] = f[i] + oi;
-      f[j] = f[j] + oj;
-    }
+    srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl, gpref);
   } else {
     // ---- PSM cell: B, u_s from the solid word (or the test-only dense fields) ----
     int id = 0;
@@ -298,12 +328,7 @@ __global__ void __launch_bounds__(kTileCells)
       m[1] = Bd * (double)msy;
       m[2] = Bd * (double)msz;
     } else {
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        T o = om * (feq_q<Q, T>(q, rho, ux, uy, uz, usq15) - f[q]);
-        if (FORCE) o += guo_q<Q, T>(q, ux, uy, uz, gl, gpref);
-        f[q] = f[q] + o;
-      }
+      srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl, gpref);
     }
     // ---- per-body F/T partial of this tile (deterministic block reduction) ----
     double v[kSlotVals];
