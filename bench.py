@@ -1,14 +1,15 @@
 #!/usr/bin/env python
 """Benchmark of the B200 PSM hot path (arXiv 2502.20049): MLUPS and % of the HBM roofline.
 
-Default workload (N=1): BASELINE config c4 — D3Q19 PSM fp32, 512^3 periodic cells per GPU, one
-sphere r=64 translating at v=(1/32,0,0) with s=1 and remapped every step, SRT + SC1, weighted B
-(Eq.(6)), two-array pull streaming.  A "step" is one pass of the whole hot path: closed-form pose
-advance, fraction remap (GPU), fused PSM stream-collide with force/torque partials (GPU), halo
-exchange (N>1), and the per-call force/torque reduction.  N>1: weak scaling, 512^3 per GPU
-stacked along z (global 512 x 512 x 512N), one moving sphere per GPU slab, NCCL halo exchange.
+Default workload: BASELINE config c5 (weak scaling) — D3Q19 PSM fp32, 512^3 periodic cells per
+GPU stacked along z (global 512 x 512 x 512N), one CROR-like counter-rotating rotor pair per GPU
+(triangle meshes of ~0.6 M faces each, voxelised once, remapped every step at s=1), SRT + SC1,
+weighted B (Eq.(6)), two-array pull streaming, NCCL halo exchange for N>1.  A "step" is one pass
+of the whole hot path: closed-form pose advance, fraction remap (GPU), fused PSM stream-collide
+with force/torque partials (GPU), halo exchange (N>1), and the per-call force/torque reduction.
+Other workloads: --config c4 (moving sphere r=64, 512^3), c4aa, c4f64, c3f64.
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config c4]
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config c5w]
 Multi-GPU: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ...
 Prints ONE JSON line on rank 0.
 """
@@ -31,7 +32,14 @@ METRIC = "MLUPS per GPU and % of HBM roofline at 1/2/4/8 B200 (PSM moving geomet
 UNIT = "MLUPS"
 
 WORKLOADS = {
-    # name: (nx, ny, nz_per_gpu, Q, prec, tau, sphere r, s, v, pattern)
+    # c5 weak scaling: 512^3 per GPU stacked in z, one CROR-like counter-rotating rotor pair per
+    # GPU (front 12 blades tip 200 at x=200, +Omega; rear 10 blades tip 180 at x=330, -Omega;
+    # Omega = 0.05/220 rad/step; ~0.6 M faces each; s=1), D3Q19 fp32 SRT+SC1, weighted B
+    "c5w": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.55, rotors=True, s=1,
+                omega=0.05 / 220.0, pattern="two_array", sc=1, bmode=1,
+                desc="c5 weak: D3Q19 PSM fp32, 512^3 per GPU, CROR-like counter-rotating rotor "
+                     "pair per GPU (12+10 blades, ~1.1 M faces, s=1, remapped every step), SC1, "
+                     "weighted B"),
     "c4": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.6, r=64.0, s=1,
                v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
                desc="c4: D3Q19 PSM fp32 512^3/GPU periodic, sphere r=64 translating "
@@ -126,29 +134,45 @@ def profiles_traffic(workload: str):
 # ------------------------------------------------------------------------ CPU oracle leg ---
 def oracle_sample(wl: dict, steps: int, budget_s: float, seed: int):
     """Time the CPU oracle (as it stands) on a bounded sub-box of the same workload: same
-    stencil/tau/operator, sphere scaled with the box, moving, remapped every step."""
+    stencil/tau/operator, bodies scaled with the box, moving, remapped every step."""
     import oracle
     import psm_inputs as pi
     cores = os.cpu_count() or 1
     # oracle throughput is ~0.6 MLUPS per core for D3Q19; size the box for the budget
     est = 0.6e6 * cores * (19.0 / wl["Q"])
     cells = max(32 ** 3, min(256 ** 3, int(budget_s * est / max(1, steps))))
-    n = int(round(cells ** (1 / 3) / 16)) * 16
-    n = max(32, n)
+    n = max(32, int(round(cells ** (1 / 3) / 16)) * 16)
     scale = n / wl["nx"]
     o = oracle.Oracle(n, n, n, wl["Q"], wl["tau"], (0, 0, 0), wl["sc"], wl["bmode"])
-    o.set_sphere(1, max(2.0, wl["r"] * scale), wl["s"])
     rho, u = pi.perturbed_flow((n, n, n), seed, u0=(0.02, 0.0, 0.0), u_amp=0.001)
     o.init_equilibrium(rho, u)
+    if wl.get("rotors"):
+        bodies = []
+        for k, (nbl, tip, xc) in enumerate(((12, 200.0, 200.0), (10, 180.0, 330.0))):
+            v, t = pi.propeller_mesh(n_blades=nbl, scale=tip / 110.0 * scale, n_st=16,
+                                     n_pts=24, hub_seg=32)
+            o.set_mesh(k + 1, v, t, wl["s"])
+            w = (wl["omega"] / scale * (1 if k == 0 else -1), 0.0, 0.0)
+            bodies.append((k + 1, (xc * scale, n / 2, n / 2), w))
+        what = "CROR-like rotor pair (12+10 blades, coarse meshes)"
+    else:
+        o.set_sphere(1, max(2.0, wl["r"] * scale), wl["s"])
+        bodies = [(1, None, None)]
+        what = f"sphere r={max(2.0, wl['r'] * scale):g}"
     t0 = time.perf_counter()
     for k in range(steps):
-        o.set_pose(1, np.eye(3), (n / 2 + k * wl["v"][0], n / 2, n / 2), wl["v"])
+        for bid, pos, w in bodies:
+            if pos is None:
+                o.set_pose(1, np.eye(3), (n / 2 + k * wl["v"][0], n / 2, n / 2), wl["v"])
+            else:
+                Qk, _ = oracle.pose_advance(np.eye(3), pos, (0, 0, 0), w, k, [n] * 3, [1] * 3)
+                o.set_pose(bid, Qk, pos, (0, 0, 0), w)
         o.map()
         o.step(1)
     dt = time.perf_counter() - t0
     mlups = n ** 3 * steps / dt / 1e6
     sample = (f"oracle fp64 on a {n}^3 periodic sub-box of {wl['desc'].split(':')[0]} "
-              f"(sphere r={max(2.0, wl['r'] * scale):g}, moving, remap+collide every step), "
+              f"({what}, scaled by {scale:g}, moving, remap+collide every step), "
               f"{steps} steps, {dt:.1f} s")
     return {"value": mlups, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
 
@@ -177,7 +201,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c5w", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -213,11 +237,20 @@ def main():
                          world=world, nccl_id=nccl_id)
     z0, nzl = sim.z0, sim.nzl
     sim.init_equilibrium(None, None)
-    # one moving sphere per GPU slab, centred in it
-    t0 = (nx / 2, ny / 2, z0 + nzl / 2)
+    nbodies = 0
     for r in range(world):
         zc = (nzg * r) // world + ((nzg * (r + 1)) // world - (nzg * r) // world) / 2
-        sim.set_sphere(1 + r, wl["r"], wl["s"], np.eye(3), (nx / 2, ny / 2, zc), wl["v"])
+        if wl.get("rotors"):
+            # counter-rotating pair per GPU slab; every rank holds every body (F/T allreduce)
+            for k, front in enumerate((True, False)):
+                v, t = pi.cror_rotor(front)
+                w = (wl["omega"] if front else -wl["omega"], 0.0, 0.0)
+                sim.set_mesh(1 + 2 * r + k, v, t, wl["s"], np.eye(3),
+                             (200.0 if front else 330.0, ny / 2, zc), (0, 0, 0), w)
+                nbodies += 1
+        else:  # one moving sphere per GPU slab, centred in it
+            sim.set_sphere(1 + r, wl["r"], wl["s"], np.eye(3), (nx / 2, ny / 2, zc), wl["v"])
+            nbodies += 1
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -269,8 +302,8 @@ def main():
         sim.init_equilibrium(rho_h, u_h)
         for k in range(args.steps):
             sim.step(1)
-            for r in range(world):
-                sim.force_torque(1 + r)
+            for b in range(nbodies):
+                sim.force_torque(1 + b)
         sim.velocity() if False else None
         rho_o = np.empty(shape)
         u_o = np.empty((3,) + shape)
@@ -282,7 +315,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         h2d = (rho_h.nbytes + u_h.nbytes) / args.steps
-        d2h = (rho_o.nbytes + u_o.nbytes) / args.steps + 2 * 12 * 8 * world
+        d2h = (rho_o.nbytes + u_o.nbytes) / args.steps + 6 * 8 * nbodies
         e2e = {"value": cells_total * args.steps / dt / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "what": "init_equilibrium(host rho,u) + K x (psm_step(1) + psm_force_torque) + "

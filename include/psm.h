@@ -150,6 +150,14 @@ psm_status psm_set_body(psm_ctx* ctx, int32_t body_id, const psm_shape* shape,
                         const psm_pose* pose, const psm_velocity* vel);
 psm_status psm_remove_body(psm_ctx* ctx, int32_t body_id);
 
+/* Host-only: the super-sampled geometry field psm_set_body builds for a mesh (PAPER.md:299-308,
+ * exact ray parity, A15/A17).  dims[3] (geometry cells per axis, = LBM cells * 2^s) and
+ * origin[3] (body frame, integer valued) are always written; bits (one byte 0/1 per geometry
+ * cell, [dims2][dims1][dims0]) is written if non-NULL and must hold dims0*dims1*dims2 bytes.
+ * Errors: PSM_E_ARG (s out of 0..3, NULL arrays), PSM_E_MESH (as psm_set_body). */
+psm_status psm_voxelize(const double* verts, int64_t nverts, const int32_t* tris, int64_t ntris,
+                        int32_t s, double origin[3], int64_t dims[3], uint8_t* bits);
+
 /* Recompute the solid fraction field of every body at its current pose:
  * eps = (#inside sub-samples) / 2^(3s) (reading R1, A12), B by Eq.(5)/(6). */
 psm_status psm_map_fractions(psm_ctx* ctx);

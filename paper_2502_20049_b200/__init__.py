@@ -36,7 +36,7 @@ PHASES = ("map", "collide", "ft_reduce", "halo")
 EXPORTED = (
     "psm_create", "psm_destroy", "psm_required_bytes", "psm_bind_memory", "psm_local_extent",
     "psm_init_equilibrium", "psm_write_pdfs", "psm_read_pdfs", "psm_read_velocity",
-    "psm_set_body", "psm_remove_body", "psm_map_fractions", "psm_step", "psm_force_torque",
+    "psm_set_body", "psm_remove_body", "psm_voxelize", "psm_map_fractions", "psm_step", "psm_force_torque",
     "psm_read_fractions", "psm_debug_set_fields", "psm_get_step", "psm_launch_count",
     "psm_profile", "psm_profile_read", "psm_nccl_id_bytes", "psm_nccl_get_unique_id",
     "psm_last_error",
@@ -94,7 +94,8 @@ def load(build_if_missing: bool = True):
         "psm_bind_memory": [P, P, SZ], "psm_local_extent": [P, P, P],
         "psm_init_equilibrium": [P, P, P], "psm_write_pdfs": [P, P], "psm_read_pdfs": [P, P],
         "psm_read_velocity": [P, P, P], "psm_set_body": [P, I32, P, P, P],
-        "psm_remove_body": [P, I32], "psm_map_fractions": [P], "psm_step": [P, I64],
+        "psm_remove_body": [P, I32], "psm_map_fractions": [P],
+        "psm_voxelize": [P, I64, P, I64, I32, P, P, P], "psm_step": [P, I64],
         "psm_force_torque": [P, I32, P, P, P, P], "psm_read_fractions": [P, P, P, P],
         "psm_debug_set_fields": [P, P, P, P], "psm_get_step": [P, P],
         "psm_launch_count": [P, P], "psm_profile": [P, I32], "psm_profile_read": [P, P, P],
@@ -181,6 +182,21 @@ def psm_set_body(ctx, body_id: int, shape, pose: psm_pose, vel: psm_velocity):
 
 def psm_remove_body(ctx, body_id: int):
     _check(load().psm_remove_body(ctx, body_id), ctx)
+
+
+def psm_voxelize(verts, tris, s: int):
+    """Host-side geometry field of a closed mesh: (origin[3], bits[gz, gy, gx] uint8)."""
+    verts = _c64(verts)
+    tris = np.ascontiguousarray(tris, np.int32)
+    origin = np.zeros(3)
+    dims = np.zeros(3, np.int64)
+    L = load()
+    _check(L.psm_voxelize(_ptr(verts), len(verts), _ptr(tris), len(tris), s, _ptr(origin),
+                          _ptr(dims), None))
+    bits = np.zeros(int(np.prod(dims)), np.uint8)
+    _check(L.psm_voxelize(_ptr(verts), len(verts), _ptr(tris), len(tris), s, _ptr(origin),
+                          _ptr(dims), _ptr(bits)))
+    return origin, bits.reshape(int(dims[2]), int(dims[1]), int(dims[0]))
 
 
 def psm_map_fractions(ctx):

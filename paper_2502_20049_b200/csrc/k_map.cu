@@ -15,137 +15,121 @@
 // sub-sample lies within one brick of the centre's brick).
 #include "psm_device.cuh"
 #include "psm_internal.h"
+#include "psm_map_common.cuh"
 
 namespace psm {
 
-__device__ __forceinline__ void body_frame(const BodyGeo& b, const double p[3], const double L[3],
-                                           const int wall[3], double q[3]) {
-  double d[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) d[a] = min_image(__dsub_rn(p[a], b.t[a]), L[a], !wall[a]);
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-    q[a] = __fma_rn(b.Q[6 + a], d[2], __fma_rn(b.Q[3 + a], d[1], __dmul_rn(b.Q[a], d[0])));
-}
-
-__device__ __forceinline__ int mesh_bit(const BodyGeo& b, const double q[3]) {
-  const double hs = ldexp(1.0, b.s);
-  int g[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double x = floor(__dmul_rn(__dsub_rn(q[a], b.o[a]), hs));
-    if (!(x >= 0.0) || x >= (double)(b.dims_b[a] << b.s)) return 0;
-    g[a] = (int)x;
-  }
-  const int n = 1 << b.s, msk = n - 1;
-  const long long brick =
-      ((long long)(g[2] >> b.s) * b.dims_b[1] + (g[1] >> b.s)) * b.dims_b[0] + (g[0] >> b.s);
-  const int bit = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
-  const unsigned long long w = __ldg(b.bits + brick * b.words + (bit >> 6));
-  return (int)((w >> (bit & 63)) & 1ull);
-}
-
-// number of inside sub-samples of cell (x, y, zg) for body b
-__device__ int count_inside(const BodyGeo& b, int x, int y, int zg, const double L[3],
-                            const int wall[3]) {
-  const int n = 1 << b.s;
-  const int full = n * n * n;
-  const double h = ldexp(1.0, -b.s);
-  // exact early-out from the cell centre
-  {
-    const double pc[3] = {x + 0.5, y + 0.5, zg + 0.5};
-    double qc[3];
-    body_frame(b, pc, L, wall, qc);
-    if (b.kind == 0) {
-      const double dist = sqrt(qc[0] * qc[0] + qc[1] * qc[1] + qc[2] * qc[2]);
-      const double r = sqrt(b.r2);
-      const double reach = 0.8660254037844387 + 1e-6;  // >= max |sample - centre|
-      if (dist + reach < r) return full;
-      if (dist - reach > r) return 0;
-    } else {
-      int bc[3];
-      bool outside = false;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double xb = floor(qc[a] - b.o[a]);
-        if (xb < -1.0 || xb > (double)b.dims_b[a]) outside = true;
-        bc[a] = (int)fmax(-2.0, fmin(xb, (double)b.dims_b[a] + 1.0));
-      }
-      if (outside) return 0;
-      if (bc[0] >= 0 && bc[1] >= 0 && bc[2] >= 0 && bc[0] < b.dims_b[0] &&
-          bc[1] < b.dims_b[1] && bc[2] < b.dims_b[2]) {
-        const uint8_t m =
-            __ldg(b.mask + ((long long)bc[2] * b.dims_b[1] + bc[1]) * b.dims_b[0] + bc[0]);
-        if (m == 1) return full;
-        if (m == 2) return 0;
-      }
-    }
-  }
-  int cnt = 0;
-  for (int gz = 0; gz < n; ++gz)
-    for (int gy = 0; gy < n; ++gy)
-      for (int gx = 0; gx < n; ++gx) {
-        const double p[3] = {(double)x + (gx + 0.5) * h, (double)y + (gy + 0.5) * h,
-                             (double)zg + (gz + 0.5) * h};
-        double q[3];
-        body_frame(b, p, L, wall, q);
-        if (b.kind == 0) {
-          const double d2 = __fma_rn(q[2], q[2], __fma_rn(q[1], q[1], __dmul_rn(q[0], q[0])));
-          cnt += (d2 <= b.r2);
-        } else {
-          cnt += mesh_bit(b, q);
-        }
-      }
-  return cnt;
-}
-
-__global__ void __launch_bounds__(kTileCells) k_map(const __grid_constant__ MapParams p) {
+// Remap of one 32x4x2 tile per block; grid = the box's tiles (blockIdx = tile offset in the box).
+// Each warp owns one 32-cell x-row and decides it without block barriers: (1) lanes 0..3 decide
+// the row's four 8-cell segments (fp64, reach kSubReach bricks) and broadcast them by shuffles,
+// (2) per cell in fp32 (dilated-by-one brick flags), (3) the narrow-band cells' sub-samples are
+// packed across the 32 lanes (lane -> (cell, sample)) and counted with ballots — exact fp64 per
+// sample (A14).
+__global__ void __launch_bounds__(kTileCells, 6) k_map(const __grid_constant__ MapParams p) {
   const Geom& G = p.g;
-  int k = 0;
-  while (k + 1 < p.nbox && p.box[k + 1].first <= (int)blockIdx.x) ++k;
-  const MapBox& bx = p.box[k];
-  const int li = blockIdx.x - bx.first;
-  const int tx = bx.t0[0] + li % bx.n[0];
-  const int ty = bx.t0[1] + (li / bx.n[0]) % bx.n[1];
-  const int tz = bx.t0[2] + li / (bx.n[0] * bx.n[1]);
-  const int x = tx * kTileX + threadIdx.x;
+  const int tid = threadIdx.x + kTileX * (threadIdx.y + kTileY * threadIdx.z);
+  const int lane = threadIdx.x;
+  const MapBox& bx = p.box[0];
+  const int tx = bx.t0[0] + (int)blockIdx.x;
+  const int ty = bx.t0[1] + (int)blockIdx.y;
+  const int tz = bx.t0[2] + (int)blockIdx.z;
+  // The tile flag says whether any word of this tile is nonzero now; if it is 0, writing a
+  // zero word is redundant, so warps far from every body store nothing.
+  const int flag_old = p.tile_flag[(tz * G.gy + ty) * G.gx + tx];
+  const int x = tx * kTileX + lane;
   const int y = ty * kTileY + threadIdx.y;
   const int z = tz * kTileZ + threadIdx.z;
-  const bool act = x < G.nx && y < G.ny && z < G.nzl;
-  uint32_t word = 0;
-  if (act) {
-    const int zg = G.z0 + z;
-    const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
-    const double xc[3] = {x + 0.5, y + 0.5, zg + 0.5};
-    int best = 0, bestcnt = 0;
-    double beste = 0.0;
-    for (int id = 1; id <= kMaxBodies; ++id) {
-      const BodyGeo& b = p.bodies[id];
-      if (!b.present) continue;
-      bool in = true;
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-        if (fabs(min_image(xc[a] - b.t[a], L[a], !G.wall[a])) > b.rb1) in = false;
-      if (!in) continue;
-      const int cnt = count_inside(b, x, y, zg, L, G.wall);
-      const double e = ldexp((double)cnt, -3 * b.s);
-      if (cnt > 0 && e > beste) {
-        best = id;
-        bestcnt = cnt;
-        beste = e;
+  const bool row_ok = y < G.ny && z < G.nzl;
+  const bool act = row_ok && x < G.nx;
+  const int zg = G.z0 + z;
+  const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
+  int best = 0, bestcnt = 0;
+  double beste = 0.0;
+  for (uint32_t msk = bx.bodymask; msk; msk &= msk - 1) {  // warp-uniform loop
+    const int id = __ffs(msk) - 1;
+    const BodyGeo& b = p.bodies[id];
+    const int s = b.s;
+    // (1) segment decisions: lane k < 4 evaluates segment k of this row
+    int sd = 0;
+    float q0 = 0.f, q1 = 0.f, q2 = 0.f;
+    if (lane < kTileX / kSubX && row_ok) {
+      const double ps[3] = {tx * kTileX + lane * kSubX + 0.5 * kSubX, y + 0.5, zg + 0.5};
+      double qs[3];
+      sd = tile_decision<kSubReach, 16, 32>(b, ps, L, G.wall, qs);
+      q0 = (float)qs[0];
+      q1 = (float)qs[1];
+      q2 = (float)qs[2];
+      if (p.stats) atomicAdd(p.stats + sd, 1ull);
+    }
+    const int seg = lane / kSubX;
+    const int sdec = __shfl_sync(0xFFFFFFFFu, sd, seg);
+    // (2) per-cell fp32 decision from the segment-centre transform
+    int cd = sdec;
+    const unsigned need = __ballot_sync(0xFFFFFFFFu, sdec == 2);
+    if (need) {
+      const float qs0 = __shfl_sync(0xFFFFFFFFu, q0, seg);
+      const float qs1 = __shfl_sync(0xFFFFFFFFu, q1, seg);
+      const float qs2 = __shfl_sync(0xFFFFFFFFu, q2, seg);
+      if (sdec == 2) {
+        const float off = (float)(lane % kSubX) + 0.5f - 0.5f * kSubX;
+        const float qc[3] = {qs0 + (float)b.Q[0] * off, qs1 + (float)b.Q[1] * off,
+                             qs2 + (float)b.Q[2] * off};
+        cd = cell_decision(b, qc);
       }
     }
-    if (best) word = (uint32_t)bestcnt | ((uint32_t)best << 16);
-    p.word[((long long)z * G.ny + y) * G.nx + x] = word;
+    if (!act) cd = 0;
+    int cnt = (cd == 1) ? (1 << (3 * s)) : 0;
+    // (3) narrow band: pack (cell, sample) pairs of the warp's band cells over the lanes
+    const unsigned band = __ballot_sync(0xFFFFFFFFu, cd == 2);
+    if (band) {
+      const int ls = 3 * s;
+      const int nsamp = 1 << ls;
+      const int nband = __popc(band);
+      const int items = nband << ls;
+      for (int base = 0; base < items; base += 32) {
+        const int it = base + lane;
+        int c = -1;
+        if (it < items) {
+          c = (int)__fns(band, 0, (it >> ls) + 1);  // (it >> ls)-th set bit of `band`
+        }
+        const int inside =
+            (c >= 0) ? sample_inside(b, tx * kTileX + c, y, zg, it & (nsamp - 1), L, G.wall)
+                     : 0;
+        const unsigned vote = __ballot_sync(0xFFFFFFFFu, inside);
+        // lanes carrying samples of MY cell: it in [base, base + 32) with (it >> ls) == my rank
+        if (cd == 2) {
+          const int rank = __popc(band & ((1u << lane) - 1));
+          const int first = (rank << ls) - base, last = first + nsamp;  // lane range
+          const int l0 = max(first, 0), l1 = min(last, 32);
+          if (l1 > l0) {
+            const unsigned sel = (l1 - l0 == 32) ? 0xFFFFFFFFu
+                                                 : (((1u << (l1 - l0)) - 1u) << l0);
+            cnt += __popc(vote & sel);
+          }
+        }
+      }
+    }
+    if (p.stats && act) atomicAdd(p.stats + 3 + cd, 1ull);
+    const double e = ldexp((double)cnt, -3 * s);
+    if (cnt > 0 && e > beste) {
+      best = id;
+      bestcnt = cnt;
+      beste = e;
+    }
   }
+  uint32_t word = 0;
+  if (best) word = (uint32_t)bestcnt | ((uint32_t)best << 16);
+  if (act && (word != 0 || flag_old != 0)) p.word[((long long)z * G.ny + y) * G.nx + x] = word;
   const int any = __syncthreads_or(word != 0);
-  if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0)
-    p.tile_flag[(tz * G.gy + ty) * G.gx + tx] = (uint8_t)(any ? 1 : 0);
+  if (tid == 0) p.tile_flag[(tz * G.gy + ty) * G.gx + tx] = (uint8_t)(any ? 1 : 0);
 }
 
 cudaError_t launch_map(const MapParams& p, cudaStream_t st) {
-  if (p.ntiles <= 0) return cudaSuccess;
-  k_map<<<p.ntiles, dim3(kTileX, kTileY, kTileZ), 0, st>>>(p);
+  // one launch per box: blockIdx is the tile offset inside box[0]
+  if (p.nbox != 1) return cudaErrorInvalidValue;
+  const MapBox& b = p.box[0];
+  if (b.n[0] <= 0 || b.n[1] <= 0 || b.n[2] <= 0) return cudaSuccess;
+  k_map<<<dim3(b.n[0], b.n[1], b.n[2]), dim3(kTileX, kTileY, kTileZ), 0, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,199 @@
+// k_remap.cu — narrow-band fraction remap for a box holding a single body (the common case:
+// every moving body in its own bounding box), arXiv 2502.20049 §III.
+//
+// The count of a cell changes only near the body surface, so the work is organised as a flat
+// pipeline of barrier-free kernels over compacted device lists, each level deciding exactly what
+// it can and passing the rest on:
+//   L0  one thread per tile of the box     : tile-centre test with reach kTileReach bricks
+//   L1  one thread per 8-cell segment      : segment-centre test with reach kSubReach
+//   L2  one thread per cell                : fp32 centre test against dilated-by-one bricks
+//   L3  one thread per (cell, sub-sample)  : exact fp64 inside test (reading R1, A14 order)
+//   L4  one thread per narrow-band cell    : count -> word
+// Every early decision is conservative (it only claims "all sub-samples outside/inside" when the
+// brick flags prove it), so the words equal the brute-force counts bit for bit.  Counts are
+// integers accumulated with atomics: order-independent.  Tile flags ("any word nonzero") are
+// reset for every tile that reaches L1 and set by whichever level writes a nonzero word.
+#include "psm_device.cuh"
+#include "psm_internal.h"
+#include "psm_map_common.cuh"
+
+namespace psm {
+
+namespace {
+
+constexpr int kSegPerTile = (kTileX / kSubX) * kTileY * kTileZ;  // 32
+
+__device__ __forceinline__ void tile_coords(int t, const Geom& G, int& tx, int& ty, int& tz) {
+  tx = t % G.gx;
+  ty = (t / G.gx) % G.gy;
+  tz = t / (G.gx * G.gy);
+}
+
+__device__ __forceinline__ void put_word(const RemapParams& r, int x, int y, int z, uint32_t w,
+                                         int tile) {
+  r.word[((long long)z * r.g.ny + y) * r.g.nx + x] = w;
+  if (w) r.tile_flag[tile] = 1;
+}
+
+// L0: one thread per tile of the box
+__global__ void k_remap_l0(const __grid_constant__ RemapParams r) {
+  const MapBox& bx = r.box;
+  const int ntile = bx.n[0] * bx.n[1] * bx.n[2];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntile) return;
+  const int tx = bx.t0[0] + i % bx.n[0];
+  const int ty = bx.t0[1] + (i / bx.n[0]) % bx.n[1];
+  const int tz = bx.t0[2] + i / (bx.n[0] * bx.n[1]);
+  const Geom& G = r.g;
+  const int tile = (tz * G.gy + ty) * G.gx + tx;
+  const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
+  const double pt[3] = {tx * kTileX + 0.5 * kTileX, ty * kTileY + 0.5 * kTileY,
+                        G.z0 + tz * kTileZ + 0.5 * kTileZ};
+  double qt[3];
+  const int dec = tile_decision<kTileReach, 4, 8>(r.body, pt, L, G.wall, qt);
+  if (dec == 0 && r.tile_flag[tile] == 0) return;  // far outside and already all zero
+  r.tile_flag[tile] = 0;
+  const int k = atomicAdd(r.counters + 0, 1);
+  r.tiles[k] = tile;
+}
+
+// L1: one thread per segment of the listed tiles
+__global__ void k_remap_l1(const __grid_constant__ RemapParams r) {
+  const Geom& G = r.g;
+  const int nseg = r.counters[0] * kSegPerTile;  // tiles list never overflows (<= box tiles)
+  const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
+  const BodyGeo& b = r.body;
+  const uint32_t full = ((uint32_t)1 << (3 * b.s)) | ((uint32_t)r.id << 16);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nseg; i += gridDim.x * blockDim.x) {
+    const int tile = r.tiles[i / kSegPerTile];
+    const int sg = i % kSegPerTile;
+    int tx, ty, tz;
+    tile_coords(tile, G, tx, ty, tz);
+    const int sx = sg % (kTileX / kSubX), row = sg / (kTileX / kSubX);
+    const int y = ty * kTileY + row % kTileY, z = tz * kTileZ + row / kTileY;
+    if (y >= G.ny || z >= G.nzl) continue;
+    const int x0 = tx * kTileX + sx * kSubX;
+    const double ps[3] = {x0 + 0.5 * kSubX, y + 0.5, G.z0 + z + 0.5};
+    double qs[3];
+    const int dec = tile_decision<kSubReach, 16, 32>(b, ps, L, G.wall, qs);
+    if (dec == 2) {
+      const int k = atomicAdd(r.counters + 1, 1);
+      if (k < r.seg_cap) {
+        r.segs[k] = ((uint32_t)tile << 5) | (uint32_t)sg;
+        r.segq[k] = make_float4((float)qs[0], (float)qs[1], (float)qs[2], 0.f);
+        continue;
+      }
+      // list full: finish the segment here (exact, serial)
+      for (int c = 0; c < kSubX; ++c) {
+        if (x0 + c >= G.nx) continue;
+        const float off = (float)c + 0.5f - 0.5f * kSubX;
+        const float qc[3] = {(float)qs[0] + (float)b.Q[0] * off, (float)qs[1] + (float)b.Q[1] * off,
+                             (float)qs[2] + (float)b.Q[2] * off};
+        const int cd = cell_decision(b, qc);
+        int cnt = cd == 1 ? (1 << (3 * b.s)) : 0;
+        if (cd == 2)
+          for (int si = 0; si < (1 << (3 * b.s)); ++si)
+            cnt += sample_inside(b, x0 + c, y, G.z0 + z, si, L, G.wall);
+        put_word(r, x0 + c, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
+      }
+      continue;
+    }
+    const uint32_t w = dec == 1 ? full : 0u;
+    for (int c = 0; c < kSubX; ++c)
+      if (x0 + c < G.nx) put_word(r, x0 + c, y, z, w, tile);
+  }
+}
+
+// L2: one thread per cell of the listed segments
+__global__ void k_remap_l2(const __grid_constant__ RemapParams r) {
+  const Geom& G = r.g;
+  const int ncell = min(r.counters[1], r.seg_cap) * kSubX;
+  const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
+  const BodyGeo& b = r.body;
+  const uint32_t full = ((uint32_t)1 << (3 * b.s)) | ((uint32_t)r.id << 16);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ncell; i += gridDim.x * blockDim.x) {
+    const int si = i / kSubX, c = i % kSubX;
+    const uint32_t sgw = r.segs[si];
+    const int tile = (int)(sgw >> 5), sg = (int)(sgw & 31u);
+    int tx, ty, tz;
+    tile_coords(tile, G, tx, ty, tz);
+    const int sx = sg % (kTileX / kSubX), row = sg / (kTileX / kSubX);
+    const int y = ty * kTileY + row % kTileY, z = tz * kTileZ + row / kTileY;
+    const int x = tx * kTileX + sx * kSubX + c;
+    if (x >= G.nx) continue;
+    const float4 q = r.segq[si];
+    const float off = (float)c + 0.5f - 0.5f * kSubX;
+    const float qc[3] = {q.x + (float)b.Q[0] * off, q.y + (float)b.Q[1] * off,
+                         q.z + (float)b.Q[2] * off};
+    const int cd = cell_decision(b, qc);
+    if (cd == 2) {
+      const int k = atomicAdd(r.counters + 2, 1);
+      if (k < r.band_cap) {
+        r.band[k] = ((uint32_t)tile << 8) | (uint32_t)(row * kTileX + sx * kSubX + c);
+        r.bandcnt[k] = 0;
+        continue;
+      }
+      int cnt = 0;  // list full: exact serial count here
+      for (int si = 0; si < (1 << (3 * b.s)); ++si)
+        cnt += sample_inside(b, x, y, G.z0 + z, si, L, G.wall);
+      put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
+      continue;
+    }
+    put_word(r, x, y, z, cd == 1 ? full : 0u, tile);
+  }
+}
+
+__device__ __forceinline__ void band_cell(const RemapParams& r, uint32_t e, int& x, int& y,
+                                          int& z, int& tile) {
+  tile = (int)(e >> 8);
+  const int c = (int)(e & 255u);
+  int tx, ty, tz;
+  tile_coords(tile, r.g, tx, ty, tz);
+  x = tx * kTileX + c % kTileX;
+  y = ty * kTileY + (c / kTileX) % kTileY;
+  z = tz * kTileZ + c / (kTileX * kTileY);
+}
+
+// L3: one thread per (band cell, sub-sample), exact fp64 inside test
+__global__ void k_remap_l3(const __grid_constant__ RemapParams r) {
+  const Geom& G = r.g;
+  const BodyGeo& b = r.body;
+  const int ls = 3 * b.s;
+  const long long items = (long long)min(r.counters[2], r.band_cap) << ls;
+  const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < items;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i >> ls), si = (int)(i & ((1 << ls) - 1));
+    int x, y, z, tile;
+    band_cell(r, r.band[k], x, y, z, tile);
+    if (sample_inside(b, x, y, G.z0 + z, si, L, G.wall)) atomicAdd(r.bandcnt + k, 1);
+  }
+}
+
+// L4: one thread per band cell -> word
+__global__ void k_remap_l4(const __grid_constant__ RemapParams r) {
+  const int n = min(r.counters[2], r.band_cap);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    int x, y, z, tile;
+    band_cell(r, r.band[k], x, y, z, tile);
+    const int cnt = r.bandcnt[k];
+    put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cudaStream_t st) {
+  const int ntile = r.box.n[0] * r.box.n[1] * r.box.n[2];
+  if (ntile <= 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(r.counters, 0, 4 * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  k_remap_l0<<<(ntile + 255) / 256, 256, 0, st>>>(r);
+  k_remap_l1<<<persistent_blocks, 256, 0, st>>>(r);
+  k_remap_l2<<<persistent_blocks, 256, 0, st>>>(r);
+  k_remap_l3<<<persistent_blocks, 256, 0, st>>>(r);
+  k_remap_l4<<<persistent_blocks, 256, 0, st>>>(r);
+  return cudaGetLastError();
+}
+
+}  // namespace psm

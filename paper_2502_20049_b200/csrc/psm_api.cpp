@@ -11,6 +11,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -32,6 +33,7 @@ struct Body {
   bool present = false;
   int kind = 0, s = 0;
   double radius = 0, rbound = 0;
+  double bmin[3] = {0, 0, 0}, bmax[3] = {0, 0, 0};  // body-frame AABB of the shape
   // mesh geometry field (device)
   double o[3] = {0, 0, 0};
   int64_t dims[3] = {0, 0, 0};
@@ -82,6 +84,14 @@ struct psm_ctx {
   int* ft_ids = nullptr;
   double* stage = nullptr;
   size_t stage_bytes = 0;
+  // narrow-band remap lists
+  int* r_counters = nullptr;
+  int* r_tiles = nullptr;
+  uint32_t* r_segs = nullptr;
+  float4* r_segq = nullptr;
+  uint32_t* r_band = nullptr;
+  int* r_bandcnt = nullptr;
+  int seg_cap = 0, band_cap = 0;
   double* pinned = nullptr;  // host staging (ft + err)
   // test-only dense fields
   double *dbg_B = nullptr, *dbg_us = nullptr;
@@ -167,12 +177,25 @@ static void pose_at(const psm_ctx* c, const Body& b, int64_t step, double Q[9], 
   rodrigues(b.w, n, b.Q0, Q);
 }
 
-static void body_box(const psm_ctx* c, const Body& b, const double t[3], int64_t lo[3],
-                     int64_t hi[3]) {
+// world box of the cells the body can touch at pose (Q, t): AABB of the rotated body-frame
+// AABB, dilated by one cell (the kernel's per-cell filter uses the same +-1 margin)
+static void body_box(const psm_ctx* c, const Body& b, const double Q[9], const double t[3],
+                     int64_t lo[3], int64_t hi[3]) {
   (void)c;
+  double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+  for (int k = 0; k < 8; ++k) {
+    const double p[3] = {(k & 1) ? b.bmax[0] : b.bmin[0], (k & 2) ? b.bmax[1] : b.bmin[1],
+                         (k & 4) ? b.bmax[2] : b.bmin[2]};
+    for (int a = 0; a < 3; ++a) {
+      const double w = Q[3 * a] * p[0] + Q[3 * a + 1] * p[1] + Q[3 * a + 2] * p[2];
+      mn[a] = std::min(mn[a], w);
+      mx[a] = std::max(mx[a], w);
+    }
+  }
   for (int a = 0; a < 3; ++a) {
-    lo[a] = (int64_t)std::floor(t[a] - b.rbound - 1.0);
-    hi[a] = (int64_t)std::floor(t[a] + b.rbound + 1.0) + 1;
+    // +2: one cell for the kernel filter margin, one for rounding of the corner transform
+    lo[a] = (int64_t)std::floor(t[a] + mn[a] - 2.0);
+    hi[a] = (int64_t)std::floor(t[a] + mx[a] + 2.0) + 1;
   }
 }
 
@@ -224,9 +247,10 @@ static void add_box(const psm_ctx* c, const int64_t lo[3], const int64_t hi[3],
 
 // region to remap for body b moving to pose t: hull of the old and new boxes if they overlap
 // (after the periodic shift that brings them closest), both boxes otherwise
-static void remap_region(const psm_ctx* c, Body& b, const double t[3], std::vector<Box>& boxes) {
+static void remap_region(const psm_ctx* c, Body& b, const double Q[9], const double t[3],
+                         std::vector<Box>& boxes) {
   int64_t lo[3], hi[3];
-  body_box(c, b, t, lo, hi);
+  body_box(c, b, Q, t, lo, hi);
   if (b.has_box) {
     bool overlap = true;
     int64_t slo[3], shi[3];
@@ -279,6 +303,8 @@ static cudaError_t record(psm_ctx* c, int phase, int which) {
 struct Plan {
   size_t off_A0, off_A1, off_word, off_flag, off_partial, off_overflow, off_err, off_scratch,
       off_ftout, off_ids, off_stage, stage_bytes, total;
+  size_t off_rcnt, off_rtiles, off_rsegs, off_rsegq, off_rband, off_rbandcnt;
+  int seg_cap, band_cap;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -302,6 +328,15 @@ static Plan make_plan(const psm_ctx* c) {
   p.off_scratch = take((size_t)kFtChunks * kMaxBodies * kSlotVals * 8);
   p.off_ftout = take(kMaxBodies * kSlotVals * 8);
   p.off_ids = take(kMaxBodies * 4);
+  // narrow-band remap lists (k_remap.cu); overflow is handled in-kernel (serial fallback)
+  p.seg_cap = (int)std::min<int64_t>(32 * c->ntiles, 1 << 22);
+  p.band_cap = (int)std::min<int64_t>(c->ncell_local, 1 << 23);
+  p.off_rcnt = take(4 * sizeof(int));
+  p.off_rtiles = take((size_t)c->ntiles * 4);
+  p.off_rsegs = take((size_t)p.seg_cap * 4);
+  p.off_rsegq = take((size_t)p.seg_cap * 16);
+  p.off_rband = take((size_t)p.band_cap * 4);
+  p.off_rbandcnt = take((size_t)p.band_cap * 4);
   const size_t plane = (size_t)c->grid.nx * c->grid.ny * 8;
   const size_t per = plane * (size_t)c->Q;
   size_t planes = std::max<size_t>(3, kStageBudget / per);
@@ -339,6 +374,14 @@ static psm_status bind(psm_ctx* c, void* mem, size_t bytes) {
   c->ft_out = reinterpret_cast<double*>(m + p.off_ftout);
   c->ft_ids = reinterpret_cast<int*>(m + p.off_ids);
   c->stage = reinterpret_cast<double*>(m + p.off_stage);
+  c->r_counters = reinterpret_cast<int*>(m + p.off_rcnt);
+  c->r_tiles = reinterpret_cast<int*>(m + p.off_rtiles);
+  c->r_segs = reinterpret_cast<uint32_t*>(m + p.off_rsegs);
+  c->r_segq = reinterpret_cast<float4*>(m + p.off_rsegq);
+  c->r_band = reinterpret_cast<uint32_t*>(m + p.off_rband);
+  c->r_bandcnt = reinterpret_cast<int*>(m + p.off_rbandcnt);
+  c->seg_cap = p.seg_cap;
+  c->band_cap = p.band_cap;
   c->stage_bytes = p.stage_bytes;
   CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->st));
   CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->st));
@@ -447,7 +490,10 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
     if (!b.present) continue;
     std::memcpy(g.Q, b.Qc, sizeof(g.Q));
     std::memcpy(g.t, b.tc, sizeof(g.t));
-    g.rb1 = b.rbound + 1.0;
+    for (int a = 0; a < 3; ++a) {
+      g.lo1[a] = b.bmin[a] - 1.0;
+      g.hi1[a] = b.bmax[a] + 1.0;
+    }
     g.r2 = b.radius * b.radius;
     for (int a = 0; a < 3; ++a) {
       g.o[a] = b.o[a];
@@ -474,23 +520,78 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
     m.t0[2] = (int)(zlo / kTileZ);
     m.n[2] = (int)((zhi - 1) / kTileZ + 1 - m.t0[2]);
     m.first = 0;
+    // bodies whose current box overlaps this box (ascending id order is kept by the bit loop)
+    m.bodymask = 0;
+    for (int id = 1; id <= kMaxBodies; ++id) {
+      const Body& bd = c->bodies[id];
+      if (!bd.present || !bd.has_box) continue;
+      std::vector<Box> pieces;
+      add_box(c, bd.box_lo, bd.box_hi, pieces);
+      for (const Box& pc : pieces) {
+        bool ov = true;
+        for (int a = 0; a < 3; ++a)
+          if (pc.hi[a] <= b.lo[a] || pc.lo[a] >= b.hi[a]) ov = false;
+        if (ov) {
+          m.bodymask |= 1u << id;
+          break;
+        }
+      }
+    }
+    if (!m.bodymask) {
+      // nothing can be inside: still launched so the words/flags of the box are cleared
+    }
     tb.push_back(m);
   }
+  static const bool stats_on = std::getenv("PSM_MAP_STATS") != nullptr;
+  unsigned long long* dstats = nullptr;
+  if (stats_on) {
+    CUDA_TRY(c, cudaMalloc(&dstats, 8 * 8));
+    CUDA_TRY(c, cudaMemsetAsync(dstats, 0, 8 * 8, c->st));
+  }
+  mp.stats = dstats;
   if (record(c, 0, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
-  for (size_t i = 0; i < tb.size(); i += kMaxBoxes) {
-    const size_t nb = std::min<size_t>(kMaxBoxes, tb.size() - i);
-    int total = 0;
-    for (size_t k = 0; k < nb; ++k) {
-      mp.box[k] = tb[i + k];
-      mp.box[k].first = total;
-      total += mp.box[k].n[0] * mp.box[k].n[1] * mp.box[k].n[2];
+  static const bool force_general = std::getenv("PSM_REMAP_GENERAL") != nullptr;
+  for (size_t i = 0; i < tb.size(); ++i) {
+    if (__builtin_popcount(tb[i].bodymask) == 1 && !force_general) {
+      // one body in the box: narrow-band pipeline (k_remap.cu)
+      RemapParams r;
+      std::memset(&r, 0, sizeof(r));
+      r.g = c->geom;
+      r.box = tb[i];
+      r.id = __builtin_ctz(tb[i].bodymask);
+      r.body = mp.bodies[r.id];
+      r.word = c->word;
+      r.tile_flag = c->tile_flag;
+      r.counters = c->r_counters;
+      r.tiles = c->r_tiles;
+      r.segs = c->r_segs;
+      r.segq = c->r_segq;
+      r.band = c->r_band;
+      r.bandcnt = c->r_bandcnt;
+      r.seg_cap = c->seg_cap;
+      r.band_cap = c->band_cap;
+      CUDA_TRY(c, launch_remap_single(r, 148 * 8, c->st));
+      c->launches += 5;
+      continue;
     }
-    mp.nbox = (int)nb;
-    mp.ntiles = total;
+    // general box (several bodies may cover its cells): one launch, 3D grid of its tiles
+    mp.box[0] = tb[i];
+    mp.nbox = 1;
+    mp.ntiles = tb[i].n[0] * tb[i].n[1] * tb[i].n[2];
     CUDA_TRY(c, launch_map(mp, c->st));
     c->launches += 1;
   }
   if (record(c, 0, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+  if (dstats) {
+    unsigned long long h[8];
+    CUDA_TRY(c, cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    cudaFree(dstats);
+    std::fprintf(stderr,
+                 "[psm map] boxes %zu  8-cell segments: out %llu in %llu cell %llu | "
+                 "cells: out %llu in %llu band %llu | tiles skipped %llu\n",
+                 tb.size(), h[0], h[1], h[2], h[3], h[4], h[5], h[7]);
+  }
   return PSM_OK;
 }
 
@@ -509,7 +610,7 @@ static psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
     }
     std::memcpy(b.Qc, Q, sizeof(Q));
     std::memcpy(b.tc, t, sizeof(t));
-    remap_region(c, b, t, boxes);
+    remap_region(c, b, Q, t, boxes);
     b.mapped_step = step;
   }
   if (boxes.empty()) return PSM_OK;
@@ -815,6 +916,10 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
         FAIL(c, PSM_E_ARG, "sphere radius must be > 0");
       nb.radius = shape->radius;
       nb.rbound = shape->radius;
+      for (int a = 0; a < 3; ++a) {
+        nb.bmin[a] = -shape->radius;
+        nb.bmax[a] = shape->radius;
+      }
     } else if (shape->kind == PSM_MESH) {
       std::string why;
       if (!shape->verts || !shape->tris ||
@@ -825,9 +930,17 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
       if (bits / 8.0 > (double)kGeomCapBytes)
         FAIL(c, PSM_E_OOM, "geometry field exceeds the 1 GiB cap (reduce s)");
       double rb = 0.0;
+      for (int a = 0; a < 3; ++a) {
+        nb.bmin[a] = shape->verts[a];
+        nb.bmax[a] = shape->verts[a];
+      }
       for (int64_t k = 0; k < shape->nverts; ++k) {
         const double* v = shape->verts + 3 * k;
         rb = std::max(rb, std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]));
+        for (int a = 0; a < 3; ++a) {
+          nb.bmin[a] = std::min(nb.bmin[a], v[a]);
+          nb.bmax[a] = std::max(nb.bmax[a], v[a]);
+        }
       }
       nb.rbound = rb;
       std::vector<uint8_t> field, mask;
@@ -869,6 +982,23 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
   b.step0 = c->step;
   c->ft_valid = false;
   return remap(c, std::vector<int>{id}, c->step);
+}
+
+psm_status psm_voxelize(const double* verts, int64_t nverts, const int32_t* tris, int64_t ntris,
+                        int32_t s, double origin[3], int64_t dims[3], uint8_t* bits) {
+  if (!verts || !tris || !origin || !dims) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null argument");
+  if (s < 0 || s > 3) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "s must be in 0..3");
+  std::string why;
+  if (check_mesh(verts, nverts, tris, ntris, &why) != 0) FAIL((psm_ctx*)nullptr, PSM_E_MESH, why);
+  int64_t cells[3];
+  geometry_extent(verts, nverts, s, origin, cells);
+  for (int a = 0; a < 3; ++a) dims[a] = cells[a] << s;
+  if (bits) {
+    std::vector<uint8_t> field;
+    voxelize_mesh(verts, nverts, tris, ntris, s, origin, cells, field);
+    std::memcpy(bits, field.data(), field.size());
+  }
+  return PSM_OK;
 }
 
 psm_status psm_remove_body(psm_ctx* c, int32_t id) {

@@ -13,7 +13,13 @@ constexpr int kTileX = 32;       // one warp along x (coalesced SoA rows)
 constexpr int kTileY = 4;
 constexpr int kTileZ = 2;
 constexpr int kTileCells = kTileX * kTileY * kTileZ;  // 256 threads = one collide/map block
-constexpr int kMaxBoxes = 64;    // remap boxes per launch
+constexpr int kMaxBoxes = 1;     // remap boxes per launch (one launch per box)
+// Chebyshev reach (in LBM cells) of a tile's sub-samples from the tile centre, plus one:
+// half-diagonal of a 32x4x2 tile = sqrt(16^2 + 2^2 + 1^2) = 16.16 -> brick offset <= 17
+constexpr int kTileReach = 18;
+// second level: 8x4x2 sub-tiles (half-diagonal sqrt(4^2 + 2^2 + 1^2) = 4.58 -> offset <= 5)
+constexpr int kSubX = 8;
+constexpr int kSubReach = 6;
 constexpr int kSlotVals = 12;    // F/T partial: m[3], (x_c-R) x m [3], |m| [3], |(x_c-R) x m| [3]
 
 // ------------------------------------------------------------------------------ stencils ----
@@ -60,7 +66,8 @@ struct BodyKin {
 struct BodyGeo {
   double Q[9];      // body -> world, row major; sample maps to q = Q^T mi(p - t)
   double t[3];
-  double rb1;       // bounding radius + 1 (conservative cell filter |mi(x_c - t)|_a <= rb1)
+  double lo1[3];    // body-frame AABB - 1: a cell whose centre maps outside [lo1, hi1] has
+  double hi1[3];    // every sub-sample outside the body (samples lie within sqrt(3)/2)
   double r2;        // sphere: r*r
   double o[3];      // mesh: geometry-field origin (body frame, integer valued)
   int dims_b[3];    // mesh: field extent in bricks (LBM cells)
@@ -69,7 +76,7 @@ struct BodyGeo {
   int words;        // uint64 words per brick = max(1, 8^s / 64)
   int present;
   const unsigned long long* bits;  // [brick][words]
-  const uint8_t* mask;             // [brick]: 1 dilated-all-in, 2 dilated-all-out, 0 otherwise
+  const uint8_t* mask;             // [brick] flag bits, see pack_bricks (voxelize.cpp)
 };
 
 // ---------------------------------------------------------------------- launch params -----
@@ -104,19 +111,39 @@ struct CollideParams {
 };
 
 struct MapBox {
-  int t0[3];   // first tile (local tile coords)
-  int n[3];    // tiles per axis
-  int first;   // prefix sum of tiles before this box
+  int t0[3];          // first tile (local tile coords)
+  int n[3];           // tiles per axis
+  int first;          // prefix sum of tiles before this box
+  uint32_t bodymask;  // bit id: body id's current box overlaps this box
 };
 
 struct MapParams {
   Geom g;
   uint32_t* word;
   uint8_t* tile_flag;
+  unsigned long long* stats;  // optional diagnostics (PSM_MAP_STATS): tiles by decision, cells
+                              // by decision, sub-samples evaluated
   int nbox;
   int ntiles;
   MapBox box[kMaxBoxes];
   BodyGeo bodies[kMaxBodies + 1];
+};
+
+// single-body narrow-band remap (k_remap.cu)
+struct RemapParams {
+  Geom g;
+  MapBox box;
+  BodyGeo body;
+  int id;
+  uint32_t* word;
+  uint8_t* tile_flag;
+  int* counters;        // [0] tiles, [1] segments, [2] band cells
+  int* tiles;           // listed tiles
+  uint32_t* segs;       // listed segments: tile << 5 | segment
+  float4* segq;         // body-frame segment centres
+  uint32_t* band;       // narrow-band cells: tile << 8 | cell-in-tile
+  int* bandcnt;         // their inside counts
+  int seg_cap, band_cap;
 };
 
 #if defined(__CUDACC__)

@@ -12,8 +12,9 @@ namespace psm {
 cudaError_t launch_collide(int Q, bool fp64, const CollideParams& p, int pat, bool force,
                            bool dbg, cudaStream_t st);
 
-// k_map.cu
+// k_map.cu (general boxes) and k_remap.cu (boxes holding one body)
 cudaError_t launch_map(const MapParams& p, cudaStream_t st);
+cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cudaStream_t st);
 
 // k_state.cu — conversions between the Eq.(4) state and the storage pattern, z-chunked.
 struct StateParams {

@@ -1,0 +1,139 @@
+// psm_map_common.cuh — device helpers of the fraction remap (k_map.cu, k_remap.cu):
+// body-frame transform with the A14 fma order, geometry-field bit lookup, exact sub-sample test,
+// and the conservative region decisions (tile / segment / cell) built on the brick flags.
+#pragma once
+#include "psm_device.cuh"
+
+namespace psm {
+
+__device__ __forceinline__ void body_frame(const BodyGeo& b, const double p[3], const double L[3],
+                                           const int wall[3], double q[3]) {
+  double d[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) d[a] = min_image(__dsub_rn(p[a], b.t[a]), L[a], !wall[a]);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    q[a] = __fma_rn(b.Q[6 + a], d[2], __fma_rn(b.Q[3 + a], d[1], __dmul_rn(b.Q[a], d[0])));
+}
+
+__device__ __forceinline__ int mesh_bit(const BodyGeo& b, const double q[3]) {
+  const double hs = ldexp(1.0, b.s);
+  int g[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double x = floor(__dmul_rn(__dsub_rn(q[a], b.o[a]), hs));
+    if (!(x >= 0.0) || x >= (double)(b.dims_b[a] << b.s)) return 0;
+    g[a] = (int)x;
+  }
+  const int n = 1 << b.s, msk = n - 1;
+  const long long brick =
+      ((long long)(g[2] >> b.s) * b.dims_b[1] + (g[1] >> b.s)) * b.dims_b[0] + (g[0] >> b.s);
+  const int bit = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
+  const unsigned long long w = __ldg(b.bits + brick * b.words + (bit >> 6));
+  return (int)((w >> (bit & 63)) & 1ull);
+}
+
+// exact inside test of sub-sample `si` (0 .. 8^s - 1) of cell (x, y, zg) for body b (reading R1,
+// A14 arithmetic: dyadic sample point, q = Q^T mi(p - t) with the fixed fma order)
+__device__ __forceinline__ int sample_inside(const BodyGeo& b, int x, int y, int zg, int si,
+                                             const double L[3], const int wall[3]) {
+  const int n = 1 << b.s;
+  const double h = ldexp(1.0, -b.s);
+  const int gx = si & (n - 1), gy = (si >> b.s) & (n - 1), gz = si >> (2 * b.s);
+  const double p[3] = {(double)x + (gx + 0.5) * h, (double)y + (gy + 0.5) * h,
+                       (double)zg + (gz + 0.5) * h};
+  double q[3];
+  body_frame(b, p, L, wall, q);
+  if (b.kind == 0) {
+    const double d2 = __fma_rn(q[2], q[2], __fma_rn(q[1], q[1], __dmul_rn(q[0], q[0])));
+    return d2 <= b.r2;
+  }
+  return mesh_bit(b, q);
+}
+
+// Whole-tile decision (block-uniform): 0 = every sub-sample of the tile is outside, 1 = every
+// sub-sample is inside, 2 = decide per cell.  Every sub-sample lies within 16.16 cells of the
+// tile centre, i.e. within kTileReach - 1 bricks of the centre's brick.  qt = body-frame tile
+// centre (used as the base of the per-cell fp32 decisions).
+template <int REACH, int BIT_OUT, int BIT_IN>
+__device__ __forceinline__ int tile_decision(const BodyGeo& b, const double pt[3],
+                                             const double L[3], const int wall[3],
+                                             double qt[3]) {
+  constexpr int kTileReach = REACH;  // brick reach of the region's sub-samples + 1
+  body_frame(b, pt, L, wall, qt);
+  if (b.kind != 1) {
+    const double dist = sqrt(qt[0] * qt[0] + qt[1] * qt[1] + qt[2] * qt[2]);
+    const double r = sqrt(b.r2);
+    if (dist - (double)(kTileReach - 1) > r) return 0;
+    if (dist + (double)(kTileReach - 1) < r) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double d = min_image(pt[a] - b.t[a], L[a], !wall[a]);
+        if (!wall[a] && fabs(d) > 0.5 * L[a] - 2.0 * kTileReach) return 2;
+      }
+      return 1;
+    }
+    return 2;
+  }
+  int bc[3];
+  bool in_field = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double xb = floor(qt[a] - b.o[a]);
+    if (xb < -(double)kTileReach || xb > (double)(b.dims_b[a] - 1 + kTileReach)) return 0;
+    if (xb < 0.0 || xb > (double)(b.dims_b[a] - 1)) in_field = false;
+    bc[a] = (int)xb;
+  }
+  if (!in_field) return 2;
+  const uint8_t m =
+      __ldg(b.mask + ((long long)bc[2] * b.dims_b[1] + bc[1]) * b.dims_b[0] + bc[0]);
+  if (m & BIT_OUT) return 0;
+  if (m & BIT_IN) {
+    // "full" must not straddle a periodic minimum-image cut
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double d = min_image(pt[a] - b.t[a], L[a], !wall[a]);
+      if (!wall[a] && fabs(d) > 0.5 * L[a] - 2.0 * kTileReach) return 2;
+    }
+    return 1;
+  }
+  return 2;
+}
+
+// Conservative per-cell decision in fp32 from the tile-centre transform (error << 0.1 cell):
+// 0 outside, 1 inside, 2 needs exact sampling.  Sub-samples lie within sqrt(3)/2 of the centre.
+__device__ __forceinline__ int cell_decision(const BodyGeo& b, const float qc[3]) {
+  constexpr float kEps = 0.01f;  // >> fp32 error of qc
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (qc[a] < (float)b.lo1[a] - kEps || qc[a] > (float)b.hi1[a] + kEps) return 0;
+  if (b.kind == 0) {
+    const float dist = sqrtf(qc[0] * qc[0] + qc[1] * qc[1] + qc[2] * qc[2]);
+    const float r = sqrtf((float)b.r2);
+    const float reach = 0.8660254f + kEps;
+    if (dist + reach < r) return 1;
+    if (dist - reach > r) return 0;
+    return 2;
+  }
+  int bc[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float xb = floorf(qc[a] - (float)b.o[a]);
+    if (xb < -1.0f || xb > (float)b.dims_b[a]) return 0;  // every sample beyond the field
+    bc[a] = (int)xb;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (bc[a] < 0 || bc[a] >= b.dims_b[a]) return 2;
+  const uint8_t m =
+      __ldg(b.mask + ((long long)bc[2] * b.dims_b[1] + bc[1]) * b.dims_b[0] + bc[0]);
+  if (m & 2) return 1;
+  if (m & 1) return 0;
+  return 2;
+}
+
+// Warp-centric remap of one 32x4x2 tile per block: each warp owns one 32-cell x-row and decides
+// it without block barriers: (1) per 8-cell segment (reach kSubReach bricks), (2) per cell in
+// fp32 (dilated-by-one brick flags), (3) the narrow-band cells' sub-samples packed across the 32
+// lanes (lane -> (cell, sample) pairs) and counted with ballots — exact fp64 per sample.
+}  // namespace psm

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "psm_host.h"
+#include "psm_device.cuh"
 
 namespace psm {
 
@@ -167,8 +168,36 @@ void voxelize_mesh(const double* verts, int64_t nv, const int32_t* tris, int64_t
 }
 
 // Pack into LBM-cell bricks of (2^s)^3 bits (words = max(1, 8^s/64) uint64 each) and build the
-// dilated mask: 1 if the brick and its 26 neighbours are all-inside, 2 if all-outside (cells
-// beyond the field count as outside), 0 otherwise.
+// per-brick flags the remap kernel's exact early-outs use (cells beyond the field count as
+// all-outside):
+//   bit0: the brick and its 26 neighbours are all-outside   (one cell's sub-samples)
+//   bit1: the brick and its 26 neighbours are all-inside
+//   bit2: every brick within Chebyshev distance kTileReach is all-outside (a whole tile)
+//   bit3: every brick within Chebyshev distance kTileReach is all-inside
+//   bit4/bit5: the same within kSubReach (an 8x4x2 sub-tile)
+static void box_or(std::vector<uint8_t>& v, int64_t bx, int64_t by, int64_t bz, int r) {
+  // in place: v := OR of v over the L-infinity ball of radius r (separable running counts);
+  // cells beyond the grid contribute 0
+  std::vector<uint8_t> tmp(v.size());
+  auto pass = [&](int64_t n, int64_t stride, int64_t lines, auto line_base) {
+#pragma omp parallel for schedule(static)
+    for (int64_t l = 0; l < lines; ++l) {
+      const int64_t b0 = line_base(l);
+      int cnt = 0;
+      for (int64_t i = 0; i < std::min<int64_t>(n, r); ++i) cnt += v[(size_t)(b0 + i * stride)];
+      for (int64_t i = 0; i < n; ++i) {
+        if (i + r < n) cnt += v[(size_t)(b0 + (i + r) * stride)];
+        if (i - r - 1 >= 0) cnt -= v[(size_t)(b0 + (i - r - 1) * stride)];
+        tmp[(size_t)(b0 + i * stride)] = cnt > 0;
+      }
+    }
+    v.swap(tmp);
+  };
+  pass(bx, 1, by * bz, [&](int64_t l) { return l * bx; });
+  pass(by, bx, bx * bz, [&](int64_t l) { return (l / bx) * bx * by + (l % bx); });
+  pass(bz, bx * by, bx * by, [&](int64_t l) { return l; });
+}
+
 void pack_bricks(const std::vector<uint8_t>& bits, int s, const int64_t dims_cells[3],
                  std::vector<unsigned long long>& words, std::vector<uint8_t>& mask,
                  int* words_per_brick) {
@@ -179,7 +208,7 @@ void pack_bricks(const std::vector<uint8_t>& bits, int s, const int64_t dims_cel
   const int64_t NX = bx << s, NY = by << s;
   const int64_t nb = bx * by * bz;
   words.assign((size_t)(nb * W), 0ull);
-  std::vector<uint8_t> cls((size_t)nb, 0);  // 1 full, 2 empty, 0 mixed
+  std::vector<uint8_t> any_in((size_t)nb, 0), any_out((size_t)nb, 0);
 #pragma omp parallel for schedule(static)
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t ix = b % bx, iy = (b / bx) % by, iz = b / (bx * by);
@@ -194,24 +223,35 @@ void pack_bricks(const std::vector<uint8_t>& bits, int s, const int64_t dims_cel
             ++ones;
           }
         }
-    cls[(size_t)b] = ones == n * n * n ? 1 : (ones == 0 ? 2 : 0);
+    any_in[(size_t)b] = ones > 0;
+    any_out[(size_t)b] = ones < n * n * n;
   }
+  // "beyond the field" is outside: any_out must be 1 there, which box_or cannot see, so the
+  // all-inside flags additionally require the whole ball to lie inside the field
+  std::vector<uint8_t> in1 = any_in, out1 = any_out, inK = any_in, outK = any_out;
+  std::vector<uint8_t> inS = any_in, outS = any_out;
+  box_or(in1, bx, by, bz, 1);
+  box_or(out1, bx, by, bz, 1);
+  box_or(inK, bx, by, bz, kTileReach);
+  box_or(outK, bx, by, bz, kTileReach);
+  box_or(inS, bx, by, bz, kSubReach);
+  box_or(outS, bx, by, bz, kSubReach);
   mask.assign((size_t)nb, 0);
 #pragma omp parallel for schedule(static)
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t ix = b % bx, iy = (b / bx) % by, iz = b / (bx * by);
-    bool all_in = true, all_out = true;
-    for (int dz = -1; dz <= 1; ++dz)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-          const int64_t x = ix + dx, y = iy + dy, z = iz + dz;
-          uint8_t c = 2;
-          if (x >= 0 && y >= 0 && z >= 0 && x < bx && y < by && z < bz)
-            c = cls[(size_t)((z * by + y) * bx + x)];
-          if (c != 1) all_in = false;
-          if (c != 2) all_out = false;
-        }
-    mask[(size_t)b] = all_in ? 1 : (all_out ? 2 : 0);
+    auto inside_field = [&](int r) {
+      return ix - r >= 0 && iy - r >= 0 && iz - r >= 0 && ix + r < bx && iy + r < by &&
+             iz + r < bz;
+    };
+    uint8_t m = 0;
+    if (!in1[(size_t)b]) m |= 1;
+    if (!out1[(size_t)b] && inside_field(1)) m |= 2;
+    if (!inK[(size_t)b]) m |= 4;
+    if (!outK[(size_t)b] && inside_field(kTileReach)) m |= 8;
+    if (!inS[(size_t)b]) m |= 16;
+    if (!outS[(size_t)b] && inside_field(kSubReach)) m |= 32;
+    mask[(size_t)b] = m;
   }
 }
 

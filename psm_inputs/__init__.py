@@ -80,6 +80,17 @@ def rot90(axis: int, k: int) -> np.ndarray:
     return np.array([[c, -s, 0], [s, c, 0], [0, 0, 1]], np.float64)
 
 
+def cror_rotor(front: bool, faces: str = "full"):
+    """Synthetic CROR rotor of BASELINE config c5 (SURVEY §8(d) recipe): front rotor 12 blades,
+    tip 200; rear rotor 10 blades, tip 180; propeller_mesh geometry scaled from the c3 recipe
+    (hub r=12, length 48, chord 28->12, pitch 55->20 deg, 4-cell section at tip 110).
+    faces="full": ~0.6 M faces per rotor (P:284's ~1.2 M for the pair); "small" for tests."""
+    n_bl, tip = (12, 200.0) if front else (10, 180.0)
+    n_st, n_pts, hub = (200, 128, 256) if faces == "full" else (16, 24, 32)
+    return propeller_mesh(n_blades=n_bl, scale=tip / 110.0, n_st=n_st, n_pts=n_pts,
+                          hub_seg=hub)
+
+
 # ----------------------------------------------------------------------- BASELINE configs ---
 CONFIGS = {
     # c1: D3Q19 PSM fp64, 32^3 periodic, stationary sphere r=6 at a lattice vertex, tau=0.8

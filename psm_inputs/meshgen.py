@@ -94,34 +94,32 @@ def _blade(r0, r1, n_st, n_pts, chord0, chord1, pitch0, pitch1, thick, phi, swee
     er = np.array([0.0, np.cos(phi), np.sin(phi)])
     et = np.array([0.0, -np.sin(phi), np.cos(phi)])
     ex = np.array([1.0, 0.0, 0.0])
-    verts = []
+    f = np.arange(n_st) / (n_st - 1)
+    r = r0 + (r1 - r0) * f
+    ch = chord0 + (chord1 - chord0) * f
+    b = np.deg2rad(pitch0 + (pitch1 - pitch0) * f)
+    verts = np.empty((n_st, n_pts, 3))
     for k in range(n_st):
-        f = k / (n_st - 1)
-        r = r0 + (r1 - r0) * f
-        ch = chord0 + (chord1 - chord0) * f
-        b = np.deg2rad(pitch0 + (pitch1 - pitch0) * f)
-        sec = _naca_section(n_pts, thick, ch)
-        dc = np.cos(b) * ex + np.sin(b) * et     # chordwise direction
-        dn = -np.sin(b) * ex + np.cos(b) * et    # thickness direction
-        off = sweep * f * ex
-        for p in sec:
-            verts.append(r * er + p[0] * dc + p[1] * dn + off)
+        sec = _naca_section(n_pts, thick, ch[k])
+        dc = np.cos(b[k]) * ex + np.sin(b[k]) * et     # chordwise direction
+        dn = -np.sin(b[k]) * ex + np.cos(b[k]) * et    # thickness direction
+        verts[k] = r[k] * er + sec[:, :1] * dc + sec[:, 1:] * dn + sweep * f[k] * ex
+    verts = verts.reshape(-1, 3)
     m = n_pts
+    caps = np.stack([verts[:m].mean(0), verts[(n_st - 1) * m:].mean(0)])
     base = len(verts)
-    # cap centres
-    verts.append(np.mean(verts[0:m], axis=0))
-    verts.append(np.mean(verts[(n_st - 1) * m:n_st * m], axis=0))
-    tris = []
-    for k in range(n_st - 1):
-        for j in range(m):
-            a, b = k * m + j, k * m + (j + 1) % m
-            c, d = (k + 1) * m + j, (k + 1) * m + (j + 1) % m
-            tris.append([a, b, d])
-            tris.append([a, d, c])
-    for j in range(m):
-        tris.append([base, (j + 1) % m, j])
-        tris.append([base + 1, (n_st - 1) * m + j, (n_st - 1) * m + (j + 1) % m])
-    return np.array(verts), np.array(tris, np.int64)
+    k = np.arange(n_st - 1)[:, None]
+    j = np.arange(m)[None, :]
+    a = k * m + j
+    bb = k * m + (j + 1) % m
+    c = (k + 1) * m + j
+    d = (k + 1) * m + (j + 1) % m
+    side = np.concatenate([np.stack([a, bb, d], -1).reshape(-1, 3),
+                           np.stack([a, d, c], -1).reshape(-1, 3)])
+    jj = np.arange(m)
+    cap0 = np.stack([np.full(m, base), (jj + 1) % m, jj], -1)
+    cap1 = np.stack([np.full(m, base + 1), (n_st - 1) * m + jj, (n_st - 1) * m + (jj + 1) % m], -1)
+    return np.concatenate([verts, caps]), np.concatenate([side, cap0, cap1]).astype(np.int64)
 
 
 def _orient_outward(verts, tris):

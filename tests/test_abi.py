@@ -92,3 +92,31 @@ def test_simulation_refuses_to_run_without_cuda():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         psm.Simulation(8, 8, 8)
+
+
+@pytest.mark.parametrize("s", [0, 1, 2])
+def test_product_voxelizer_matches_oracle_bit_exact(s):
+    """The library's row-binned voxelizer (csrc/voxelize.cpp) and the oracle's plain per-row
+    one implement reading A15 independently; their geometry fields must agree bit for bit."""
+    import oracle
+    import psm_inputs as pi
+    for v, t in (pi.propeller_mesh(n_blades=5, scale=0.12, n_st=10, n_pts=20, hub_seg=20),
+                 pi.uv_sphere_mesh(4.3, 12, 24), pi.box_mesh([-2.5, -1.0, -3.0], [2.0, 3.0, 1.5])):
+        o1, b1 = psm.psm_voxelize(v, t, s)
+        o2, b2 = oracle.voxelize(v, t, s)
+        assert np.array_equal(o1, o2)
+        assert b1.shape == b2.shape and np.array_equal(b1, b2)
+        assert b1.sum() > 0
+
+
+def test_voxelize_rejects_open_mesh():
+    import psm_inputs as pi
+    v, t = pi.box_mesh([0, 0, 0], [1, 1, 1])
+    with pytest.raises(psm.PSMError) as e:
+        psm.psm_voxelize(v, t[:-1], 1)
+    assert e.value.code == psm.PSM_E_MESH
+    t2 = t.copy()
+    t2[0, 0] = 99
+    with pytest.raises(psm.PSMError) as e:
+        psm.psm_voxelize(v, t2, 1)
+    assert e.value.code == psm.PSM_E_MESH

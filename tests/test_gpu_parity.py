@@ -232,3 +232,64 @@ def test_write_read_roundtrip_and_equilibrium():
     s.init_equilibrium(rho, u)
     r2, u2 = s.velocity()
     assert np.allclose(r2, rho, atol=1e-14) and np.allclose(u2, u, atol=1e-14)
+
+
+@pytest.mark.parametrize("s", [1, 2])
+def test_cror_rotor_fractions_bit_exact_large(s):
+    """A 12-blade rotor (tip 55 cells, coarse CROR recipe) rotating about x in a 128^3 box: the
+    remap's tile-level (18-brick reach) and cell-level early-outs must reproduce the oracle's
+    brute-force counts bit for bit at several poses; then 3 coupled steps."""
+    v, tr = pi.propeller_mesh(n_blades=12, scale=55.0 / 110.0, n_st=16, n_pts=24, hub_seg=32)
+    n = 128
+    w = (0.004, 0.0, 0.0)
+    o = oracle.Oracle(n, n, n, 19, 0.6, (0, 0, 0), 1, 1)
+    g = _sim(nx=n, ny=n, nz=n, Q=19, tau=0.6, prec="f32", sc=1, bmode=1)
+    o.set_mesh(1, v, tr, s)
+    rho, u = pi.perturbed_flow((n, n, n), 3, u0=(0.02, 0, 0), u_amp=0.001)
+    o.init_equilibrium(rho, u)
+    g.init_equilibrium(rho, u)
+    t = (60.3, 64.0, 63.7)
+    for k, ang in enumerate((0.0, 0.37, 1.1 - 0.004)):
+        Q = pi.rotation_about([1, 0, 0], ang) @ pi.rotation_about([0.2, 1, 0], 0.05)
+        o.set_pose(1, Q, t, (0, 0, 0), w)
+        o.map()
+        if k == 0:
+            g.set_mesh(1, v, tr, s, Q, t, (0, 0, 0), w)
+        else:
+            g.set_pose(1, Q, t, (0, 0, 0), w)
+        Bo, ido, co, _ = o.fractions()
+        Bg, idg, cg = g.fractions()
+        assert np.array_equal(co, cg), (k, int((co != cg).sum()))
+        assert np.array_equal(Bo, Bg)
+        assert co.sum() > 1000
+    for k in range(3):  # explicit poses on both sides (A13); k = 0 is the last checked pose
+        if k > 0:
+            Q = (pi.rotation_about([1, 0, 0], 1.1 - 0.004 + 0.004 * k)
+                 @ pi.rotation_about([0.2, 1, 0], 0.05))
+            o.set_pose(1, Q, t, (0, 0, 0), w)
+            o.map()
+            g.set_pose(1, Q, t, (0, 0, 0), w)
+        o.step(1)
+        g.step(1)
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F32_TOL
+    ok, info = _ft_close(g.force_torque(1), o.force_torque(1), rel=1e-4)
+    assert ok, info
+
+
+def test_two_bodies_with_overlapping_boxes():
+    """Two bodies whose remap boxes overlap (a sphere passing next to a rotating mesh): those
+    boxes go through the general multi-body remap kernel; max-eps / lower-id rule (A18)."""
+    v, tr = pi.propeller_mesh(n_blades=4, scale=0.09, n_st=8, n_pts=16, hub_seg=16)
+    w = np.array([0.0, 0.03, 0.0])
+
+    def pose_mesh(k):
+        return oracle.pose_advance(np.eye(3), [24.0, 20.0, 18.2], [0, 0, 0], w, k,
+                                   [48, 40, 36], [1, 1, 1])
+
+    vs = np.array([0.0, 0.0, 1.0 / 16])
+    bodies = [dict(id=2, kind="mesh", verts=v, tris=tr, s=1, pose=pose_mesh, w=w),
+              dict(id=5, kind="sphere", r=4.0, s=2, v=vs,
+                   pose=lambda k: (np.eye(3), tuple(np.array([24.0, 20.0, 28.0]) + k * vs)))]
+    o, g = _run_pair(48, 40, 36, 19, 0.7, (0, 0, 0), 3, 1, "f64", "two_array", bodies, 24, 13,
+                     u0=(0.02, 0.0, 0.0))
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL

@@ -1,0 +1,5 @@
+# full GPU check: tests, benches, launch list (1 GPU)
+set -x
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; echo rc=$? >> gpurun_out/gputests.log
+timeout 600 python bench.py --steps 50 --warmup 5 > gpurun_out/bench_c5w.json 2> gpurun_out/bench_c5w.err
+for c in c4 c4aa c3f64; do timeout 300 python bench.py --config $c --steps 30 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
