@@ -190,12 +190,30 @@ def run_reference(args, wl, rank, world):
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
 # ---------------------------------------------------------------------------- GPU leg -----
+def _json_out():
+    """The driver reads ONE JSON line from stdout; libraries (NCCL prints its version banner)
+    must not write there.  Route fd 1 to stderr and keep a private handle for the result."""
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    return os.fdopen(saved, "w")
+
+
+OUT = None
+
+
+def emit(line: dict):
+    OUT.write(json.dumps(line) + "\n")
+    OUT.flush()
+
+
 def main():
+    global OUT
+    OUT = _json_out()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -238,6 +256,7 @@ def main():
     z0, nzl = sim.z0, sim.nzl
     sim.init_equilibrium(None, None)
     nbodies = 0
+    body_poses = []  # (Q0, t0, v, w) per body, in id order
     for r in range(world):
         zc = (nzg * r) // world + ((nzg * (r + 1)) // world - (nzg * r) // world) / 2
         if wl.get("rotors"):
@@ -245,11 +264,13 @@ def main():
             for k, front in enumerate((True, False)):
                 v, t = pi.cror_rotor(front)
                 w = (wl["omega"] if front else -wl["omega"], 0.0, 0.0)
-                sim.set_mesh(1 + 2 * r + k, v, t, wl["s"], np.eye(3),
-                             (200.0 if front else 330.0, ny / 2, zc), (0, 0, 0), w)
+                tpos = (200.0 if front else 330.0, ny / 2, zc)
+                sim.set_mesh(1 + 2 * r + k, v, t, wl["s"], np.eye(3), tpos, (0, 0, 0), w)
+                body_poses.append((np.eye(3), tpos, (0.0, 0.0, 0.0), w))
                 nbodies += 1
         else:  # one moving sphere per GPU slab, centred in it
             sim.set_sphere(1 + r, wl["r"], wl["s"], np.eye(3), (nx / 2, ny / 2, zc), wl["v"])
+            body_poses.append((np.eye(3), (nx / 2, ny / 2, zc), wl["v"], (0.0, 0.0, 0.0)))
             nbodies += 1
     stream = torch.cuda.current_stream()
 
@@ -289,37 +310,53 @@ def main():
     achieved = bpu * cells_local / (avg / 1e3) / 1e9 if coll_n else None
     step_gbs = bpu * cells_local * args.steps / (ms / 1e3) / 1e9
 
-    # end-to-end through the public API with host buffers: upload of the initial fields,
-    # per-step host pose in (closed form, 96 B) and force/torque out (48 B), final readback
+    # end-to-end through the public API with host buffers (the coupled-simulation loop a user
+    # runs): every step the host computes each body's pose in closed form and hands it to
+    # psm_set_body (H2D, 144 B per body: pose + velocity), runs psm_step(1), and reads every
+    # body's force/torque back (D2H, 96 B per body + the 8 B error word).  The one-off field
+    # upload (psm_init_equilibrium from pinned host rho/u) and readback (psm_read_velocity) are
+    # timed separately and reported as setup_ms / readback_ms.
     e2e = None
     if not args.no_e2e:
+        import math
         shape = (nzl, ny, nx)
         rho_h = torch.ones(shape, dtype=torch.float64).pin_memory().numpy()
         u_h = torch.zeros((3,) + shape, dtype=torch.float64).pin_memory().numpy()
         u_h[0] = 0.02
         barrier()
-        t_start = time.perf_counter()
+        t_a = time.perf_counter()
         sim.init_equilibrium(rho_h, u_h)
+        barrier()
+        t_b = time.perf_counter()
         for k in range(args.steps):
+            for b, (Q0, t0, v, w) in enumerate(body_poses):
+                ang = k * math.sqrt(w[0] ** 2 + w[1] ** 2 + w[2] ** 2)
+                Qk = pi.rotation_about(w, ang) @ Q0 if ang else Q0
+                tk = tuple(t0[a] + k * v[a] for a in range(3))
+                sim.set_pose(1 + b, Qk, tk, v, w)
             sim.step(1)
             for b in range(nbodies):
                 sim.force_torque(1 + b)
-        sim.velocity() if False else None
+        barrier()
+        t_c = time.perf_counter()
         rho_o = np.empty(shape)
         u_o = np.empty((3,) + shape)
         psm.psm_read_velocity(sim.ctx, rho_o, u_o)
         barrier()
-        dt = time.perf_counter() - t_start
+        t_d = time.perf_counter()
+        dt = t_c - t_b
         if dist is not None:
             t = torch.tensor([dt], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        h2d = (rho_h.nbytes + u_h.nbytes) / args.steps
-        d2h = (rho_o.nbytes + u_o.nbytes) / args.steps + 6 * 8 * nbodies
         e2e = {"value": cells_total * args.steps / dt / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "what": "init_equilibrium(host rho,u) + K x (psm_step(1) + psm_force_torque) + "
-                       "psm_read_velocity(host), wall clock"}
+               "h2d_bytes_per_step": 144 * nbodies, "d2h_bytes_per_step": 96 * nbodies + 8,
+               "ms_per_step": dt / args.steps * 1e3,
+               "setup_ms": (t_b - t_a) * 1e3, "setup_h2d_bytes": int(rho_h.nbytes + u_h.nbytes),
+               "readback_ms": (t_d - t_c) * 1e3,
+               "readback_d2h_bytes": int(rho_o.nbytes + u_o.nbytes),
+               "what": "K x [host closed-form pose -> psm_set_body (each body), psm_step(1), "
+                       "psm_force_torque (each body)], wall clock, max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -350,7 +387,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line))
+        emit(line)
     if dist is not None:
         dist.barrier()
         sim.close()

@@ -161,9 +161,10 @@ __global__ void __launch_bounds__(kTileCells)
   const Geom& G = p.g;
   const int x = blockIdx.x * kTileX + threadIdx.x;
   const int y = blockIdx.y * kTileY + threadIdx.y;
-  const int z = blockIdx.z * kTileZ + threadIdx.z;
+  const int tzl = blockIdx.z + p.tz0;
+  const int z = tzl * kTileZ + threadIdx.z;
   const bool act = (x < G.nx) && (y < G.ny) && (z < G.nzl);
-  const int tile = (blockIdx.z * G.gy + blockIdx.y) * G.gx + blockIdx.x;
+  const int tile = (tzl * G.gy + blockIdx.y) * G.gx + blockIdx.x;
   const bool solid_tile = DBG ? true : (p.tile_flag[tile] != 0);
 
   const int nx = G.nx, ny = G.ny;
@@ -364,9 +365,10 @@ __global__ void __launch_bounds__(kTileCells)
 
 // ------------------------------------------------------------------------------ launcher ---
 template <int Q, typename T>
-static cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool dbg,
+static cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool dbg, int ntz,
                             cudaStream_t st) {
-  dim3 grid(p.g.gx, p.g.gy, p.g.gz), block(kTileX, kTileY, kTileZ);
+  if (ntz <= 0) return cudaSuccess;
+  dim3 grid(p.g.gx, p.g.gy, ntz), block(kTileX, kTileY, kTileZ);
   const bool walls = p.g.wall[0] || p.g.wall[1] || p.g.wall[2];
   if (dbg || force) {
     if (dbg && force) k_collide<Q, T, 0, true, true, true><<<grid, block, 0, st>>>(p);
@@ -385,11 +387,11 @@ static cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool db
 }
 
 cudaError_t launch_collide(int Q, bool fp64, const CollideParams& p, int pat, bool force,
-                           bool dbg, cudaStream_t st) {
-  if (Q == 19) return fp64 ? launch_t<19, double>(p, pat, force, dbg, st)
-                           : launch_t<19, float>(p, pat, force, dbg, st);
-  return fp64 ? launch_t<27, double>(p, pat, force, dbg, st)
-              : launch_t<27, float>(p, pat, force, dbg, st);
+                           bool dbg, int ntz, cudaStream_t st) {
+  if (Q == 19) return fp64 ? launch_t<19, double>(p, pat, force, dbg, ntz, st)
+                           : launch_t<19, float>(p, pat, force, dbg, ntz, st);
+  return fp64 ? launch_t<27, double>(p, pat, force, dbg, ntz, st)
+              : launch_t<27, float>(p, pat, force, dbg, ntz, st);
 }
 
 }  // namespace psm

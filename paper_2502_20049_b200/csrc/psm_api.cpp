@@ -103,6 +103,8 @@ struct psm_ctx {
   bool ft_valid = false;
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
+  cudaStream_t comm_st = nullptr;     // halo stream (overlaps the interior collide)
+  cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
   unsigned char nccl_id[128] = {};
   std::string err_msg;
   int64_t launches = 0;
@@ -408,6 +410,12 @@ static psm_status ensure_comm(psm_ctx* c) {
   static_assert(sizeof(id) == sizeof(c->nccl_id), "ncclUniqueId size");
   std::memcpy(&id, c->nccl_id, sizeof(id));
   NCCL_TRY(c, ncclCommInitRank(&c->comm, c->world, id, c->rank));
+  // highest priority: NCCL's blocks are scheduled as soon as interior-collide blocks retire
+  int lo_prio = 0, hi_prio = 0;
+  CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  CUDA_TRY(c, cudaStreamCreateWithPriority(&c->comm_st, cudaStreamNonBlocking, hi_prio));
+  CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_bnd, cudaEventDisableTiming));
+  CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
   return PSM_OK;
 }
 
@@ -427,11 +435,10 @@ static psm_status ensure_mem(psm_ctx* c) {
   return bind(c, m, p.total);
 }
 
-static psm_status halo(psm_ctx* c, void* arr) {
+static psm_status halo(psm_ctx* c, void* arr, cudaStream_t hst) {
   // two-array pull: ship the c_z = +1 populations of the top plane up and the c_z = -1
   // populations of the bottom plane down, straight from/into the SoA planes (no packing)
   if (c->world == 1) return PSM_OK;
-  if (record(c, 3, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
   const int P = c->world, r = c->rank;
   const bool zwall = c->grid.bc[2] == PSM_WALL;
   const int up = (r + 1) % P, down = (r - 1 + P) % P;
@@ -446,15 +453,14 @@ static psm_status halo(psm_ctx* c, void* arr) {
   for (int q = 0; q < c->Q; ++q) {
     const int cz = stc_z(q);
     if (cz > 0) {
-      if (has_up) NCCL_TRY(c, ncclSend(ptr(q, c->nzl), plane, dt, up, c->comm, c->st));
-      if (has_down) NCCL_TRY(c, ncclRecv(ptr(q, 0), plane, dt, down, c->comm, c->st));
+      if (has_up) NCCL_TRY(c, ncclSend(ptr(q, c->nzl), plane, dt, up, c->comm, hst));
+      if (has_down) NCCL_TRY(c, ncclRecv(ptr(q, 0), plane, dt, down, c->comm, hst));
     } else if (cz < 0) {
-      if (has_down) NCCL_TRY(c, ncclSend(ptr(q, 1), plane, dt, down, c->comm, c->st));
-      if (has_up) NCCL_TRY(c, ncclRecv(ptr(q, c->nzl + 1), plane, dt, up, c->comm, c->st));
+      if (has_down) NCCL_TRY(c, ncclSend(ptr(q, 1), plane, dt, down, c->comm, hst));
+      if (has_up) NCCL_TRY(c, ncclRecv(ptr(q, c->nzl + 1), plane, dt, up, c->comm, hst));
     }
   }
   NCCL_TRY(c, ncclGroupEnd());
-  if (record(c, 3, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
   return PSM_OK;
 }
 
@@ -836,6 +842,9 @@ psm_status psm_destroy(psm_ctx* c) {
       cudaEventDestroy(e[1]);
     }
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm_st) cudaStreamDestroy(c->comm_st);
+  if (c->ev_bnd) cudaEventDestroy(c->ev_bnd);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   delete c;
   return PSM_OK;
 }
@@ -1076,14 +1085,40 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
       p.dst = c->A[0];
       pat = (c->step & 1) ? 2 : 1;
     }
-    if (record(c, 1, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
-    CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, c->st));
-    c->launches += 1;
-    if (record(c, 1, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
-    if (c->opt.pattern == PSM_TWO_ARRAY) c->cur ^= 1;
-    // 3. halo exchange of the freshly written array (world > 1)
-    st = halo(c, c->opt.pattern == PSM_TWO_ARRAY ? c->A[c->cur] : c->A[0]);
-    if (st != PSM_OK) return st;
+    const int gz = c->geom.gz;
+    if (c->world == 1 || gz < 3) {
+      if (record(c, 1, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+      p.tz0 = 0;
+      CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, gz, c->st));
+      c->launches += 1;
+      if (record(c, 1, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+      if (c->opt.pattern == PSM_TWO_ARRAY) c->cur ^= 1;
+      if (c->world > 1) {
+        if (record(c, 3, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+        st = halo(c, c->A[c->cur], c->st);
+        if (st != PSM_OK) return st;
+        if (record(c, 3, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+      }
+    } else {
+      // boundary tile layers first, then the halo on the comm stream overlaps the interior
+      if (record(c, 1, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+      p.tz0 = 0;
+      CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, 1, c->st));
+      p.tz0 = gz - 1;
+      CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, 1, c->st));
+      CUDA_TRY(c, cudaEventRecord(c->ev_bnd, c->st));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->comm_st, c->ev_bnd, 0));
+      st = halo(c, p.dst, c->comm_st);
+      if (st != PSM_OK) return st;
+      CUDA_TRY(c, cudaEventRecord(c->ev_halo, c->comm_st));
+      p.tz0 = 1;
+      CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, gz - 2, c->st));
+      c->launches += 3;
+      if (record(c, 1, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+      // the next collide (and any readback) reads the ghost planes: join the halo
+      CUDA_TRY(c, cudaStreamWaitEvent(c->st, c->ev_halo, 0));
+      c->cur ^= 1;
+    }
     c->step += 1;
   }
   // 4. force/torque of the last step: deterministic two-pass reduction, then allreduce

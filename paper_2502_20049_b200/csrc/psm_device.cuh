@@ -107,6 +107,7 @@ struct CollideParams {
   int sc;                 // 1, 2, 3
   int bmode;              // 0 direct, 1 weighted
   long long step;         // for the error word
+  int tz0;                // first tile layer (z) of this launch: blockIdx.z + tz0
   BodyKin bodies[kMaxBodies + 1];
 };
 

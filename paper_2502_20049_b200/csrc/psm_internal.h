@@ -9,8 +9,9 @@
 namespace psm {
 
 // k_collide.cu
+// launches tile layers [p.tz0, p.tz0 + ntz) in z
 cudaError_t launch_collide(int Q, bool fp64, const CollideParams& p, int pat, bool force,
-                           bool dbg, cudaStream_t st);
+                           bool dbg, int ntz, cudaStream_t st);
 
 // k_map.cu (general boxes) and k_remap.cu (boxes holding one body)
 cudaError_t launch_map(const MapParams& p, cudaStream_t st);
