@@ -155,8 +155,16 @@ __device__ __forceinline__ T ld_stream(const T* p) {
   return __ldg(p);
 }
 
+// Minimum resident 256-thread blocks per SM (= register budget 65536 / (256 * n)): enough warps
+// in flight to cover HBM latency without spilling the populations.
+template <int Q, typename T, int PAT>
+constexpr int collide_min_blocks() {
+  // the AA odd step keeps the scatter offsets live as well: one block less for fp32
+  return sizeof(T) == 8 ? 2 : (Q == 19 ? (PAT == 2 ? 3 : 4) : (PAT == 2 ? 2 : 3));
+}
+
 template <int Q, typename T, int PAT, bool WALLS, bool FORCE, bool DBG>
-__global__ void __launch_bounds__(kTileCells)
+__global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT>()))
     k_collide(const __grid_constant__ CollideParams p) {
   const Geom& G = p.g;
   const int x = blockIdx.x * kTileX + threadIdx.x;
