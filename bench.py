@@ -194,6 +194,36 @@ def run_reference(args, wl, rank, world):
     return 0
 
 
+def build_workload(psm, wl: dict, rank: int, world: int, nccl_id=None):
+    """The bench's simulation: the grid of `wl` (nz per GPU stacked in z), rest fluid, and the
+    bodies (a CROR-like rotor pair or one moving sphere per GPU slab; every rank holds every
+    body so the force/torque allreduce is consistent).  Returns (sim, body_poses, nbodies, S)."""
+    import psm_inputs as pi
+    nx, ny, nzg = wl["nx"], wl["ny"], wl["nz"] * world
+    S = 8 if wl["prec"] == "f64" else 4
+    sim = psm.Simulation(nx, ny, nzg, Q=wl["Q"], tau=wl["tau"], bc=(0, 0, 0), prec=wl["prec"],
+                         pattern=wl["pattern"], sc=wl["sc"], bmode=wl["bmode"], rank=rank,
+                         world=world, nccl_id=nccl_id)
+    sim.init_equilibrium(None, None)
+    nbodies = 0
+    body_poses = []  # (Q0, t0, v, w) per body, in id order
+    for r in range(world):
+        zc = (nzg * r) // world + ((nzg * (r + 1)) // world - (nzg * r) // world) / 2
+        if wl.get("rotors"):
+            for k, front in enumerate((True, False)):
+                v, t = pi.cror_rotor(front)
+                w = (wl["omega"] if front else -wl["omega"], 0.0, 0.0)
+                tpos = (200.0 if front else 330.0, ny / 2, zc)
+                sim.set_mesh(1 + 2 * r + k, v, t, wl["s"], np.eye(3), tpos, (0, 0, 0), w)
+                body_poses.append((np.eye(3), tpos, (0.0, 0.0, 0.0), w))
+                nbodies += 1
+        else:
+            sim.set_sphere(1 + r, wl["r"], wl["s"], np.eye(3), (nx / 2, ny / 2, zc), wl["v"])
+            body_poses.append((np.eye(3), (nx / 2, ny / 2, zc), wl["v"], (0.0, 0.0, 0.0)))
+            nbodies += 1
+    return sim, body_poses, nbodies, S
+
+
 # ---------------------------------------------------------------------------- GPU leg -----
 def _json_out():
     """The driver reads ONE JSON line from stdout; libraries (NCCL prints its version banner)
@@ -248,30 +278,9 @@ def main():
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy().tobytes())
 
+    sim, body_poses, nbodies, S = build_workload(psm, wl, rank, world, nccl_id)
     nx, ny, nzg = wl["nx"], wl["ny"], wl["nz"] * world
-    S = 8 if wl["prec"] == "f64" else 4
-    sim = psm.Simulation(nx, ny, nzg, Q=wl["Q"], tau=wl["tau"], bc=(0, 0, 0), prec=wl["prec"],
-                         pattern=wl["pattern"], sc=wl["sc"], bmode=wl["bmode"], rank=rank,
-                         world=world, nccl_id=nccl_id)
     z0, nzl = sim.z0, sim.nzl
-    sim.init_equilibrium(None, None)
-    nbodies = 0
-    body_poses = []  # (Q0, t0, v, w) per body, in id order
-    for r in range(world):
-        zc = (nzg * r) // world + ((nzg * (r + 1)) // world - (nzg * r) // world) / 2
-        if wl.get("rotors"):
-            # counter-rotating pair per GPU slab; every rank holds every body (F/T allreduce)
-            for k, front in enumerate((True, False)):
-                v, t = pi.cror_rotor(front)
-                w = (wl["omega"] if front else -wl["omega"], 0.0, 0.0)
-                tpos = (200.0 if front else 330.0, ny / 2, zc)
-                sim.set_mesh(1 + 2 * r + k, v, t, wl["s"], np.eye(3), tpos, (0, 0, 0), w)
-                body_poses.append((np.eye(3), tpos, (0.0, 0.0, 0.0), w))
-                nbodies += 1
-        else:  # one moving sphere per GPU slab, centred in it
-            sim.set_sphere(1 + r, wl["r"], wl["s"], np.eye(3), (nx / 2, ny / 2, zc), wl["v"])
-            body_poses.append((np.eye(3), (nx / 2, ny / 2, zc), wl["v"], (0.0, 0.0, 0.0)))
-            nbodies += 1
     stream = torch.cuda.current_stream()
 
     def barrier():

@@ -107,6 +107,9 @@ psm_status psm_init_equilibrium(psm_ctx* ctx, const double* rho, const double* u
 psm_status psm_write_pdfs(psm_ctx* ctx, const double* f);
 /* Read the Eq.(4) state f: [Q][nz_l][ny][nx] fp64 (converted from the storage pattern). */
 psm_status psm_read_pdfs(psm_ctx* ctx, double* f);
+/* Read the Eq.(4) state of local planes [z_begin, z_begin + nz): f [Q][nz][ny][nx] fp64 (probes and
+ * sampled checks of large grids).  PSM_E_ARG if the range leaves the local slab. */
+psm_status psm_read_pdfs_planes(psm_ctx* ctx, int64_t z_begin, int64_t nz, double* f);
 /* Read density rho = sum_i f_i [nz_l][ny][nx] and velocity u = sum_i f_i c_i / rho
  * [3][nz_l][ny][nx] of the Eq.(4) state (either pointer may be NULL). */
 psm_status psm_read_velocity(psm_ctx* ctx, double* rho, double* u);

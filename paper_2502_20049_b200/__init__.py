@@ -35,7 +35,8 @@ PHASES = ("map", "collide", "ft_reduce", "halo")
 
 EXPORTED = (
     "psm_create", "psm_destroy", "psm_required_bytes", "psm_bind_memory", "psm_local_extent",
-    "psm_init_equilibrium", "psm_write_pdfs", "psm_read_pdfs", "psm_read_velocity",
+    "psm_init_equilibrium", "psm_write_pdfs", "psm_read_pdfs", "psm_read_pdfs_planes",
+    "psm_read_velocity",
     "psm_set_body", "psm_remove_body", "psm_voxelize", "psm_map_fractions", "psm_step", "psm_force_torque",
     "psm_read_fractions", "psm_debug_set_fields", "psm_get_step", "psm_launch_count",
     "psm_profile", "psm_profile_read", "psm_nccl_id_bytes", "psm_nccl_get_unique_id",
@@ -94,6 +95,7 @@ def load(build_if_missing: bool = True):
         "psm_bind_memory": [P, P, SZ], "psm_local_extent": [P, P, P],
         "psm_init_equilibrium": [P, P, P], "psm_write_pdfs": [P, P], "psm_read_pdfs": [P, P],
         "psm_read_velocity": [P, P, P], "psm_set_body": [P, I32, P, P, P],
+        "psm_read_pdfs_planes": [P, I64, I64, P],
         "psm_remove_body": [P, I32], "psm_map_fractions": [P],
         "psm_voxelize": [P, I64, P, I64, I32, P, P, P], "psm_step": [P, I64],
         "psm_force_torque": [P, I32, P, P, P, P], "psm_read_fractions": [P, P, P, P],
@@ -169,6 +171,10 @@ def psm_write_pdfs(ctx, f):
 
 def psm_read_pdfs(ctx, out):
     _check(load().psm_read_pdfs(ctx, _ptr(out)), ctx)
+
+
+def psm_read_pdfs_planes(ctx, z_begin: int, nz: int, out):
+    _check(load().psm_read_pdfs_planes(ctx, int(z_begin), int(nz), _ptr(out)), ctx)
 
 
 def psm_read_velocity(ctx, rho, u):
@@ -308,6 +314,11 @@ class Simulation:
     def pdfs(self):
         out = np.empty((self.Q,) + self.shape)
         psm_read_pdfs(self.ctx, out)
+        return out
+
+    def pdfs_planes(self, z_begin, nz):
+        out = np.empty((self.Q, nz, self.ny, self.nx))
+        psm_read_pdfs_planes(self.ctx, z_begin, nz, out)
         return out
 
     def velocity(self):

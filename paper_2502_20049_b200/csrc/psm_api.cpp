@@ -711,9 +711,11 @@ static psm_status state_write(psm_ctx* c, const double* host, int mode) {
   return PSM_OK;
 }
 
-static psm_status state_read(psm_ctx* c, double* f, double* rho, double* u) {
+static psm_status state_read(psm_ctx* c, double* f, double* rho, double* u, int64_t zbeg = 0,
+                             int64_t zend = -1) {
   psm_status s = ensure_mem(c);
   if (s != PSM_OK) return s;
+  if (zend < 0) zend = c->nzl;
   const size_t plane = (size_t)c->grid.nx * c->grid.ny;
   const int mode = f ? 0 : 1;
   const int nvals = mode == 0 ? c->Q : 4;
@@ -721,10 +723,10 @@ static psm_status state_read(psm_ctx* c, double* f, double* rho, double* u) {
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(c->nzl,
                                                               (int64_t)(c->stage_bytes / per)));
   const void* arr = (c->opt.pattern == PSM_TWO_ARRAY) ? c->A[c->cur] : c->A[0];
-  const size_t N = (size_t)c->nzl * plane;
+  const size_t N = (size_t)(zend - zbeg) * plane;
   std::vector<double> tmp;
-  for (int64_t za = 0; za < c->nzl; za += chunk) {
-    const int64_t zb = std::min<int64_t>(c->nzl, za + chunk);
+  for (int64_t za = zbeg; za < zend; za += chunk) {
+    const int64_t zb = std::min<int64_t>(zend, za + chunk);
     StateParams p{};
     p.g = c->geom;
     p.A = const_cast<void*>(arr);
@@ -745,12 +747,13 @@ static psm_status state_read(psm_ctx* c, double* f, double* rho, double* u) {
     CUDA_TRY(c, cudaStreamSynchronize(c->st));
     for (int v = 0; v < nvals; ++v) {
       const double* src = &tmp[(size_t)v * nz * plane];
+      const size_t o = (size_t)(za - zbeg) * plane;
       if (mode == 0) {
-        std::memcpy(f + (size_t)v * N + (size_t)za * plane, src, nz * plane * 8);
+        std::memcpy(f + (size_t)v * N + o, src, nz * plane * 8);
       } else if (v == 0) {
-        if (rho) std::memcpy(rho + (size_t)za * plane, src, nz * plane * 8);
+        if (rho) std::memcpy(rho + o, src, nz * plane * 8);
       } else if (u) {
-        std::memcpy(u + (size_t)(v - 1) * N + (size_t)za * plane, src, nz * plane * 8);
+        std::memcpy(u + (size_t)(v - 1) * N + o, src, nz * plane * 8);
       }
     }
   }
@@ -884,6 +887,12 @@ psm_status psm_write_pdfs(psm_ctx* c, const double* f) {
 psm_status psm_read_pdfs(psm_ctx* c, double* f) {
   if (!c || !f) FAIL(c, PSM_E_ARG, "null argument");
   return state_read(c, f, nullptr, nullptr);
+}
+
+psm_status psm_read_pdfs_planes(psm_ctx* c, int64_t z_begin, int64_t nz, double* f) {
+  if (!c || !f) FAIL(c, PSM_E_ARG, "null argument");
+  if (z_begin < 0 || nz < 1 || z_begin + nz > c->nzl) FAIL(c, PSM_E_ARG, "plane range outside the slab");
+  return state_read(c, f, nullptr, nullptr, z_begin, z_begin + nz);
 }
 
 psm_status psm_read_velocity(psm_ctx* c, double* rho, double* u) {

@@ -65,8 +65,8 @@ def cylinder_mesh(radius: float, x0: float, x1: float, n_seg: int = 48):
     tris = []
     for j in range(n_seg):
         a, b = j, (j + 1) % n_seg
-        tris.append([a, n_seg + a, n_seg + b])
-        tris.append([a, n_seg + b, b])
+        tris.append([a, n_seg + b, n_seg + a])  # outward (radial) normals
+        tris.append([a, b, n_seg + b])
         tris.append([c0, b, a])
         tris.append([c1, n_seg + a, n_seg + b])
     return verts, np.array(tris, np.int32)

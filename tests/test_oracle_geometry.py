@@ -221,3 +221,14 @@ def test_p10_voxelizer_matches_winding_number_on_sphere_mesh():
     # inside volume ~ polyhedron volume (divergence theorem)
     vol = np.einsum("ij,ij->i", v[tr[:, 0]], np.cross(v[tr[:, 1]], v[tr[:, 2]])).sum() / 6
     assert abs(bits.sum() * h ** 3 / vol - 1) < 0.05
+
+
+def test_p10_voxel_volume_matches_mesh_volume():
+    """Voxel volume (inside geometry cells x h^3) approaches the polyhedron volume from the
+    divergence theorem (consistently oriented closed meshes), for the propeller recipe."""
+    v, tr = pi.propeller_mesh(n_blades=5, scale=0.2, n_st=12, n_pts=24, hub_seg=32)
+    vol = np.einsum("ij,ij->i", v[tr[:, 0]], np.cross(v[tr[:, 1]], v[tr[:, 2]])).sum() / 6.0
+    for s in (1, 2):
+        _, bits = oracle.voxelize(v, tr, s)
+        got = bits.sum() * 8.0 ** -s
+        assert abs(got / vol - 1) < (0.06 if s == 1 else 0.03), (s, got, vol)
