@@ -56,6 +56,10 @@ typedef enum { PSM_TWO_ARRAY = 0, PSM_AA = 1 } psm_pattern;
 /* Domain boundary per axis: periodic, or half-way bounce-back resting wall. */
 typedef enum { PSM_PERIODIC = 0, PSM_WALL = 1 } psm_bc;
 typedef enum { PSM_SPHERE = 0, PSM_MESH = 1 } psm_shape_kind;
+/* Fluid collision operator: SRT (Eq.(2)) or TRT (two relaxation times, one of
+ * the operators the paper lists; symmetric rate 1/tau, antisymmetric 1/tau_- with
+ * tau_- = 1/2 + Lambda/(tau - 1/2)). */
+typedef enum { PSM_SRT = 0, PSM_TRT = 1 } psm_collision;
 
 typedef struct {
   int64_t nx, ny, nz; /* GLOBAL extents in cells, each >= 1                                  */
@@ -73,6 +77,9 @@ typedef struct {
   const void* nccl_unique_id; /* 128-byte ncclUniqueId (fresh per context) shared by all ranks; NULL iff world==1 */
   void* cuda_stream;     /* cudaStream_t to enqueue on (e.g. torch's current stream); NULL = */
                          /* the legacy default stream                                       */
+  int32_t collision;     /* psm_collision: fluid operator Omega^F                            */
+  double trt_magic;      /* TRT magic parameter Lambda = (tau - 1/2)(tau_- - 1/2) (> 0);     */
+                         /* 3/16 puts half-way bounce-back walls exactly mid-link            */
 } psm_options;
 
 /* Create a context.  Host-only: validates and plans the layout; no device memory yet.  With

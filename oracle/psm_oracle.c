@@ -133,8 +133,27 @@ double orc_weight_fraction(double eps, double tau, int mode) {
  * m = B sum_i Omega^S_i c_i (the summand of Eq.(10)).  g is the test-only Guo body force (A-P12):
  * u = (j + g/2)/rho and Omega^F gains (1 - 1/(2 tau)) w_i [(c_i - u)/c_s^2 + (c_i.u) c_i/c_s^4].g.
  * Returns 0, or 1 if rho <= 0 or a value is non-finite (error rule of S:66/S:93). */
+/* Fluid operator kind: 0 = SRT, Eq.(2); 1 = TRT (two relaxation times, listed by the paper
+ * among lbmpy's operators; standard definition: with f^+-_i = (f_i +- f_ibar)/2,
+ * Omega_i = -(1/tau)(f^+_i - f^eq+_i) - (1/tau_-)(f^-_i - f^eq-_i), tau_- = 1/2 + magic/(tau - 1/2);
+ * the Guo source splits the same way with (1 - 1/(2 tau)) and (1 - 1/(2 tau_-))). */
+static int collide_cell_impl(int Q, const double* f, double tau, int sc, double B,
+                             const double us[3], const double g[3], int coll, double magic,
+                             double* fstar, double m[3]);
+
 int orc_collide_cell(int Q, const double* f, double tau, int sc, double B, const double us[3],
                      const double g[3], double* fstar, double m[3]) {
+  return collide_cell_impl(Q, f, tau, sc, B, us, g, 0, 0.0, fstar, m);
+}
+
+int orc_collide_cell_trt(int Q, const double* f, double tau, double magic, int sc, double B,
+                         const double us[3], const double g[3], double* fstar, double m[3]) {
+  return collide_cell_impl(Q, f, tau, sc, B, us, g, 1, magic, fstar, m);
+}
+
+static int collide_cell_impl(int Q, const double* f, double tau, int sc, double B,
+                             const double us[3], const double g[3], int coll, double magic,
+                             double* fstar, double m[3]) {
   tables_init();
   double rho = 0.0, j[3] = {0.0, 0.0, 0.0};
   for (int i = 0; i < Q; ++i) {
@@ -154,16 +173,34 @@ int orc_collide_cell(int Q, const double* f, double tau, int sc, double B, const
   for (int a = 0; a < 3; ++a) u[a] = (j[a] + 0.5 * g[a]) / rho; /* A4/A5: local pre-collision u */
   double feq[27], fs[27], omF[27], omS[27];
   orc_equilibrium(Q, rho, u, feq);
-  /* Eq.(2): Omega^F_i = -(1/tau)(f_i - f_i^eq) */
+  double src[27];  /* raw Guo source w_i [(c_i - u)/c_s^2 + (c_i.u) c_i / c_s^4] . g */
   for (int i = 0; i < Q; ++i) {
-    omF[i] = -(f[i] - feq[i]) / tau;
-    if (g[0] != 0.0 || g[1] != 0.0 || g[2] != 0.0) {
-      int c[3];
-      stencil_c(Q, i, c);
-      double cu = c[0] * u[0] + c[1] * u[1] + c[2] * u[2];
-      double s = 0.0;
-      for (int a = 0; a < 3; ++a) s += ((c[a] - u[a]) / CS2 + cu * c[a] / (CS2 * CS2)) * g[a];
-      omF[i] += (1.0 - 1.0 / (2.0 * tau)) * stencil_w(Q, i) * s;
+    int c[3];
+    stencil_c(Q, i, c);
+    double cu = c[0] * u[0] + c[1] * u[1] + c[2] * u[2];
+    double s = 0.0;
+    for (int a = 0; a < 3; ++a) s += ((c[a] - u[a]) / CS2 + cu * c[a] / (CS2 * CS2)) * g[a];
+    src[i] = stencil_w(Q, i) * s;
+  }
+  const int forced = (g[0] != 0.0 || g[1] != 0.0 || g[2] != 0.0);
+  if (coll == 0) {
+    /* Eq.(2): Omega^F_i = -(1/tau)(f_i - f_i^eq) */
+    for (int i = 0; i < Q; ++i) {
+      omF[i] = -(f[i] - feq[i]) / tau;
+      if (forced) omF[i] += (1.0 - 1.0 / (2.0 * tau)) * src[i];
+    }
+  } else {
+    /* TRT on the symmetric / antisymmetric parts of each (i, ibar) pair */
+    const double taum = 0.5 + magic / (tau - 0.5);
+    for (int i = 0; i < Q; ++i) {
+      int ib = TOPP[Q][i];
+      double fp = 0.5 * (f[i] + f[ib]), fm = 0.5 * (f[i] - f[ib]);
+      double ep = 0.5 * (feq[i] + feq[ib]), em = 0.5 * (feq[i] - feq[ib]);
+      omF[i] = -(fp - ep) / tau - (fm - em) / taum;
+      if (forced) {
+        double sp = 0.5 * (src[i] + src[ib]), sm = 0.5 * (src[i] - src[ib]);
+        omF[i] += (1.0 - 1.0 / (2.0 * tau)) * sp + (1.0 - 1.0 / (2.0 * taum)) * sm;
+      }
     }
   }
   if (B > 0.0) {
@@ -349,6 +386,8 @@ typedef struct {
   int64_t step;
   int64_t err_cell; /* -1 none */
   int map_all_cells; /* 1: evaluate every cell for every body (no bbox restriction) */
+  int coll;          /* 0 SRT, 1 TRT */
+  double magic;      /* TRT magic parameter */
 } orc_sim;
 
 static int64_t cidx(const orc_sim* S, int x, int y, int z) {
@@ -394,6 +433,10 @@ void orc_set_force(orc_sim* S, const double g[3]) {
   for (int a = 0; a < 3; ++a) S->g[a] = g[a];
 }
 void orc_set_map_all_cells(orc_sim* S, int on) { S->map_all_cells = on; }
+void orc_set_collision(orc_sim* S, int coll, double magic) {
+  S->coll = coll;
+  S->magic = magic;
+}
 
 void orc_init_equilibrium(orc_sim* S, const double* rho, const double* u) {
   int64_t N = (int64_t)S->nx * S->ny * S->nz;
@@ -626,7 +669,7 @@ int orc_step(orc_sim* S) {
         for (int i = 0; i < Q; ++i) f[i] = S->f[(int64_t)i * N + c];
         double us[3] = {S->us[c], S->us[N + c], S->us[2 * N + c]};
         double B = S->B[c];
-        int bad = orc_collide_cell(Q, f, S->tau, S->sc, B, us, S->g, fs, m);
+        int bad = collide_cell_impl(Q, f, S->tau, S->sc, B, us, S->g, S->coll, S->magic, fs, m);
         if (bad && perr[z] < 0) perr[z] = c;
         int id = S->id[c];
         if (B > 0.0) {

@@ -29,6 +29,7 @@ PSM_F64, PSM_F32 = 0, 1
 PSM_TWO_ARRAY, PSM_AA = 0, 1
 PSM_PERIODIC, PSM_WALL = 0, 1
 PSM_SPHERE, PSM_MESH = 0, 1
+PSM_SRT, PSM_TRT = 0, 1
 PSM_MAX_BODIES = 16
 PSM_NUM_PHASES = 4
 PHASES = ("map", "collide", "ft_reduce", "halo")
@@ -52,7 +53,8 @@ class psm_options(C.Structure):
     _fields_ = [("prec", C.c_int32), ("pattern", C.c_int32), ("sc", C.c_int32),
                 ("bmode", C.c_int32), ("body_force", C.c_double * 3), ("rank", C.c_int32),
                 ("world", C.c_int32), ("nccl_unique_id", C.c_void_p),
-                ("cuda_stream", C.c_void_p)]
+                ("cuda_stream", C.c_void_p), ("collision", C.c_int32),
+                ("trt_magic", C.c_double)]
 
 
 class psm_shape(C.Structure):
@@ -263,7 +265,7 @@ class Simulation:
 
     def __init__(self, nx, ny, nz, Q=19, tau=0.8, bc=(0, 0, 0), prec="f64", pattern="two_array",
                  sc=1, bmode=1, body_force=(0.0, 0.0, 0.0), rank=0, world=1, nccl_id=None,
-                 stream=None, device=None):
+                 stream=None, device=None, collision="srt", trt_magic=3.0 / 16.0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2502_20049_b200 needs a CUDA device (no CPU fallback)")
@@ -281,7 +283,8 @@ class Simulation:
                         PSM_TWO_ARRAY if pattern == "two_array" else PSM_AA, sc, bmode,
                         (C.c_double * 3)(*body_force), rank, world,
                         C.cast(self._idbuf, C.c_void_p) if self._idbuf is not None else None,
-                        C.c_void_p(self._stream.cuda_stream))
+                        C.c_void_p(self._stream.cuda_stream),
+                        PSM_TRT if collision == "trt" else PSM_SRT, float(trt_magic))
         self.ctx = psm_create(g, Q, tau, o)
         nbytes = psm_required_bytes(self.ctx)
         self.mem = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)

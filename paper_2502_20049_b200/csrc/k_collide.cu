@@ -24,16 +24,6 @@ __device__ __forceinline__ T feq_q(int q, T rho, T ux, T uy, T uz, T usq15) {
   return T(stc_w<Q>(q)) * rho * (T(1) - usq15 + cu * (T(3) + T(4.5) * cu));
 }
 
-template <int Q, typename T>
-__device__ __forceinline__ T guo_q(int q, T ux, T uy, T uz, const T (&g)[3], T pref) {
-  // (1 - 1/(2 tau)) w_i [3 (c_i - u) + 9 (c_i.u) c_i] . g   (test-only forcing)
-  const T cx = T(stc_x(q)), cy = T(stc_y(q)), cz = T(stc_z(q));
-  const T cu = cx * ux + cy * uy + cz * uz;
-  const T s = (T(3) * (cx - ux) + T(9) * cu * cx) * g[0] + (T(3) * (cy - uy) + T(9) * cu * cy) * g[1] +
-              (T(3) * (cz - uz) + T(9) * cu * cz) * g[2];
-  return pref * T(stc_w<Q>(q)) * s;
-}
-
 __device__ __forceinline__ double weight_fraction(double e, double tau, int mode) {
   // Eq.(6) in fp64, fixed operation order (bit-exact with the method definition, A14)
   if (mode == 0) return e;
@@ -118,17 +108,33 @@ __device__ __forceinline__ T cdot(int q, T ux, T uy, T uz) {
   return r;
 }
 
-// Plain SRT for one cell, f* = f + omega (f^eq - f) (Eq.(1) with Eq.(2)-(3)), pairs (i, ibar)
-// sharing f^eq_i = a + b, f^eq_ibar = a - b with a = w rho (1 - 1.5 u.u + 4.5 (c.u)^2),
-// b = 3 w rho c.u.  Every operation is explicitly rounded.
+// Guo source parts of the pair (i, ibar): symmetric w [-3 u.g + 9 (c.u)(c.g)], antisymmetric
+// w 3 c.g (test-only forcing; TRT weights them with (1 - w+/2) and (1 - w-/2)).
+template <int Q, typename T>
+__device__ __forceinline__ void guo_pair(int i, T ux, T uy, T uz, const T (&g)[3], T& sp, T& sm) {
+  const T cx = T(stc_x(i)), cy = T(stc_y(i)), cz = T(stc_z(i));
+  const T cu = cx * ux + cy * uy + cz * uz;
+  const T cg = cx * g[0] + cy * g[1] + cz * g[2];
+  const T ug = ux * g[0] + uy * g[1] + uz * g[2];
+  sp = T(stc_w<Q>(i)) * (T(-3) * ug + T(9) * cu * cg);
+  sm = T(stc_w<Q>(i)) * (T(3) * cg);
+}
+
+// Plain SRT update of one cell, f* = f + omega (f^eq - f) (Eq.(1) with Eq.(2)-(3)), pairs
+// (i, ibar) sharing f^eq_i = a + b, f^eq_ibar = a - b.  Explicitly rounded (see fluid_update).
 template <int Q, typename T, bool FORCE>
 __device__ __forceinline__ void srt_update(T (&f)[Q], T rho, T ux, T uy, T uz, T om,
-                                           const T (&gl)[3], T gpref) {
+                                           const T (&gl)[3]) {
   const T usq = rfma(uz, uz, rfma(uy, uy, rmul(ux, ux)));
   const T base = rsub(T(1), rmul(T(1.5), usq));
+  const T gp = rsub(T(1), rmul(T(0.5), om));
   {
     T o0 = rmul(om, rsub(rmul(rmul(T(stc_w<Q>(0)), rho), base), f[0]));
-    if (FORCE) o0 = radd(o0, guo_q<Q, T>(0, ux, uy, uz, gl, gpref));
+    if (FORCE) {
+      T sp, sm;
+      guo_pair<Q, T>(0, ux, uy, uz, gl, sp, sm);
+      o0 = radd(o0, rmul(gp, sp));
+    }
     f[0] = radd(f[0], o0);
   }
 #pragma unroll
@@ -142,11 +148,57 @@ __device__ __forceinline__ void srt_update(T (&f)[Q], T rho, T ux, T uy, T uz, T
     T oi = rmul(om, rsub(radd(a, b), f[i]));
     T oj = rmul(om, rsub(rsub(a, b), f[j]));
     if (FORCE) {
-      oi = radd(oi, guo_q<Q, T>(i, ux, uy, uz, gl, gpref));
-      oj = radd(oj, guo_q<Q, T>(j, ux, uy, uz, gl, gpref));
+      T sp, sm;
+      guo_pair<Q, T>(i, ux, uy, uz, gl, sp, sm);
+      oi = radd(oi, rmul(gp, radd(sp, sm)));
+      oj = radd(oj, rmul(gp, rsub(sp, sm)));
     }
     f[i] = radd(f[i], oi);
     f[j] = radd(f[j], oj);
+  }
+}
+
+// Fluid update of one cell, f* = f + Omega^F: SRT (Eq.(2)) or TRT, as pairs
+// (i, ibar) with f^eq_i = a + b, f^eq_ibar = a - b, a = w rho (1 - 1.5 u.u + 4.5 (c.u)^2),
+// b = 3 w rho c.u:  P = w+ (a - f+), M = w- (b - f-), f*_i = f_i + P + M, f*_ibar = f_ibar + P - M
+// with f+- = (f_i +- f_ibar)/2.  SRT is w- = w+.  Every operation is explicitly rounded, so the
+// update gives the same bits wherever it runs (fluid tiles, B = 0 cells of PSM tiles, any slab
+// decomposition).
+template <int Q, typename T, bool FORCE>
+__device__ __forceinline__ void fluid_update(T (&f)[Q], T rho, T ux, T uy, T uz, T omp, T omm,
+                                             const T (&gl)[3]) {
+  const T usq = rfma(uz, uz, rfma(uy, uy, rmul(ux, ux)));
+  const T base = rsub(T(1), rmul(T(1.5), usq));
+  const T gp = rsub(T(1), rmul(T(0.5), omp)), gm = rsub(T(1), rmul(T(0.5), omm));
+  {
+    T o0 = rmul(omp, rsub(rmul(rmul(T(stc_w<Q>(0)), rho), base), f[0]));
+    if (FORCE) {
+      T sp, sm;
+      guo_pair<Q, T>(0, ux, uy, uz, gl, sp, sm);
+      o0 = radd(o0, rmul(gp, sp));
+    }
+    f[0] = radd(f[0], o0);
+  }
+#pragma unroll
+  for (int i = 1; i < Q; ++i) {
+    const int j = stc_opp(i);
+    if (j < i) continue;
+    const T cu = cdot<T>(i, ux, uy, uz);
+    const T wr = rmul(T(stc_w<Q>(i)), rho);
+    const T a = rmul(wr, rfma(rmul(T(4.5), cu), cu, base));
+    const T b = rmul(wr, rmul(T(3), cu));
+    const T fp = rmul(T(0.5), radd(f[i], f[j]));
+    const T fm = rmul(T(0.5), rsub(f[i], f[j]));
+    T P = rmul(omp, rsub(a, fp));
+    T M = rmul(omm, rsub(b, fm));
+    if (FORCE) {
+      T sp, sm;
+      guo_pair<Q, T>(i, ux, uy, uz, gl, sp, sm);
+      P = radd(P, rmul(gp, sp));
+      M = radd(M, rmul(gm, sm));
+    }
+    f[i] = radd(f[i], radd(P, M));
+    f[j] = radd(f[j], rsub(P, M));
   }
 }
 
@@ -163,7 +215,7 @@ constexpr int collide_min_blocks() {
   return sizeof(T) == 8 ? 2 : (Q == 19 ? (PAT == 2 ? 3 : 4) : (PAT == 2 ? 2 : 3));
 }
 
-template <int Q, typename T, int PAT, bool WALLS, bool FORCE, bool DBG>
+template <int Q, typename T, int PAT, bool WALLS, bool FORCE, bool DBG, bool TRT>
 __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT>()))
     k_collide(const __grid_constant__ CollideParams p) {
   const Geom& G = p.g;
@@ -251,11 +303,12 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT>()))
   const T uy = FORCE ? rmul(rfma(T(0.5), gl[1], jy), ir) : rmul(jy, ir);
   const T uz = FORCE ? rmul(rfma(T(0.5), gl[2], jz), ir) : rmul(jz, ir);
   const T usq15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
-  const T om = T(p.omega);
-  const T gpref = T(1) - T(0.5) * om;
+  const T om = T(p.omega), omm = T(p.omega_m);
+  const T gpref = T(1) - T(0.5) * om, gmref = T(1) - T(0.5) * omm;
 
   if (!solid_tile) {
-    srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl, gpref);
+    if (TRT) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
+    else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
   } else {
     // ---- PSM cell: B, u_s from the solid word (or the test-only dense fields) ----
     int id = 0;
@@ -308,10 +361,22 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT>()))
         const T ej = feq_q<Q, T>(j, rho, ux, uy, uz, usq15);
         const T si = feq_q<Q, T>(i, rho, sux, suy, suz, susq15);
         const T sj = feq_q<Q, T>(j, rho, sux, suy, suz, susq15);
-        T oFi = om * (ei - fi), oFj = om * (ej - fj);
+        // fluid operator on the pair: SRT, or TRT on the symmetric/antisymmetric parts
+        T oFi, oFj;
+        if (TRT) {
+          const T Pp = om * (T(0.5) * (ei + ej) - T(0.5) * (fi + fj));
+          const T Mm = omm * (T(0.5) * (ei - ej) - T(0.5) * (fi - fj));
+          oFi = Pp + Mm;
+          oFj = Pp - Mm;
+        } else {
+          oFi = om * (ei - fi);
+          oFj = om * (ej - fj);
+        }
         if (FORCE) {
-          oFi += guo_q<Q, T>(i, ux, uy, uz, gl, gpref);
-          oFj += guo_q<Q, T>(j, ux, uy, uz, gl, gpref);
+          T sp, sm;
+          guo_pair<Q, T>(i, ux, uy, uz, gl, sp, sm);
+          oFi += gpref * sp + gmref * sm;
+          oFj += gpref * sp - gmref * sm;
         }
         T oSi, oSj;
         if (p.sc == 1) {         // Eq.(7)
@@ -337,7 +402,8 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT>()))
       m[1] = Bd * (double)msy;
       m[2] = Bd * (double)msz;
     } else {
-      srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl, gpref);
+      if (TRT) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
+      else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
     }
     // ---- per-body F/T partial of this tile (deterministic block reduction) ----
     double v[kSlotVals];
@@ -378,18 +444,33 @@ static cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool db
   if (ntz <= 0) return cudaSuccess;
   dim3 grid(p.g.gx, p.g.gy, ntz), block(kTileX, kTileY, kTileZ);
   const bool walls = p.g.wall[0] || p.g.wall[1] || p.g.wall[2];
+  if (p.trt) {
+    // TRT: the general (runtime wall flags) variants only
+    if (dbg || force) {
+      if (dbg && force) k_collide<Q, T, 0, true, true, true, true><<<grid, block, 0, st>>>(p);
+      else if (dbg) k_collide<Q, T, 0, true, false, true, true><<<grid, block, 0, st>>>(p);
+      else k_collide<Q, T, 0, true, true, false, true><<<grid, block, 0, st>>>(p);
+    } else if (pat == 0) {
+      k_collide<Q, T, 0, true, false, false, true><<<grid, block, 0, st>>>(p);
+    } else if (pat == 1) {
+      k_collide<Q, T, 1, false, false, false, true><<<grid, block, 0, st>>>(p);
+    } else {
+      k_collide<Q, T, 2, true, false, false, true><<<grid, block, 0, st>>>(p);
+    }
+    return cudaGetLastError();
+  }
   if (dbg || force) {
-    if (dbg && force) k_collide<Q, T, 0, true, true, true><<<grid, block, 0, st>>>(p);
-    else if (dbg) k_collide<Q, T, 0, true, false, true><<<grid, block, 0, st>>>(p);
-    else k_collide<Q, T, 0, true, true, false><<<grid, block, 0, st>>>(p);
+    if (dbg && force) k_collide<Q, T, 0, true, true, true, false><<<grid, block, 0, st>>>(p);
+    else if (dbg) k_collide<Q, T, 0, true, false, true, false><<<grid, block, 0, st>>>(p);
+    else k_collide<Q, T, 0, true, true, false, false><<<grid, block, 0, st>>>(p);
   } else if (pat == 0) {
-    if (walls) k_collide<Q, T, 0, true, false, false><<<grid, block, 0, st>>>(p);
-    else k_collide<Q, T, 0, false, false, false><<<grid, block, 0, st>>>(p);
+    if (walls) k_collide<Q, T, 0, true, false, false, false><<<grid, block, 0, st>>>(p);
+    else k_collide<Q, T, 0, false, false, false, false><<<grid, block, 0, st>>>(p);
   } else if (pat == 1) {
-    k_collide<Q, T, 1, false, false, false><<<grid, block, 0, st>>>(p);
+    k_collide<Q, T, 1, false, false, false, false><<<grid, block, 0, st>>>(p);
   } else {
-    if (walls) k_collide<Q, T, 2, true, false, false><<<grid, block, 0, st>>>(p);
-    else k_collide<Q, T, 2, false, false, false><<<grid, block, 0, st>>>(p);
+    if (walls) k_collide<Q, T, 2, true, false, false, false><<<grid, block, 0, st>>>(p);
+    else k_collide<Q, T, 2, false, false, false, false><<<grid, block, 0, st>>>(p);
   }
   return cudaGetLastError();
 }

@@ -778,8 +778,11 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
       FAIL((psm_ctx*)nullptr, PSM_E_ARG, "bad boundary kind");
   if ((opt->prec != PSM_F64 && opt->prec != PSM_F32) ||
       (opt->pattern != PSM_TWO_ARRAY && opt->pattern != PSM_AA) || opt->sc < 1 || opt->sc > 3 ||
-      (opt->bmode != PSM_B_DIRECT && opt->bmode != PSM_B_WEIGHTED))
+      (opt->bmode != PSM_B_DIRECT && opt->bmode != PSM_B_WEIGHTED) ||
+      (opt->collision != PSM_SRT && opt->collision != PSM_TRT))
     FAIL((psm_ctx*)nullptr, PSM_E_ARG, "bad option enum");
+  if (opt->collision == PSM_TRT && !(opt->trt_magic > 0.0 && std::isfinite(opt->trt_magic)))
+    FAIL((psm_ctx*)nullptr, PSM_E_ARG, "TRT magic parameter must be finite and > 0");
   const int world = opt->world < 1 ? 1 : opt->world;
   if (opt->rank < 0 || opt->rank >= world) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "bad rank");
   if (grid->nz < world) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "nz < world");
@@ -1065,6 +1068,10 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
   p.dbg_id = c->dbg_id;
   p.tau = c->tau;
   p.omega = 1.0 / c->tau;
+  p.omega_m = (c->opt.collision == PSM_TRT)
+                  ? 1.0 / (0.5 + c->opt.trt_magic / (c->tau - 0.5))
+                  : p.omega;
+  p.trt = c->opt.collision == PSM_TRT ? 1 : 0;
   for (int a = 0; a < 3; ++a) p.gforce[a] = c->opt.body_force[a];
   p.sc = c->opt.sc;
   p.bmode = c->opt.bmode;

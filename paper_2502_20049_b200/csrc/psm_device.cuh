@@ -102,7 +102,9 @@ struct CollideParams {
   const double* dbg_B;    // DBG: B [cell]
   const double* dbg_us;   // DBG: u_s [3][cell]
   const uint8_t* dbg_id;  // DBG: id [cell]
-  double tau, omega;      // omega = 1/tau
+  double tau, omega;      // omega = 1/tau (symmetric rate w+)
+  double omega_m;         // antisymmetric rate w- (TRT; == omega for SRT)
+  int trt;                // fluid operator: 0 SRT (Eq.(2)), 1 TRT
   double gforce[3];       // test-only Guo force
   int sc;                 // 1, 2, 3
   int bmode;              // 0 direct, 1 weighted

@@ -29,9 +29,9 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_struct_layouts_match_header():
-    # psm_options: 4 int32 + 3 double + 2 int32 + 2 pointers
+    # psm_options: 4 int32 + 3 double + 2 int32 + 2 pointers + int32 (+4 pad) + double
     assert C.sizeof(psm.psm_grid) == 3 * 8 + 3 * 4 + 4
-    assert C.sizeof(psm.psm_options) == 16 + 24 + 8 + 16
+    assert C.sizeof(psm.psm_options) == 16 + 24 + 8 + 16 + 8 + 8
     assert C.sizeof(psm.psm_pose) == 12 * 8
     assert C.sizeof(psm.psm_velocity) == 6 * 8
     assert C.sizeof(psm.psm_shape) == 8 + 8 + 8 + 8 + 8 + 8
@@ -43,7 +43,7 @@ def _opts(**kw):
     o.update(kw)
     return psm.psm_options(o["prec"], o["pattern"], o["sc"], o["bmode"],
                            (C.c_double * 3)(*o.get("force", (0, 0, 0))), o["rank"], o["world"],
-                           None, None)
+                           None, None, o.get("coll", 0), o.get("magic", 0.1875))
 
 
 def _grid(nx=8, ny=8, nz=8, bc=(0, 0, 0)):
@@ -67,6 +67,8 @@ def test_create_validation_codes():
         (dict(world=2, rank=0), _grid(), 19, psm.PSM_E_UNSUPPORTED if False else psm.PSM_E_ARG),
         (dict(world=2, rank=2), _grid(), 19, psm.PSM_E_ARG),
         (dict(), _grid(8, 8, 8, (0, 3, 0)), 19, psm.PSM_E_ARG),
+        (dict(coll=2), _grid(), 19, psm.PSM_E_ARG),
+        (dict(coll=1, magic=0.0), _grid(), 19, psm.PSM_E_ARG),
     ]
     for kw, g, q, code in cases:
         with pytest.raises(psm.PSMError) as e:

@@ -31,15 +31,17 @@ def _ft_close(g, o, rel=FT_REL):
 
 
 def _run_pair(nx, ny, nz, Q, tau, bc, sc, bmode, prec, pattern, bodies, steps, seed,
-              u0=(0.05, 0.0, 0.0), ft_every=True, force=(0.0, 0.0, 0.0)):
+              u0=(0.05, 0.0, 0.0), ft_every=True, force=(0.0, 0.0, 0.0), collision="srt",
+              magic=3.0 / 16.0):
     """bodies: list of dicts (id, kind, r | mesh, s, pose(k) -> (Q, t), v, w).  Explicit poses
     are passed every step to both sides (reading A13)."""
     shape = (nz, ny, nx)
     rho, u = pi.perturbed_flow(shape, seed, u0=u0)
     o = oracle.Oracle(nx, ny, nz, Q, tau, bc, sc, bmode)
     o.set_force(force)
+    o.set_collision(collision, magic)
     g = _sim(nx=nx, ny=ny, nz=nz, Q=Q, tau=tau, bc=bc, prec=prec, pattern=pattern, sc=sc,
-             bmode=bmode, body_force=force)
+             bmode=bmode, body_force=force, collision=collision, trt_magic=magic)
     o.init_equilibrium(rho, u)
     g.init_equilibrium(rho, u)
     for b in bodies:
@@ -292,4 +294,28 @@ def test_two_bodies_with_overlapping_boxes():
                    pose=lambda k: (np.eye(3), tuple(np.array([24.0, 20.0, 28.0]) + k * vs)))]
     o, g = _run_pair(48, 40, 36, 19, 0.7, (0, 0, 0), 3, 1, "f64", "two_array", bodies, 24, 13,
                      u0=(0.02, 0.0, 0.0))
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+
+
+@pytest.mark.parametrize("pattern,Q,sc", [("two_array", 19, 1), ("aa", 27, 3),
+                                          ("two_array", 27, 2)])
+def test_trt_psm_rotating_mesh(pattern, Q, sc):
+    """TRT fluid operator (NEXT rank 2) inside the PSM update with a rotating mesh and walls."""
+    v, tr = pi.propeller_mesh(n_blades=3, scale=0.07, n_st=8, n_pts=16, hub_seg=16)
+    w = np.array([0.025, 0.0, 0.0])
+
+    def pose(k):
+        return oracle.pose_advance(np.eye(3), [20.0, 11.0, 9.5], [0, 0, 0], w, k, [40, 22, 19],
+                                   [1, 0, 0])
+
+    o, g = _run_pair(40, 22, 19, Q, 0.62, (0, 1, 1), sc, 1, "f64", pattern,
+                     [dict(id=1, kind="mesh", verts=v, tris=tr, s=1, pose=pose, w=w)], 30, 17,
+                     u0=(0.02, 0.0, 0.01), collision="trt", magic=0.1)
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+
+
+def test_trt_forced_channel_with_sphere():
+    body = dict(id=1, kind="sphere", r=3.5, s=1, pose=_static(t=(10.0, 8.0, 6.0)))
+    o, g = _run_pair(20, 16, 12, 19, 0.7, (0, 1, 0), 1, 1, "f64", "two_array", [body], 40, 3,
+                     u0=(0.0, 0.0, 0.0), force=(1e-5, 0.0, 2e-6), collision="trt")
     assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL

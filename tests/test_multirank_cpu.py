@@ -25,7 +25,7 @@ def _worker(rank, world, port, q):
     nz = 37
     g = psm.psm_grid(24, 20, nz, (C.c_int32 * 3)(0, 0, 0))
     o = psm.psm_options(psm.PSM_F32, psm.PSM_TWO_ARRAY, 1, 1, (C.c_double * 3)(0, 0, 0), rank,
-                        world, C.cast(buf, C.c_void_p), None)
+                        world, C.cast(buf, C.c_void_p), None, 0, 0.1875)
     ctx = psm.psm_create(g, 19, 0.6, o)  # host-only: no device touched
     z0, nzl = psm.psm_local_extent(ctx)
     psm.psm_destroy(ctx)

@@ -274,3 +274,37 @@ def test_p11_pose_closed_form():
     _, tn = oracle.pose_advance(np.eye(3), [63.0, 1.0, 0.0], [1.0, -1.5, 0.0], [0, 0, 0], 3,
                                 L, per)
     assert np.allclose(tn, [2.0, 60.5, 0.0])  # 63+3=66->2 ; 1-4.5=-3.5->60.5
+
+
+# ---------------------------------------------------------------- TRT (NEXT rank 2) ---
+def test_trt_reduces_to_srt_and_conserves():
+    """tau_- = tau (magic = (tau - 1/2)^2) is SRT; TRT conserves mass and momentum per cell."""
+    Q = 19
+    c, w, _ = oracle.stencil(Q)
+    cf = c.astype(float)
+    f = pi.random_pdfs(Q, (1,), 61, w=w)[:, 0]
+    tau = 0.73
+    a, _, _ = oracle.collide_cell(Q, f, tau, 1, 0.0, [0, 0, 0])
+    b, _, _ = oracle.collide_cell_trt(Q, f, tau, (tau - 0.5) ** 2, 1, 0.0, [0, 0, 0])
+    assert np.allclose(a, b, atol=2e-16, rtol=0)
+    for magic in (3 / 16, 1 / 4, 1 / 12):
+        out, _, _ = oracle.collide_cell_trt(Q, f, tau, magic, 1, 0.0, [0, 0, 0])
+        assert abs(out.sum() - f.sum()) < 1e-15
+        assert np.allclose(out @ cf, f @ cf, atol=1e-16, rtol=0)
+        assert np.max(np.abs(out - a)) > 1e-6  # the antisymmetric rate really differs
+
+
+def test_trt_poiseuille_is_exact_at_magic_3_16():
+    """Half-way bounce-back + Guo force + TRT with Lambda = 3/16: the parabolic profile is
+    reproduced to round-off (the known exact-wall property of TRT), with u = (j + g/2)/rho."""
+    H, tau, g = 16, 0.8, 1e-6
+    o = oracle.Oracle(1, H, 1, 19, tau, (0, 1, 0), 1, 1)
+    o.set_collision("trt", 3 / 16)
+    o.init_equilibrium(None, None)
+    o.set_force([g, 0, 0])
+    o.step(60000)
+    rho, u = o.velocity()
+    ux = u[0, 0, :, 0] + 0.5 * g / rho[0, :, 0]
+    yc = np.arange(H) + 0.5
+    ref = g * yc * (H - yc) / (2 * (tau - 0.5) / 3)
+    assert np.max(np.abs(ux - ref)) / ref.max() < 1e-9
