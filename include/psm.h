@@ -160,6 +160,26 @@ psm_status psm_set_body(psm_ctx* ctx, int32_t body_id, const psm_shape* shape,
                         const psm_pose* pose, const psm_velocity* vel);
 psm_status psm_remove_body(psm_ctx* ctx, int32_t body_id);
 
+/* Two-way coupling (NEXT row of the hot path; the paper's settling-sphere validation couples the
+ * PSM force back to the body; its integrator is unstated).
+ * With dyn != NULL the body becomes dynamic: after every step the library reduces F, T of
+ * Eqs.(10)-(11) on the device (allreduced over ranks), and integrates on the host in fp64:
+ *   v += (F + ext_force)/mass;  t += v (wrapped);  I_w = Q I Q^T;  omega += I_w^-1 (T + ext_torque);
+ *   Q = Rot(omega/|omega|, |omega|) Q, then Gram-Schmidt on the columns of Q.
+ * The pose and velocities given to psm_set_body are the initial state.  dyn == NULL returns the
+ * body to prescribed motion (closed form from its current state).  Errors: PSM_E_ARG (unknown
+ * body, mass <= 0, inertia not symmetric positive definite). */
+typedef struct {
+  double mass;           /* > 0, lattice units                                                */
+  double inertia[9];     /* body-frame inertia tensor about the body origin, row-major        */
+  double ext_force[3];   /* constant external force, world frame (e.g. (m - rho_f V) g)       */
+  double ext_torque[3];  /* constant external torque, world frame                             */
+} psm_dynamics;
+psm_status psm_set_dynamics(psm_ctx* ctx, int32_t body_id, const psm_dynamics* dyn);
+/* Current pose and velocities of a body (the state the next step will map and use for u_s). */
+psm_status psm_get_body_state(const psm_ctx* ctx, int32_t body_id, psm_pose* pose,
+                              psm_velocity* vel);
+
 /* Host-only: the super-sampled geometry field psm_set_body builds for a mesh (PAPER.md:299-308,
  * exact ray parity, A15/A17).  dims[3] (geometry cells per axis, = LBM cells * 2^s) and
  * origin[3] (body frame, integer valued) are always written; bits (one byte 0/1 per geometry

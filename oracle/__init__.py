@@ -68,6 +68,9 @@ def lib():
             "orc_step": (I, [P]),
             "orc_error_cell": (I64, [P]),
             "orc_force_torque": (None, [P, I, P, P, P, P]),
+            "orc_set_dynamics": (None, [P, I, D, P, P, P]),
+            "orc_integrate": (None, [P]),
+            "orc_get_body_state": (None, [P, I, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -244,6 +247,19 @@ class Oracle:
             if err:
                 raise FloatingPointError(
                     f"oracle: invalid state at cell {lib().orc_error_cell(self._h)}")
+
+    def set_dynamics(self, bid, mass, inertia, ext_force=(0, 0, 0), ext_torque=(0, 0, 0)):
+        keep = [_f64(np.ravel(inertia)), _f64(ext_force), _f64(ext_torque)]
+        lib().orc_set_dynamics(self._h, bid, float(mass), *[_p(k) for k in keep])
+
+    def integrate(self):
+        """Advance the dynamic bodies with the force/torque of the last step (two-way coupling)."""
+        lib().orc_integrate(self._h)
+
+    def body_state(self, bid):
+        Q, t, v, w = np.zeros(9), np.zeros(3), np.zeros(3), np.zeros(3)
+        lib().orc_get_body_state(self._h, bid, _p(Q), _p(t), _p(v), _p(w))
+        return Q.reshape(3, 3), t, v, w
 
     def force_torque(self, bid):
         F, T, AF, AT = (np.zeros(3) for _ in range(4))

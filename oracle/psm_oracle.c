@@ -365,6 +365,8 @@ typedef struct {
   int present, kind, s; /* kind 0 sphere, 1 mesh */
   double radius, rbound;
   double Q[9], t[3], v[3], w[3];
+  int dynamic;          /* two-way coupled: orc_integrate advances Q, t, v, w */
+  double mass, I[9], fext[3], text[3];
   double gorigin[3];
   int64_t gdims[3];
   uint8_t* gbits;
@@ -738,6 +740,95 @@ int orc_step(orc_sim* S) {
 }
 
 int64_t orc_error_cell(const orc_sim* S) { return S->err_cell; }
+
+/* ---------------------------------------------------------------- two-way coupling -------
+ * (NEXT row; the paper couples force and torque back to a settling sphere, PAPER.md:441-447,
+ * without stating the integrator; DESIGN.md §12 fixes semi-implicit Euler.)  For every dynamic
+ * body, with F, T the force and torque ON the body from the last orc_step:
+ *   v <- v + (F + F_ext)/m;  t <- t + v (wrapped into [0, L) on periodic axes);
+ *   I_w = Q I Q^T;  w <- w + I_w^{-1} (T + T_ext)  (adjugate / determinant);
+ *   Q <- Rot(w/|w|, |w|) Q;  columns of Q re-orthonormalised (Gram-Schmidt). */
+void orc_set_dynamics(orc_sim* S, int id, double mass, const double I[9], const double fext[3],
+                      const double text[3]) {
+  orc_body* b = &S->bodies[id];
+  b->dynamic = 1;
+  b->mass = mass;
+  memcpy(b->I, I, sizeof(b->I));
+  memcpy(b->fext, fext, sizeof(b->fext));
+  memcpy(b->text, text, sizeof(b->text));
+}
+
+void orc_integrate(orc_sim* S) {
+  double L[3] = {S->nx, S->ny, S->nz};
+  for (int id = 1; id <= ORC_MAXB; ++id) {
+    orc_body* b = &S->bodies[id];
+    if (!b->present || !b->dynamic) continue;
+    double F[3], T[3];
+    for (int a = 0; a < 3; ++a) {
+      F[a] = -S->SF[id][a];
+      T[a] = -S->ST[id][a];
+    }
+    for (int a = 0; a < 3; ++a) b->v[a] = b->v[a] + (F[a] + b->fext[a]) / b->mass;
+    for (int a = 0; a < 3; ++a) {
+      double x = b->t[a] + b->v[a];
+      if (S->bc[a] == 0) x = x - L[a] * floor(x / L[a]);
+      b->t[a] = x;
+    }
+    double QI[9], Iw[9];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        double acc = 0.0;
+        for (int k = 0; k < 3; ++k) acc += b->Q[3 * r + k] * b->I[3 * k + c];
+        QI[3 * r + c] = acc;
+      }
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        double acc = 0.0;
+        for (int k = 0; k < 3; ++k) acc += QI[3 * r + k] * b->Q[3 * c + k];
+        Iw[3 * r + c] = acc;
+      }
+    /* inverse by the adjugate: inv = adj / det */
+    double a = Iw[0], bb = Iw[1], c = Iw[2], d = Iw[3], e = Iw[4], f = Iw[5], g = Iw[6],
+           h = Iw[7], i = Iw[8];
+    double adj[9] = {e * i - f * h, c * h - bb * i, bb * f - c * e,
+                     f * g - d * i, a * i - c * g, c * d - a * f,
+                     d * h - e * g, bb * g - a * h, a * e - bb * d};
+    double det = a * (e * i - f * h) - bb * (d * i - f * g) + c * (d * h - e * g);
+    double tt[3] = {T[0] + b->text[0], T[1] + b->text[1], T[2] + b->text[2]};
+    for (int r = 0; r < 3; ++r) {
+      double acc = 0.0;
+      for (int k = 0; k < 3; ++k) acc += adj[3 * r + k] * tt[k];
+      b->w[r] = b->w[r] + acc / det;
+    }
+    double Qn[9], zero[3] = {0, 0, 0}, one[3] = {1, 1, 1}, tdummy[3];
+    int noper[3] = {0, 0, 0};
+    orc_pose_advance(b->Q, zero, zero, b->w, 1, one, noper, Qn, tdummy);
+    double c0[3] = {Qn[0], Qn[3], Qn[6]}, c1[3] = {Qn[1], Qn[4], Qn[7]}, c2[3];
+    double n0 = sqrt(c0[0] * c0[0] + c0[1] * c0[1] + c0[2] * c0[2]);
+    for (int k = 0; k < 3; ++k) c0[k] = c0[k] / n0;
+    double d01 = c0[0] * c1[0] + c0[1] * c1[1] + c0[2] * c1[2];
+    for (int k = 0; k < 3; ++k) c1[k] = c1[k] - d01 * c0[k];
+    double n1 = sqrt(c1[0] * c1[0] + c1[1] * c1[1] + c1[2] * c1[2]);
+    for (int k = 0; k < 3; ++k) c1[k] = c1[k] / n1;
+    c2[0] = c0[1] * c1[2] - c0[2] * c1[1];
+    c2[1] = c0[2] * c1[0] - c0[0] * c1[2];
+    c2[2] = c0[0] * c1[1] - c0[1] * c1[0];
+    for (int k = 0; k < 3; ++k) {
+      b->Q[3 * k + 0] = c0[k];
+      b->Q[3 * k + 1] = c1[k];
+      b->Q[3 * k + 2] = c2[k];
+    }
+  }
+}
+
+void orc_get_body_state(const orc_sim* S, int id, double Q[9], double t[3], double v[3],
+                        double w[3]) {
+  const orc_body* b = &S->bodies[id];
+  memcpy(Q, b->Q, sizeof(b->Q));
+  memcpy(t, b->t, 3 * sizeof(double));
+  memcpy(v, b->v, 3 * sizeof(double));
+  memcpy(w, b->w, 3 * sizeof(double));
+}
 
 /* Force and torque ON body id (A6): F = -sum B sum_i Omega^S_i c_i (the printed Eq.(10) sum is
  * the momentum the fluid gains), T = -sum B (x_c - R) x sum_i Omega^S_i c_i (Eq.(11), A7). */

@@ -38,7 +38,8 @@ EXPORTED = (
     "psm_create", "psm_destroy", "psm_required_bytes", "psm_bind_memory", "psm_local_extent",
     "psm_init_equilibrium", "psm_write_pdfs", "psm_read_pdfs", "psm_read_pdfs_planes",
     "psm_read_velocity",
-    "psm_set_body", "psm_remove_body", "psm_voxelize", "psm_map_fractions", "psm_step", "psm_force_torque",
+    "psm_set_body", "psm_remove_body", "psm_voxelize", "psm_set_dynamics",
+    "psm_get_body_state", "psm_map_fractions", "psm_step", "psm_force_torque",
     "psm_read_fractions", "psm_debug_set_fields", "psm_get_step", "psm_launch_count",
     "psm_profile", "psm_profile_read", "psm_nccl_id_bytes", "psm_nccl_get_unique_id",
     "psm_last_error",
@@ -71,6 +72,11 @@ class psm_velocity(C.Structure):
     _fields_ = [("v", C.c_double * 3), ("omega", C.c_double * 3)]
 
 
+class psm_dynamics(C.Structure):
+    _fields_ = [("mass", C.c_double), ("inertia", C.c_double * 9),
+                ("ext_force", C.c_double * 3), ("ext_torque", C.c_double * 3)]
+
+
 class PSMError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"psm error {code}: {msg}")
@@ -100,6 +106,7 @@ def load(build_if_missing: bool = True):
         "psm_read_pdfs_planes": [P, I64, I64, P],
         "psm_remove_body": [P, I32], "psm_map_fractions": [P],
         "psm_voxelize": [P, I64, P, I64, I32, P, P, P], "psm_step": [P, I64],
+        "psm_set_dynamics": [P, I32, P], "psm_get_body_state": [P, I32, P, P],
         "psm_force_torque": [P, I32, P, P, P, P], "psm_read_fractions": [P, P, P, P],
         "psm_debug_set_fields": [P, P, P, P], "psm_get_step": [P, P],
         "psm_launch_count": [P, P], "psm_profile": [P, I32], "psm_profile_read": [P, P, P],
@@ -205,6 +212,17 @@ def psm_voxelize(verts, tris, s: int):
     _check(L.psm_voxelize(_ptr(verts), len(verts), _ptr(tris), len(tris), s, _ptr(origin),
                           _ptr(dims), _ptr(bits)))
     return origin, bits.reshape(int(dims[2]), int(dims[1]), int(dims[0]))
+
+
+def psm_set_dynamics(ctx, body_id: int, dyn):
+    _check(load().psm_set_dynamics(ctx, body_id, None if dyn is None else C.byref(dyn)), ctx)
+
+
+def psm_get_body_state(ctx, body_id: int):
+    pose, vel = psm_pose(), psm_velocity()
+    _check(load().psm_get_body_state(ctx, body_id, C.byref(pose), C.byref(vel)), ctx)
+    return (np.array(pose.Q[:]).reshape(3, 3), np.array(pose.t[:]), np.array(vel.v[:]),
+            np.array(vel.omega[:]))
 
 
 def psm_map_fractions(ctx):
@@ -344,6 +362,19 @@ class Simulation:
 
     def set_pose(self, bid, Q=np.eye(3), t=(0, 0, 0), v=(0, 0, 0), w=(0, 0, 0)):
         psm_set_body(self.ctx, bid, None, _pose(Q, t), _vel(v, w))
+
+    def set_dynamics(self, bid, mass=None, inertia=None, ext_force=(0, 0, 0),
+                     ext_torque=(0, 0, 0)):
+        """Two-way coupled body (mass=None: back to prescribed motion)."""
+        if mass is None:
+            psm_set_dynamics(self.ctx, bid, None)
+            return
+        d = psm_dynamics(float(mass), (C.c_double * 9)(*np.ravel(inertia)),
+                         (C.c_double * 3)(*ext_force), (C.c_double * 3)(*ext_torque))
+        psm_set_dynamics(self.ctx, bid, d)
+
+    def body_state(self, bid):
+        return psm_get_body_state(self.ctx, bid)
 
     def remove_body(self, bid):
         psm_remove_body(self.ctx, bid)

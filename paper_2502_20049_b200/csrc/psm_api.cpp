@@ -50,6 +50,11 @@ struct Body {
   int64_t mapped_step = -1;
   bool has_box = false;
   int64_t box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};  // last mapped box (global, unwrapped)
+  // two-way coupling: state advanced by the host integrator after every step
+  bool dynamic = false;
+  double mass = 0, Ib[9] = {0}, fext[3] = {0, 0, 0}, text[3] = {0, 0, 0};
+  double Qd[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, td[3] = {0, 0, 0}, vd[3] = {0, 0, 0},
+         wd[3] = {0, 0, 0};
 };
 
 struct Box {
@@ -476,11 +481,69 @@ static void fill_kin(const psm_ctx* c, CollideParams& p, int64_t step) {
     (void)t;
     for (int a = 0; a < 3; ++a) {
       k.t[a] = b.tc[a];  // pose of the current mapping (remapped before this collide)
-      k.v[a] = b.v[a];
-      k.w[a] = b.w[a];
+      k.v[a] = b.dynamic ? b.vd[a] : b.v[a];
+      k.w[a] = b.dynamic ? b.wd[a] : b.w[a];
     }
     k.s = b.s;
     k.present = 1;
+  }
+}
+
+// Semi-implicit Euler step of a dynamic body with the force/torque ON it from the step just
+// completed (the oracle implements the same formulas independently).
+static void integrate_body(const psm_ctx* c, Body& b, const double F[3], const double T[3]) {
+  for (int a = 0; a < 3; ++a) b.vd[a] = b.vd[a] + (F[a] + b.fext[a]) / b.mass;
+  for (int a = 0; a < 3; ++a) {
+    double x = b.td[a] + b.vd[a];
+    if (c->grid.bc[a] == PSM_PERIODIC) {
+      const double L = extent(c, a);
+      x = x - L * std::floor(x / L);
+    }
+    b.td[a] = x;
+  }
+  // world-frame inertia I_w = Q I Q^T
+  double M[9], Iw[9];
+  for (int r = 0; r < 3; ++r)
+    for (int cc = 0; cc < 3; ++cc) {
+      double acc = 0.0;
+      for (int l = 0; l < 3; ++l) acc += b.Qd[3 * r + l] * b.Ib[3 * l + cc];
+      M[3 * r + cc] = acc;
+    }
+  for (int r = 0; r < 3; ++r)
+    for (int cc = 0; cc < 3; ++cc) {
+      double acc = 0.0;
+      for (int l = 0; l < 3; ++l) acc += M[3 * r + l] * b.Qd[3 * cc + l];
+      Iw[3 * r + cc] = acc;
+    }
+  // omega += I_w^-1 (T + ext_torque), by the adjugate: d_r = sum_c adj[r][c] tt[c] / det
+  const double A = Iw[0], B = Iw[1], C = Iw[2], D = Iw[3], E = Iw[4], Fm = Iw[5], G = Iw[6],
+               H = Iw[7], I = Iw[8];
+  const double adj[9] = {E * I - Fm * H, C * H - B * I, B * Fm - C * E,
+                         Fm * G - D * I, A * I - C * G, C * D - A * Fm,
+                         D * H - E * G, B * G - A * H, A * E - B * D};
+  const double det = A * (E * I - Fm * H) - B * (D * I - Fm * G) + C * (D * H - E * G);
+  const double tt[3] = {T[0] + b.text[0], T[1] + b.text[1], T[2] + b.text[2]};
+  for (int r = 0; r < 3; ++r) {
+    double acc = 0.0;
+    for (int cc = 0; cc < 3; ++cc) acc += adj[3 * r + cc] * tt[cc];
+    b.wd[r] = b.wd[r] + acc / det;
+  }
+  double Qn[9];
+  rodrigues(b.wd, 1.0, b.Qd, Qn);
+  // Gram-Schmidt on the columns
+  double c0[3] = {Qn[0], Qn[3], Qn[6]}, c1[3] = {Qn[1], Qn[4], Qn[7]};
+  const double n0 = std::sqrt(c0[0] * c0[0] + c0[1] * c0[1] + c0[2] * c0[2]);
+  for (int a = 0; a < 3; ++a) c0[a] = c0[a] / n0;
+  const double d01 = c0[0] * c1[0] + c0[1] * c1[1] + c0[2] * c1[2];
+  for (int a = 0; a < 3; ++a) c1[a] = c1[a] - d01 * c0[a];
+  const double n1 = std::sqrt(c1[0] * c1[0] + c1[1] * c1[1] + c1[2] * c1[2]);
+  for (int a = 0; a < 3; ++a) c1[a] = c1[a] / n1;
+  const double c2[3] = {c0[1] * c1[2] - c0[2] * c1[1], c0[2] * c1[0] - c0[0] * c1[2],
+                        c0[0] * c1[1] - c0[1] * c1[0]};
+  for (int a = 0; a < 3; ++a) {
+    b.Qd[3 * a + 0] = c0[a];
+    b.Qd[3 * a + 1] = c1[a];
+    b.Qd[3 * a + 2] = c2[a];
   }
 }
 
@@ -526,7 +589,12 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
     m.t0[2] = (int)(zlo / kTileZ);
     m.n[2] = (int)((zhi - 1) / kTileZ + 1 - m.t0[2]);
     m.first = 0;
-    // bodies whose current box overlaps this box (ascending id order is kept by the bit loop)
+    // bodies whose current box overlaps the TILE-ALIGNED extent of this box (the kernels
+    // rewrite whole tiles, so every body that can own a cell of those tiles must be evaluated)
+    const int64_t tlo[3] = {(int64_t)m.t0[0] * kTileX, (int64_t)m.t0[1] * kTileY,
+                            (int64_t)m.t0[2] * kTileZ + c->z0};
+    const int64_t thi[3] = {tlo[0] + (int64_t)m.n[0] * kTileX, tlo[1] + (int64_t)m.n[1] * kTileY,
+                            tlo[2] + (int64_t)m.n[2] * kTileZ};
     m.bodymask = 0;
     for (int id = 1; id <= kMaxBodies; ++id) {
       const Body& bd = c->bodies[id];
@@ -536,7 +604,7 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
       for (const Box& pc : pieces) {
         bool ov = true;
         for (int a = 0; a < 3; ++a)
-          if (pc.hi[a] <= b.lo[a] || pc.lo[a] >= b.hi[a]) ov = false;
+          if (pc.hi[a] <= tlo[a] || pc.lo[a] >= thi[a]) ov = false;
         if (ov) {
           m.bodymask |= 1u << id;
           break;
@@ -608,7 +676,10 @@ static psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
     Body& b = c->bodies[id];
     if (!b.present) continue;
     double Q[9], t[3];
-    if (b.moving) {
+    if (b.dynamic) {
+      std::memcpy(Q, b.Qd, sizeof(Q));
+      std::memcpy(t, b.td, sizeof(t));
+    } else if (b.moving) {
       pose_at(c, b, step, Q, t);
     } else {
       std::memcpy(Q, b.Q0, sizeof(Q));
@@ -761,6 +832,36 @@ static psm_status state_read(psm_ctx* c, double* f, double* rho, double* u, int6
 }
 
 // ----------------------------------------------------------------------------- ABI --------
+// Enqueue the per-body force/torque reduction of the step just collided (two deterministic
+// passes, allreduce over ranks) and its D2H copy into the pinned buffer; ids receives the body
+// order of the copied rows.  The caller synchronises.
+static psm_status ft_enqueue(psm_ctx* c, std::vector<int>& ids) {
+  ids.clear();
+  for (int id = 1; id <= kMaxBodies; ++id)
+    if (c->bodies[id].present || c->dbg) ids.push_back(id);
+  const int nb = (int)ids.size();
+  if (nb == 0) return PSM_OK;
+  int* hid = reinterpret_cast<int*>(c->pinned + kMaxBodies * kSlotVals);
+  for (int i = 0; i < nb; ++i) hid[i] = ids[i];
+  CUDA_TRY(c, cudaMemcpyAsync(c->ft_ids, hid, nb * 4, cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(c, launch_ft_reduce(c->tile_flag, c->partial, (int)c->ntiles, c->overflow, c->ft_ids,
+                               nb, c->ft_scratch, kFtChunks, c->ft_out, c->st));
+  c->launches += 2;
+  if (c->world > 1)
+    NCCL_TRY(c, ncclAllReduce(c->ft_out, c->ft_out, (size_t)nb * kSlotVals, ncclFloat64, ncclSum,
+                              c->comm, c->st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->pinned, c->ft_out, (size_t)nb * kSlotVals * 8,
+                              cudaMemcpyDeviceToHost, c->st));
+  return PSM_OK;
+}
+
+static void ft_store(psm_ctx* c, const std::vector<int>& ids) {
+  std::memset(c->ft, 0, sizeof(c->ft));
+  for (size_t i = 0; i < ids.size(); ++i)
+    std::memcpy(c->ft[ids[i]], c->pinned + i * kSlotVals, kSlotVals * 8);
+  c->ft_valid = true;
+}
+
 extern "C" {
 
 psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
@@ -1001,6 +1102,13 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
   for (int a = 0; a < 3; ++a)
     if (b.v[a] != 0.0 || b.w[a] != 0.0) b.moving = true;
   b.step0 = c->step;
+  if (b.dynamic) {  // new initial state of a dynamic body
+    b.moving = true;
+    std::memcpy(b.Qd, b.Q0, sizeof(b.Qd));
+    std::memcpy(b.td, b.t0, sizeof(b.td));
+    std::memcpy(b.vd, b.v, sizeof(b.vd));
+    std::memcpy(b.wd, b.w, sizeof(b.wd));
+  }
   c->ft_valid = false;
   return remap(c, std::vector<int>{id}, c->step);
 }
@@ -1018,6 +1126,88 @@ psm_status psm_voxelize(const double* verts, int64_t nverts, const int32_t* tris
     std::vector<uint8_t> field;
     voxelize_mesh(verts, nverts, tris, ntris, s, origin, cells, field);
     std::memcpy(bits, field.data(), field.size());
+  }
+  return PSM_OK;
+}
+
+psm_status psm_set_dynamics(psm_ctx* c, int32_t id, const psm_dynamics* d) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  if (id < 1 || id > kMaxBodies || !c->bodies[id].present) FAIL(c, PSM_E_ARG, "unknown body");
+  Body& b = c->bodies[id];
+  if (!d) {  // back to prescribed motion from the current state
+    if (b.dynamic) {
+      std::memcpy(b.Q0, b.Qd, sizeof(b.Q0));
+      std::memcpy(b.t0, b.td, sizeof(b.t0));
+      std::memcpy(b.v, b.vd, sizeof(b.v));
+      std::memcpy(b.w, b.wd, sizeof(b.w));
+      b.step0 = c->step;
+      b.dynamic = false;
+      b.moving = false;
+      for (int a = 0; a < 3; ++a)
+        if (b.v[a] != 0.0 || b.w[a] != 0.0) b.moving = true;
+    }
+    return PSM_OK;
+  }
+  if (!(d->mass > 0.0) || !std::isfinite(d->mass)) FAIL(c, PSM_E_ARG, "mass must be > 0");
+  const double* I = d->inertia;
+  for (int r = 0; r < 3; ++r)
+    for (int cc = 0; cc < 3; ++cc)
+      if (!std::isfinite(I[3 * r + cc]) || std::fabs(I[3 * r + cc] - I[3 * cc + r]) >
+                                               1e-12 * (std::fabs(I[0]) + std::fabs(I[4]) + std::fabs(I[8])))
+        FAIL(c, PSM_E_ARG, "inertia tensor must be symmetric and finite");
+  const double m1 = I[0], m2 = I[0] * I[4] - I[1] * I[3];
+  const double m3 = I[0] * (I[4] * I[8] - I[5] * I[7]) - I[1] * (I[3] * I[8] - I[5] * I[6]) +
+                    I[2] * (I[3] * I[7] - I[4] * I[6]);
+  if (!(m1 > 0 && m2 > 0 && m3 > 0)) FAIL(c, PSM_E_ARG, "inertia tensor must be positive definite");
+  // current state becomes the initial dynamic state
+  if (!b.dynamic) {
+    double Q[9], t[3];
+    if (b.moving) pose_at(c, b, c->step, Q, t);
+    else {
+      std::memcpy(Q, b.Q0, sizeof(Q));
+      std::memcpy(t, b.t0, sizeof(t));
+    }
+    std::memcpy(b.Qd, Q, sizeof(Q));
+    std::memcpy(b.td, t, sizeof(t));
+    std::memcpy(b.vd, b.v, sizeof(b.vd));
+    std::memcpy(b.wd, b.w, sizeof(b.wd));
+  }
+  b.dynamic = true;
+  b.moving = true;
+  b.mass = d->mass;
+  std::memcpy(b.Ib, d->inertia, sizeof(b.Ib));
+  std::memcpy(b.fext, d->ext_force, sizeof(b.fext));
+  std::memcpy(b.text, d->ext_torque, sizeof(b.text));
+  return PSM_OK;
+}
+
+psm_status psm_get_body_state(const psm_ctx* c, int32_t id, psm_pose* pose, psm_velocity* vel) {
+  if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
+  if (id < 1 || id > kMaxBodies || !c->bodies[id].present)
+    FAIL((psm_ctx*)nullptr, PSM_E_ARG, "unknown body");
+  const Body& b = c->bodies[id];
+  double Q[9], t[3], v[3], w[3];
+  if (b.dynamic) {
+    std::memcpy(Q, b.Qd, sizeof(Q));
+    std::memcpy(t, b.td, sizeof(t));
+    std::memcpy(v, b.vd, sizeof(v));
+    std::memcpy(w, b.wd, sizeof(w));
+  } else {
+    if (b.moving) pose_at(c, b, c->step, Q, t);
+    else {
+      std::memcpy(Q, b.Q0, sizeof(Q));
+      std::memcpy(t, b.t0, sizeof(t));
+    }
+    std::memcpy(v, b.v, sizeof(v));
+    std::memcpy(w, b.w, sizeof(w));
+  }
+  if (pose) {
+    std::memcpy(pose->Q, Q, sizeof(Q));
+    std::memcpy(pose->t, t, sizeof(t));
+  }
+  if (vel) {
+    std::memcpy(vel->v, v, sizeof(v));
+    std::memcpy(vel->omega, w, sizeof(w));
   }
   return PSM_OK;
 }
@@ -1088,7 +1278,10 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
       if (st != PSM_OK) return st;
     }
     // 2. fused PSM stream-collide (Eq.(4)) + F/T partials
-    if (k == n - 1)
+    bool any_dyn = false;
+    for (int id = 1; id <= kMaxBodies; ++id)
+      if (c->bodies[id].present && c->bodies[id].dynamic) any_dyn = true;
+    if (k == n - 1 || any_dyn)
       CUDA_TRY(c, cudaMemsetAsync(c->overflow, 0, (kMaxBodies + 1) * kSlotVals * 8, c->st));
     fill_kin(c, p, c->step);
     p.step = c->step;
@@ -1136,39 +1329,35 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
       c->cur ^= 1;
     }
     c->step += 1;
+    // 4. two-way coupling: this step's force/torque drives the dynamic bodies' next pose
+    if (any_dyn && !c->dbg) {
+      std::vector<int> ids;
+      st = ft_enqueue(c, ids);
+      if (st != PSM_OK) return st;
+      CUDA_TRY(c, cudaStreamSynchronize(c->st));
+      ft_store(c, ids);
+      for (int id = 1; id <= kMaxBodies; ++id) {
+        Body& b = c->bodies[id];
+        if (!b.present || !b.dynamic) continue;
+        const double F[3] = {-c->ft[id][0], -c->ft[id][1], -c->ft[id][2]};
+        const double T[3] = {-c->ft[id][3], -c->ft[id][4], -c->ft[id][5]};
+        integrate_body(c, b, F, T);
+      }
+    }
   }
   // 4. force/torque of the last step: deterministic two-pass reduction, then allreduce
   std::vector<int> ids;
-  for (int id = 1; id <= kMaxBodies; ++id)
-    if (c->bodies[id].present) ids.push_back(id);
-  if (c->dbg) {
-    ids.clear();
-    for (int id = 1; id <= kMaxBodies; ++id) ids.push_back(id);
-  }
-  const int nb = (int)ids.size();
   if (record(c, 2, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
-  if (nb > 0) {
-    int* hid = reinterpret_cast<int*>(c->pinned + kMaxBodies * kSlotVals);
-    for (int i = 0; i < nb; ++i) hid[i] = ids[i];
-    CUDA_TRY(c, cudaMemcpyAsync(c->ft_ids, hid, nb * 4, cudaMemcpyHostToDevice, c->st));
-    CUDA_TRY(c, launch_ft_reduce(c->tile_flag, c->partial, (int)c->ntiles, c->overflow,
-                                 c->ft_ids, nb, c->ft_scratch, kFtChunks, c->ft_out, c->st));
-    c->launches += 2;
-    if (c->world > 1)
-      NCCL_TRY(c, ncclAllReduce(c->ft_out, c->ft_out, (size_t)nb * kSlotVals, ncclFloat64,
-                                ncclSum, c->comm, c->st));
-    CUDA_TRY(c, cudaMemcpyAsync(c->pinned, c->ft_out, (size_t)nb * kSlotVals * 8,
-                                cudaMemcpyDeviceToHost, c->st));
-  }
+  st = ft_enqueue(c, ids);
+  if (st != PSM_OK) return st;
+  const int nb = (int)ids.size();
   if (record(c, 2, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
   unsigned long long* herr =
       reinterpret_cast<unsigned long long*>(c->pinned + (kMaxBodies + 1) * kSlotVals);
   CUDA_TRY(c, cudaMemcpyAsync(herr, c->err, 8, cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
-  std::memset(c->ft, 0, sizeof(c->ft));
-  for (int i = 0; i < nb; ++i)
-    std::memcpy(c->ft[ids[i]], c->pinned + (size_t)i * kSlotVals, kSlotVals * 8);
-  c->ft_valid = true;
+  (void)nb;
+  ft_store(c, ids);
   if (*herr != ~0ull) {
     const long long ncell = (long long)c->grid.nx * c->grid.ny * c->grid.nz;
     const long long stp = (long long)(*herr / (unsigned long long)ncell);

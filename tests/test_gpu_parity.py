@@ -319,3 +319,60 @@ def test_trt_forced_channel_with_sphere():
     o, g = _run_pair(20, 16, 12, 19, 0.7, (0, 1, 0), 1, 1, "f64", "two_array", [body], 40, 3,
                      u0=(0.0, 0.0, 0.0), force=(1e-5, 0.0, 2e-6), collision="trt")
     assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+
+
+@pytest.mark.parametrize("world_bc", [(0, 0, 0), (0, 1, 1)])
+def test_two_way_coupled_bodies(world_bc):
+    """NEXT rank 1: dynamic bodies driven by their own Eq.(10)-(11) force/torque every step
+    (semi-implicit Euler on the host), vs the oracle's independent integrator."""
+    n = (40, 36, 32)
+    v, tr = pi.propeller_mesh(n_blades=3, scale=0.07, n_st=8, n_pts=16, hub_seg=16)
+    o = oracle.Oracle(*n, 19, 0.7, world_bc, 1, 1)
+    g = _sim(nx=n[0], ny=n[1], nz=n[2], Q=19, tau=0.7, bc=world_bc, sc=1, bmode=1)
+    rho, u = pi.perturbed_flow(n[::-1], 29, u0=(0.02, 0.0, 0.0))
+    o.init_equilibrium(rho, u)
+    g.init_equilibrium(rho, u)
+    I_mesh = np.array([[900.0, 20.0, 0.0], [20.0, 700.0, 5.0], [0.0, 5.0, 800.0]])
+    o.set_sphere(1, 4.0, 1)
+    o.set_pose(1, np.eye(3), (12.0, 18.0, 16.0), (0.0, 0.0, 0.01), (0, 0, 0))
+    o.set_dynamics(1, 2500.0, np.eye(3) * 16000.0, (0.0, -0.5, 0.0))
+    g.set_sphere(1, 4.0, 1, np.eye(3), (12.0, 18.0, 16.0), (0.0, 0.0, 0.01), (0, 0, 0))
+    g.set_dynamics(1, 2500.0, np.eye(3) * 16000.0, (0.0, -0.5, 0.0))
+    Q0 = pi.rotation_about([1, 0, 1], 0.3)
+    o.set_mesh(2, v, tr, 1)
+    o.set_pose(2, Q0, (28.0, 18.0, 16.0), (0, 0, 0), (0.0, 0.02, 0.0))
+    o.set_dynamics(2, 3000.0, I_mesh, (0, 0, 0), (0.0, 0.0, 0.3))
+    g.set_mesh(2, v, tr, 1, Q0, (28.0, 18.0, 16.0), (0, 0, 0), (0.0, 0.02, 0.0))
+    g.set_dynamics(2, 3000.0, I_mesh, (0, 0, 0), (0.0, 0.0, 0.3))
+    for k in range(30):
+        o.map()
+        o.step(1)
+        o.integrate()
+        g.step(1)
+        for b in (1, 2):
+            so, sg = o.body_state(b), g.body_state(b)
+            for a, c in zip(so, sg):
+                assert np.allclose(a, c, rtol=1e-11, atol=1e-14), (k, b, a, c)
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+    assert not np.allclose(g.body_state(1)[2], (0.0, 0.0, 0.01))  # it really was coupled
+
+
+def test_neighbouring_bodies_sharing_tiles_keep_their_fractions():
+    """Regression: two bodies whose cell boxes are disjoint but share 32x4x2 tiles; remapping
+    one (single-body fast path) must not clear the other's words."""
+    n = (64, 24, 24)
+    o = oracle.Oracle(*n, 19, 0.7, (0, 0, 0), 1, 1)
+    g = _sim(nx=n[0], ny=n[1], nz=n[2], Q=19, tau=0.7, sc=1, bmode=1)
+    for sim in (g,):
+        sim.set_sphere(1, 3.0, 2, np.eye(3), (6.0, 12.0, 12.0))
+        sim.set_sphere(2, 3.0, 2, np.eye(3), (20.0, 12.0, 12.0), (1 / 32, 0, 0))
+    o.set_sphere(1, 3.0, 2)
+    o.set_sphere(2, 3.0, 2)
+    for k in range(5):
+        o.set_pose(1, np.eye(3), (6.0, 12.0, 12.0))
+        o.set_pose(2, np.eye(3), (20.0 + k / 32, 12.0, 12.0), (1 / 32, 0, 0))
+        o.map()
+        if k:
+            g.step(1)
+        assert np.array_equal(o.fractions()[2], g.fractions()[2]), k
+        assert np.array_equal(o.fractions()[1], g.fractions()[1]), k
