@@ -363,6 +363,7 @@ def test_neighbouring_bodies_sharing_tiles_keep_their_fractions():
     n = (64, 24, 24)
     o = oracle.Oracle(*n, 19, 0.7, (0, 0, 0), 1, 1)
     g = _sim(nx=n[0], ny=n[1], nz=n[2], Q=19, tau=0.7, sc=1, bmode=1)
+    g.init_equilibrium()
     for sim in (g,):
         sim.set_sphere(1, 3.0, 2, np.eye(3), (6.0, 12.0, 12.0))
         sim.set_sphere(2, 3.0, 2, np.eye(3), (20.0, 12.0, 12.0), (1 / 32, 0, 0))
