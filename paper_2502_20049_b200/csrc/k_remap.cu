@@ -7,11 +7,10 @@
 //   L0  one thread per tile of the box     : tile-centre test with reach kTileReach bricks
 //   L1  one thread per 8-cell segment      : segment-centre test with reach kSubReach
 //   L2  one thread per cell                : fp32 centre test against dilated-by-one bricks
-//   L3  one thread per (cell, sub-sample)  : exact fp64 inside test (reading R1, A14 order)
-//   L4  one thread per narrow-band cell    : count -> word
+//   L3  one thread per narrow-band cell    : exact fp64 inside test of each sub-sample
+//                                            (reading R1, A14 order), count -> word
 // Every early decision is conservative (it only claims "all sub-samples outside/inside" when the
-// brick flags prove it), so the words equal the brute-force counts bit for bit.  Counts are
-// integers accumulated with atomics: order-independent.  Tile flags ("any word nonzero") are
+// brick flags prove it), so the words equal the brute-force counts bit for bit.  Tile flags ("any word nonzero") are
 // reset for every tile that reaches L1 and set by whichever level writes a nonzero word.
 #include "psm_device.cuh"
 #include "psm_internal.h"
@@ -104,7 +103,8 @@ __global__ void k_remap_l1(const __grid_constant__ RemapParams r) {
   }
 }
 
-// L2: one thread per cell of the listed segments
+// L2: one thread per cell of the listed segments: fp32 centre test against the dilated-by-one
+// brick flags; decided cells are written, narrow-band cells appended to the band list.
 __global__ void k_remap_l2(const __grid_constant__ RemapParams r) {
   const Geom& G = r.g;
   const int ncell = min(r.counters[1], r.seg_cap) * kSubX;
@@ -130,12 +130,11 @@ __global__ void k_remap_l2(const __grid_constant__ RemapParams r) {
       const int k = atomicAdd(r.counters + 2, 1);
       if (k < r.band_cap) {
         r.band[k] = ((uint32_t)tile << 8) | (uint32_t)(row * kTileX + sx * kSubX + c);
-        r.bandcnt[k] = 0;
         continue;
       }
       int cnt = 0;  // list full: exact serial count here
-      for (int si = 0; si < (1 << (3 * b.s)); ++si)
-        cnt += sample_inside(b, x, y, G.z0 + z, si, L, G.wall);
+      for (int s2 = 0; s2 < (1 << (3 * b.s)); ++s2)
+        cnt += sample_inside(b, x, y, G.z0 + z, s2, L, G.wall);
       put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
       continue;
     }
@@ -154,29 +153,39 @@ __device__ __forceinline__ void band_cell(const RemapParams& r, uint32_t e, int&
   z = tz * kTileZ + c / (kTileX * kTileY);
 }
 
-// L3: one thread per (band cell, sub-sample), exact fp64 inside test
+// L3: one thread per narrow-band cell: all its sub-samples with the exact fp64 test (A14),
+// geometry-bit loads issued 8 at a time, and the word written directly.
 __global__ void k_remap_l3(const __grid_constant__ RemapParams r) {
   const Geom& G = r.g;
   const BodyGeo& b = r.body;
-  const int ls = 3 * b.s;
-  const long long items = (long long)min(r.counters[2], r.band_cap) << ls;
-  const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < items;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(i >> ls), si = (int)(i & ((1 << ls) - 1));
-    int x, y, z, tile;
-    band_cell(r, r.band[k], x, y, z, tile);
-    if (sample_inside(b, x, y, G.z0 + z, si, L, G.wall)) atomicAdd(r.bandcnt + k, 1);
-  }
-}
-
-// L4: one thread per band cell -> word
-__global__ void k_remap_l4(const __grid_constant__ RemapParams r) {
   const int n = min(r.counters[2], r.band_cap);
+  const int nsamp = 1 << (3 * b.s);
+  const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     int x, y, z, tile;
     band_cell(r, r.band[k], x, y, z, tile);
-    const int cnt = r.bandcnt[k];
+    const int zg = G.z0 + z;
+    int cnt = 0;
+    for (int s0 = 0; s0 < nsamp; s0 += 8) {
+      const int m = min(8, nsamp - s0);
+      if (b.kind == 0) {
+        for (int j = 0; j < m; ++j) cnt += sample_inside(b, x, y, zg, s0 + j, L, G.wall);
+        continue;
+      }
+      long long wi[8];
+      int bit[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        wi[j] = -1;
+        bit[j] = 0;
+        if (j < m) mesh_word_index(b, x, y, zg, s0 + j, L, G.wall, wi[j], bit[j]);
+      }
+      unsigned long long w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j] = (wi[j] >= 0) ? __ldg(b.bits + wi[j]) : 0ull;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cnt += (int)((w[j] >> bit[j]) & 1ull);
+    }
     put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
   }
 }
@@ -192,7 +201,6 @@ cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cud
   k_remap_l1<<<persistent_blocks, 256, 0, st>>>(r);
   k_remap_l2<<<persistent_blocks, 256, 0, st>>>(r);
   k_remap_l3<<<persistent_blocks, 256, 0, st>>>(r);
-  k_remap_l4<<<persistent_blocks, 256, 0, st>>>(r);
   return cudaGetLastError();
 }
 

@@ -645,7 +645,7 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
       r.seg_cap = c->seg_cap;
       r.band_cap = c->band_cap;
       CUDA_TRY(c, launch_remap_single(r, 148 * 8, c->st));
-      c->launches += 5;
+      c->launches += 4;
       continue;
     }
     // general box (several bodies may cover its cells): one launch, 3D grid of its tiles

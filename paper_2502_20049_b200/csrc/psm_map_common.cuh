@@ -16,6 +16,36 @@ __device__ __forceinline__ void body_frame(const BodyGeo& b, const double p[3], 
     q[a] = __fma_rn(b.Q[6 + a], d[2], __fma_rn(b.Q[3 + a], d[1], __dmul_rn(b.Q[a], d[0])));
 }
 
+// word index and bit of sub-sample `si` of cell (x, y, zg) in a mesh body's geometry field
+// (wi = -1: outside the field, i.e. outside the body); same arithmetic as sample_inside
+__device__ __forceinline__ void mesh_word_index(const BodyGeo& b, int x, int y, int zg, int si,
+                                                const double L[3], const int wall[3],
+                                                long long& wi, int& bitpos) {
+  const int n = 1 << b.s;
+  const double h = ldexp(1.0, -b.s);
+  const int gx = si & (n - 1), gy = (si >> b.s) & (n - 1), gz = si >> (2 * b.s);
+  const double p[3] = {(double)x + (gx + 0.5) * h, (double)y + (gy + 0.5) * h,
+                       (double)zg + (gz + 0.5) * h};
+  double q[3];
+  body_frame(b, p, L, wall, q);
+  const double hs = ldexp(1.0, b.s);
+  int g[3];
+  wi = -1;
+  bitpos = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double xx = floor(__dmul_rn(__dsub_rn(q[a], b.o[a]), hs));
+    if (!(xx >= 0.0) || xx >= (double)(b.dims_b[a] << b.s)) return;
+    g[a] = (int)xx;
+  }
+  const int msk = n - 1;
+  const long long brick =
+      ((long long)(g[2] >> b.s) * b.dims_b[1] + (g[1] >> b.s)) * b.dims_b[0] + (g[0] >> b.s);
+  const int bit = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
+  wi = brick * b.words + (bit >> 6);
+  bitpos = bit & 63;
+}
+
 __device__ __forceinline__ int mesh_bit(const BodyGeo& b, const double q[3]) {
   const double hs = ldexp(1.0, b.s);
   int g[3];

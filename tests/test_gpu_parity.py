@@ -374,6 +374,7 @@ def test_neighbouring_bodies_sharing_tiles_keep_their_fractions():
         o.set_pose(2, np.eye(3), (20.0 + k / 32, 12.0, 12.0), (1 / 32, 0, 0))
         o.map()
         if k:
-            g.step(1)
+            g.step(1)       # collides step k-1, then the body sits at pose k
+            g.map_fractions()  # fractions at the current pose
         assert np.array_equal(o.fractions()[2], g.fractions()[2]), k
         assert np.array_equal(o.fractions()[1], g.fractions()[1]), k
