@@ -40,6 +40,14 @@ WORKLOADS = {
                 desc="c5 weak: D3Q19 PSM fp32, 512^3 per GPU, CROR-like counter-rotating rotor "
                      "pair per GPU (12+10 blades, ~1.1 M faces, s=1, remapped every step), SC1, "
                      "weighted B"),
+    # c5 strong scaling: the whole ~1e9-cell CROR-like domain split over the GPUs (rotor axis x:
+    # front 12 blades tip 220 at x=760, +Omega; rear 10 blades tip 200 at x=900, -Omega)
+    "c5s": dict(nx=2048, ny=704, nz=704, Q=19, prec="f32", tau=0.55, rotors=True, s=1,
+                omega=0.05 / 220.0, pattern="two_array", sc=1, bmode=1, strong=True,
+                rotor_x=(760.0, 900.0), rotor_tip=(220.0, 200.0),
+                desc="c5 strong: D3Q19 PSM fp32, 2048x704x704 = 1.015e9 cells split over the "
+                     "GPUs, CROR-like counter-rotating rotor pair (12+10 blades, s=1, remapped "
+                     "every step), SC1, weighted B"),
     "c4": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.6, r=64.0, s=1,
                v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
                desc="c4: D3Q19 PSM fp32 512^3/GPU periodic, sphere r=64 translating "
@@ -184,9 +192,9 @@ def run_reference(args, wl, rank, world):
     cb = oracle_sample(wl, max(1, args.steps), per_step_budget * args.steps, 7)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": wl["desc"], "parallelism": "cpu oracle (OpenMP)"},
+            "higher_is_better": True, "scaling": "strong" if wl.get("strong") else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": workload_config(wl, world),
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -194,12 +202,23 @@ def run_reference(args, wl, rank, world):
     return 0
 
 
+def workload_config(wl: dict, world: int) -> dict:
+    nx, ny = wl["nx"], wl["ny"]
+    nzg = wl["nz"] if wl.get("strong") else wl["nz"] * world
+    return {"workload": wl["desc"], "grid": [nx, ny, nzg],
+            "cells_per_gpu": nx * ny * nzg // world, "global_cells": nx * ny * nzg,
+            "stencil": f"D3Q{wl['Q']}", "pattern": wl["pattern"],
+            "parallelism": f"z-slab x{world}" + (" + NCCL halo" if world > 1 else ""),
+            "l2": "inputs larger than L2 (PDF arrays >> 126 MB)"}
+
+
 def build_workload(psm, wl: dict, rank: int, world: int, nccl_id=None):
     """The bench's simulation: the grid of `wl` (nz per GPU stacked in z), rest fluid, and the
     bodies (a CROR-like rotor pair or one moving sphere per GPU slab; every rank holds every
     body so the force/torque allreduce is consistent).  Returns (sim, body_poses, nbodies, S)."""
     import psm_inputs as pi
-    nx, ny, nzg = wl["nx"], wl["ny"], wl["nz"] * world
+    nx, ny = wl["nx"], wl["ny"]
+    nzg = wl["nz"] if wl.get("strong") else wl["nz"] * world
     S = 8 if wl["prec"] == "f64" else 4
     sim = psm.Simulation(nx, ny, nzg, Q=wl["Q"], tau=wl["tau"], bc=(0, 0, 0), prec=wl["prec"],
                          pattern=wl["pattern"], sc=wl["sc"], bmode=wl["bmode"], rank=rank,
@@ -207,13 +226,17 @@ def build_workload(psm, wl: dict, rank: int, world: int, nccl_id=None):
     sim.init_equilibrium(None, None)
     nbodies = 0
     body_poses = []  # (Q0, t0, v, w) per body, in id order
-    for r in range(world):
+    for r in range(1 if wl.get("strong") else world):
         zc = (nzg * r) // world + ((nzg * (r + 1)) // world - (nzg * r) // world) / 2
+        if wl.get("strong"):
+            zc = nzg / 2
         if wl.get("rotors"):
             for k, front in enumerate((True, False)):
-                v, t = pi.cror_rotor(front)
+                tip = wl.get("rotor_tip", (200.0, 180.0))[k]
+                v, t = pi.propeller_mesh(n_blades=12 if front else 10, scale=tip / 110.0,
+                                         n_st=200, n_pts=128, hub_seg=256)
                 w = (wl["omega"] if front else -wl["omega"], 0.0, 0.0)
-                tpos = (200.0 if front else 330.0, ny / 2, zc)
+                tpos = (wl.get("rotor_x", (200.0, 330.0))[k], ny / 2, zc)
                 sim.set_mesh(1 + 2 * r + k, v, t, wl["s"], np.eye(3), tpos, (0, 0, 0), w)
                 body_poses.append((np.eye(3), tpos, (0.0, 0.0, 0.0), w))
                 nbodies += 1
@@ -279,7 +302,8 @@ def main():
         nccl_id = bytes(idt.cpu().numpy().tobytes())
 
     sim, body_poses, nbodies, S = build_workload(psm, wl, rank, world, nccl_id)
-    nx, ny, nzg = wl["nx"], wl["ny"], wl["nz"] * world
+    nx, ny = wl["nx"], wl["ny"]
+    nzg = wl["nz"] if wl.get("strong") else wl["nz"] * world
     z0, nzl = sim.z0, sim.nzl
     stream = torch.cuda.current_stream()
 
@@ -375,13 +399,9 @@ def main():
         line = {
             "metric": METRIC, "value": mlups, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": wl["prec"], "data": "synthetic",
-            "config": {"workload": wl["desc"], "grid": [nx, ny, nzg],
-                       "cells_per_gpu": cells_local, "global_cells": cells_total,
-                       "stencil": f"D3Q{wl['Q']}", "pattern": wl["pattern"],
-                       "parallelism": f"z-slab x{world}" + (" + NCCL halo" if world > 1 else ""),
-                       "l2": "inputs larger than L2 (PDF arrays >> 126 MB)"},
+            "higher_is_better": True, "scaling": "strong" if wl.get("strong") else "weak",
+            "vs_baseline": None, "dtype": wl["prec"], "data": "synthetic",
+            "config": workload_config(wl, world),
             "mlups_per_gpu": mlups / world,
             "roofline_frac_step": step_gbs / peak,
             "roofline": {"bound": "hbm", "kernel": "k_collide (fused PSM stream-collide)",
