@@ -128,6 +128,11 @@ psm_status psm_read_velocity(psm_ctx* ctx, double* rho, double* u);
  *   PSM_MESH  : closed triangle mesh verts[nverts][3] (fp64), tris[ntris][3] (int32, 0-based).
  *               Voxelised ONCE into the super-sampled binary geometry field
  *               by an exact fixed-point ray-parity test (reading A15). */
+/* Mesh fraction mapping (reading A12): R1 maps every sub-sample of the world-fixed cell
+ * into the body frame (consistent overlap estimator; default); R2 is the paper's literal wording
+ * — transform only the cell centre q_c and average the 2^s x 2^s x 2^s geometry
+ * cells g with g_a in [g0_a, g0_a + 2^s), g0_a = floor((q_c,a - o_a) 2^s - 2^(s-1) + 1/2). */
+typedef enum { PSM_MAP_R1 = 0, PSM_MAP_R2 = 1 } psm_mapping;
 typedef struct {
   int32_t kind; /* psm_shape_kind */
   int32_t s;
@@ -136,6 +141,7 @@ typedef struct {
   int64_t nverts;
   const int32_t* tris;
   int64_t ntris;
+  int32_t mapping; /* psm_mapping (meshes; spheres always sample, R1) */
 } psm_shape;
 typedef struct {
   double Q[9]; /* row-major rotation body -> world: x_world = Q x_body + t                   */

@@ -69,6 +69,7 @@ def lib():
             "orc_error_cell": (I64, [P]),
             "orc_force_torque": (None, [P, I, P, P, P, P]),
             "orc_set_dynamics": (None, [P, I, D, P, P, P]),
+            "orc_set_mapping": (None, [P, I, I]),
             "orc_integrate": (None, [P]),
             "orc_get_body_state": (None, [P, I, P, P, P, P]),
         }
@@ -217,6 +218,10 @@ class Oracle:
         verts = _f64(verts)
         tris = np.ascontiguousarray(tris, np.int32)
         assert lib().orc_set_mesh(self._h, bid, _p(verts), len(verts), _p(tris), len(tris), s) == 0
+
+    def set_mapping(self, bid, mode: str):
+        """Mesh fraction mapping: "R1" every sub-sample (default) or "R2" centre only (A12)."""
+        lib().orc_set_mapping(self._h, bid, 1 if mode == "R2" else 0)
 
     def remove_body(self, bid):
         lib().orc_remove_body(self._h, bid)

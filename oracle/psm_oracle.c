@@ -366,6 +366,7 @@ typedef struct {
   double radius, rbound;
   double Q[9], t[3], v[3], w[3];
   int dynamic;          /* two-way coupled: orc_integrate advances Q, t, v, w */
+  int mapping;          /* meshes: 0 = R1 every sub-sample, 1 = R2 centre only (A12) */
   double mass, I[9], fext[3], text[3];
   double gorigin[3];
   int64_t gdims[3];
@@ -575,6 +576,37 @@ static int sample_inside(const orc_sim* S, const orc_body* b, const double p[3])
   return b->gbits[(g[2] * b->gdims[1] + g[1]) * b->gdims[0] + g[0]];
 }
 
+/* Reading R2 of the mapping (A12; the paper's literal wording: "multiplying the
+ * cell center in LBM space with a rotation matrix"): only the cell centre p_c is mapped into the
+ * body frame, q_c = Q^T mi(p_c - t) (A14 order), and the count is the number of set geometry cells
+ * g with g_a in [g0_a, g0_a + 2^s), g0_a = floor((q_c,a - o_a) 2^s - 2^(s-1) + 1/2): the block of
+ * 2^s x 2^s x 2^s geometry cells "corresponding" to the cell.  Cells beyond the
+ * field count 0. */
+static int r2_count(const orc_sim* S, const orc_body* b, int x, int y, int z) {
+  double L[3] = {S->nx, S->ny, S->nz};
+  double pc[3] = {x + 0.5, y + 0.5, z + 0.5}, d[3], q[3];
+  for (int a = 0; a < 3; ++a) d[a] = mi(pc[a] - b->t[a], L[a], S->bc[a] == 0);
+  for (int a = 0; a < 3; ++a)
+    q[a] = fma(b->Q[6 + a], d[2], fma(b->Q[3 + a], d[1], b->Q[0 + a] * d[0]));
+  int n = 1 << b->s;
+  double hs = ldexp(1.0, b->s), half = ldexp(1.0, b->s - 1);
+  int64_t g0[3];
+  for (int a = 0; a < 3; ++a) g0[a] = (int64_t)floor((q[a] - b->gorigin[a]) * hs - half + 0.5);
+  int cnt = 0;
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        int64_t g[3] = {g0[0] + i, g0[1] + j, g0[2] + k};
+        int in = 1;
+        for (int a = 0; a < 3; ++a)
+          if (g[a] < 0 || g[a] >= b->gdims[a]) in = 0;
+        if (in) cnt += b->gbits[(g[2] * b->gdims[1] + g[1]) * b->gdims[0] + g[0]];
+      }
+  return cnt;
+}
+
+void orc_set_mapping(orc_sim* S, int id, int mode) { S->bodies[id].mapping = mode; }
+
 /* Fraction mapping: for each cell, eps_b = (#inside sub-samples)/2^(3s) over
  * the 2^(3s) sub-cell centres (A16); the body with the largest eps wins, ties to the lower id
  * (A18); B by Eq.(5)/(6); u_s = v + w x mi(x_c - t) (rigid motion). */
@@ -598,12 +630,16 @@ void orc_map(orc_sim* S) {
           }
           int n = 1 << b->s, cnt = 0;
           double h = ldexp(1.0, -b->s);
-          for (int gz = 0; gz < n; ++gz)
-            for (int gy = 0; gy < n; ++gy)
-              for (int gx = 0; gx < n; ++gx) {
-                double p[3] = {x + (gx + 0.5) * h, y + (gy + 0.5) * h, z + (gz + 0.5) * h};
-                cnt += sample_inside(S, b, p);
-              }
+          if (b->kind == 1 && b->mapping == 1) {
+            cnt = r2_count(S, b, x, y, z);
+          } else {
+            for (int gz = 0; gz < n; ++gz)
+              for (int gy = 0; gy < n; ++gy)
+                for (int gx = 0; gx < n; ++gx) {
+                  double p[3] = {x + (gx + 0.5) * h, y + (gy + 0.5) * h, z + (gz + 0.5) * h};
+                  cnt += sample_inside(S, b, p);
+                }
+          }
           /* compare eps exactly: cnt / 8^s as a dyadic double */
           double e = ldexp((double)cnt, -3 * b->s);
           double eb = best ? ldexp((double)bestcnt, -3 * S->bodies[best].s) : 0.0;

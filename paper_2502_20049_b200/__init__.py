@@ -30,6 +30,7 @@ PSM_TWO_ARRAY, PSM_AA = 0, 1
 PSM_PERIODIC, PSM_WALL = 0, 1
 PSM_SPHERE, PSM_MESH = 0, 1
 PSM_SRT, PSM_TRT = 0, 1
+PSM_MAP_R1, PSM_MAP_R2 = 0, 1
 PSM_MAX_BODIES = 16
 PSM_NUM_PHASES = 4
 PHASES = ("map", "collide", "ft_reduce", "halo")
@@ -61,7 +62,7 @@ class psm_options(C.Structure):
 class psm_shape(C.Structure):
     _fields_ = [("kind", C.c_int32), ("s", C.c_int32), ("radius", C.c_double),
                 ("verts", C.c_void_p), ("nverts", C.c_int64), ("tris", C.c_void_p),
-                ("ntris", C.c_int64)]
+                ("ntris", C.c_int64), ("mapping", C.c_int32)]
 
 
 class psm_pose(C.Structure):
@@ -349,15 +350,15 @@ class Simulation:
         return rho, u
 
     def set_sphere(self, bid, r, s, Q=np.eye(3), t=(0, 0, 0), v=(0, 0, 0), w=(0, 0, 0)):
-        sh = psm_shape(PSM_SPHERE, s, float(r), None, 0, None, 0)
+        sh = psm_shape(PSM_SPHERE, s, float(r), None, 0, None, 0, PSM_MAP_R1)
         psm_set_body(self.ctx, bid, sh, _pose(Q, t), _vel(v, w))
 
     def set_mesh(self, bid, verts, tris, s, Q=np.eye(3), t=(0, 0, 0), v=(0, 0, 0),
-                 w=(0, 0, 0)):
+                 w=(0, 0, 0), mapping="R1"):
         verts = _c64(verts)
         tris = np.ascontiguousarray(tris, np.int32)
         sh = psm_shape(PSM_MESH, s, 0.0, verts.ctypes.data, len(verts), tris.ctypes.data,
-                       len(tris))
+                       len(tris), PSM_MAP_R2 if mapping == "R2" else PSM_MAP_R1)
         psm_set_body(self.ctx, bid, sh, _pose(Q, t), _vel(v, w))
 
     def set_pose(self, bid, Q=np.eye(3), t=(0, 0, 0), v=(0, 0, 0), w=(0, 0, 0)):

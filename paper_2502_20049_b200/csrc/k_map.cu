@@ -80,6 +80,10 @@ __global__ void __launch_bounds__(kTileCells, 6) k_map(const __grid_constant__ M
     if (!act) cd = 0;
     int cnt = (cd == 1) ? (1 << (3 * s)) : 0;
     // (3) narrow band: pack (cell, sample) pairs of the warp's band cells over the lanes
+    if (b.mapping == 1 && cd == 2) {  // R2: one centre-only block count per band cell
+      cnt = r2_count(b, x, y, zg, L, G.wall);
+      cd = 3;
+    }
     const unsigned band = __ballot_sync(0xFFFFFFFFu, cd == 2);
     if (band) {
       const int ls = 3 * s;
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(kTileCells, 6) k_map(const __grid_constant__ M
         }
       }
     }
-    if (p.stats && act) atomicAdd(p.stats + 3 + cd, 1ull);
+    if (p.stats && act) atomicAdd(p.stats + 3 + (cd == 3 ? 2 : cd), 1ull);
     const double e = ldexp((double)cnt, -3 * s);
     if (cnt > 0 && e > beste) {
       best = id;

@@ -90,9 +90,7 @@ __global__ void k_remap_l1(const __grid_constant__ RemapParams r) {
                              (float)qs[2] + (float)b.Q[2] * off};
         const int cd = cell_decision(b, qc);
         int cnt = cd == 1 ? (1 << (3 * b.s)) : 0;
-        if (cd == 2)
-          for (int si = 0; si < (1 << (3 * b.s)); ++si)
-            cnt += sample_inside(b, x0 + c, y, G.z0 + z, si, L, G.wall);
+        if (cd == 2) cnt = exact_count(b, x0 + c, y, G.z0 + z, L, G.wall);
         put_word(r, x0 + c, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
       }
       continue;
@@ -132,9 +130,7 @@ __global__ void k_remap_l2(const __grid_constant__ RemapParams r) {
         r.band[k] = ((uint32_t)tile << 8) | (uint32_t)(row * kTileX + sx * kSubX + c);
         continue;
       }
-      int cnt = 0;  // list full: exact serial count here
-      for (int s2 = 0; s2 < (1 << (3 * b.s)); ++s2)
-        cnt += sample_inside(b, x, y, G.z0 + z, s2, L, G.wall);
+      const int cnt = exact_count(b, x, y, G.z0 + z, L, G.wall);  // list full: count here
       put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
       continue;
     }
@@ -166,6 +162,11 @@ __global__ void k_remap_l3(const __grid_constant__ RemapParams r) {
     band_cell(r, r.band[k], x, y, z, tile);
     const int zg = G.z0 + z;
     int cnt = 0;
+    if (b.mapping == 1) {  // R2: centre-only block count
+      cnt = r2_count(b, x, y, zg, L, G.wall);
+      put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
+      continue;
+    }
     for (int s0 = 0; s0 < nsamp; s0 += 8) {
       const int m = min(8, nsamp - s0);
       if (b.kind == 0) {

@@ -31,7 +31,7 @@ constexpr size_t kGeomCapBytes = 1ull << 30;
 
 struct Body {
   bool present = false;
-  int kind = 0, s = 0;
+  int kind = 0, s = 0, mapping = 0;
   double radius = 0, rbound = 0;
   double bmin[3] = {0, 0, 0}, bmax[3] = {0, 0, 0};  // body-frame AABB of the shape
   // mesh geometry field (device)
@@ -569,6 +569,7 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
     g.s = b.s;
     g.words = b.words;
     g.present = 1;
+    g.mapping = b.mapping;
     g.bits = b.d_bits;
     g.mask = b.d_mask;
   }
@@ -1029,6 +1030,9 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
     Body nb;
     nb.kind = shape->kind;
     nb.s = shape->s;
+    if (shape->mapping != PSM_MAP_R1 && shape->mapping != PSM_MAP_R2)
+      FAIL(c, PSM_E_ARG, "unknown mapping mode");
+    nb.mapping = shape->kind == PSM_MESH ? shape->mapping : PSM_MAP_R1;
     if (shape->kind == PSM_SPHERE) {
       if (!(shape->radius > 0.0) || !std::isfinite(shape->radius))
         FAIL(c, PSM_E_ARG, "sphere radius must be > 0");

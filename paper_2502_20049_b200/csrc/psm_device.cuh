@@ -75,6 +75,8 @@ struct BodyGeo {
   int s;
   int words;        // uint64 words per brick = max(1, 8^s / 64)
   int present;
+  int mapping;      // 0 R1 (per sub-sample), 1 R2 (centre-only block average), meshes only
+  int pad_;
   const unsigned long long* bits;  // [brick][words]
   const uint8_t* mask;             // [brick] flag bits, see pack_bricks (voxelize.cpp)
 };

@@ -63,6 +63,43 @@ __device__ __forceinline__ int mesh_bit(const BodyGeo& b, const double q[3]) {
   return (int)((w >> (bit & 63)) & 1ull);
 }
 
+// geometry bit g (in field range) of a mesh body
+__device__ __forceinline__ int field_bit(const BodyGeo& b, int gx, int gy, int gz) {
+  const int n = 1 << b.s, msk = n - 1;
+  const long long brick =
+      ((long long)(gz >> b.s) * b.dims_b[1] + (gy >> b.s)) * b.dims_b[0] + (gx >> b.s);
+  const int bit = (((gz & msk) * n) + (gy & msk)) * n + (gx & msk);
+  return (int)((__ldg(b.bits + brick * b.words + (bit >> 6)) >> (bit & 63)) & 1ull);
+}
+
+// R2 (paper-literal): only the cell centre is transformed (A14 arithmetic); the
+// count is the number of set geometry cells in the 2^s-cube block whose lower corner is
+// g0 = floor((q_c - o) 2^s - 2^(s-1) + 1/2); cells beyond the field count 0.
+static __device__ __noinline__ int r2_count(const BodyGeo& b, int x, int y, int zg, const double L[3],
+                                     const int wall[3]) {
+  const double pc[3] = {x + 0.5, y + 0.5, zg + 0.5};
+  double q[3];
+  body_frame(b, pc, L, wall, q);
+  const int n = 1 << b.s;
+  const double hs = ldexp(1.0, b.s), half = ldexp(1.0, b.s - 1);
+  long long g0[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    g0[a] = (long long)floor(__dadd_rn(__dsub_rn(__dmul_rn(__dsub_rn(q[a], b.o[a]), hs), half),
+                                       0.5));
+  int cnt = 0;
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        const long long gx = g0[0] + i, gy = g0[1] + j, gz = g0[2] + k;
+        if (gx < 0 || gy < 0 || gz < 0 || gx >= ((long long)b.dims_b[0] << b.s) ||
+            gy >= ((long long)b.dims_b[1] << b.s) || gz >= ((long long)b.dims_b[2] << b.s))
+          continue;
+        cnt += field_bit(b, (int)gx, (int)gy, (int)gz);
+      }
+  return cnt;
+}
+
 // exact inside test of sub-sample `si` (0 .. 8^s - 1) of cell (x, y, zg) for body b (reading R1,
 // A14 arithmetic: dyadic sample point, q = Q^T mi(p - t) with the fixed fma order)
 __device__ __forceinline__ int sample_inside(const BodyGeo& b, int x, int y, int zg, int si,
@@ -166,4 +203,13 @@ __device__ __forceinline__ int cell_decision(const BodyGeo& b, const float qc[3]
 // it without block barriers: (1) per 8-cell segment (reach kSubReach bricks), (2) per cell in
 // fp32 (dilated-by-one brick flags), (3) the narrow-band cells' sub-samples packed across the 32
 // lanes (lane -> (cell, sample) pairs) and counted with ballots — exact fp64 per sample.
+// exact count of a cell for body b (R1: all sub-samples; R2: the centre block)
+__device__ __forceinline__ int exact_count(const BodyGeo& b, int x, int y, int zg,
+                                           const double L[3], const int wall[3]) {
+  if (b.mapping == 1) return r2_count(b, x, y, zg, L, wall);
+  int cnt = 0;
+  for (int si = 0; si < (1 << (3 * b.s)); ++si) cnt += sample_inside(b, x, y, zg, si, L, wall);
+  return cnt;
+}
+
 }  // namespace psm

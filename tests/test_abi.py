@@ -34,7 +34,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(psm.psm_options) == 16 + 24 + 8 + 16 + 8 + 8
     assert C.sizeof(psm.psm_pose) == 12 * 8
     assert C.sizeof(psm.psm_velocity) == 6 * 8
-    assert C.sizeof(psm.psm_shape) == 8 + 8 + 8 + 8 + 8 + 8
+    assert C.sizeof(psm.psm_shape) == 8 + 8 + 8 + 8 + 8 + 8 + 8
     assert psm.load().psm_nccl_id_bytes() == 128
 
 

@@ -52,8 +52,9 @@ def _run_pair(nx, ny, nz, Q, tau, bc, sc, bmode, prec, pattern, bodies, steps, s
                          b.get("w", (0, 0, 0)))
         else:
             o.set_mesh(b["id"], b["verts"], b["tris"], b["s"])
+            o.set_mapping(b["id"], b.get("mapping", "R1"))
             g.set_mesh(b["id"], b["verts"], b["tris"], b["s"], Qp, tp, b.get("v", (0, 0, 0)),
-                       b.get("w", (0, 0, 0)))
+                       b.get("w", (0, 0, 0)), mapping=b.get("mapping", "R1"))
         o.set_pose(b["id"], Qp, tp, b.get("v", (0, 0, 0)), b.get("w", (0, 0, 0)))
     worst_ft = 0.0
     for k in range(steps):
@@ -378,3 +379,21 @@ def test_neighbouring_bodies_sharing_tiles_keep_their_fractions():
             g.map_fractions()  # fractions at the current pose
         assert np.array_equal(o.fractions()[2], g.fractions()[2]), k
         assert np.array_equal(o.fractions()[1], g.fractions()[1]), k
+
+
+@pytest.mark.parametrize("s", [1, 2])
+def test_r2_centre_only_mapping_rotating_mesh(s):
+    """NEXT rank 3: the paper-literal centre-only mapping (R2) on a rotating mesh, both remap
+    paths (single-body pipeline and, with a second body sharing tiles, the general kernel)."""
+    v, tr = pi.propeller_mesh(n_blades=4, scale=0.09, n_st=8, n_pts=16, hub_seg=16)
+    w = np.array([0.0, 0.03, 0.01])
+
+    def pose(k):
+        return oracle.pose_advance(pi.rotation_about([1, 0, 0], 0.2), [20.3, 18.0, 17.6],
+                                   [0, 0, 0], w, k, [48, 36, 34], [1, 1, 1])
+
+    bodies = [dict(id=1, kind="mesh", verts=v, tris=tr, s=s, pose=pose, w=w, mapping="R2"),
+              dict(id=2, kind="sphere", r=3.0, s=1, pose=_static(t=(36.0, 18.0, 17.0)))]
+    o, g = _run_pair(48, 36, 34, 19, 0.7, (0, 0, 0), 1, 1, "f64", "two_array", bodies, 25, 8,
+                     u0=(0.02, 0.0, 0.0))
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL

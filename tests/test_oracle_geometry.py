@@ -232,3 +232,45 @@ def test_p10_voxel_volume_matches_mesh_volume():
         _, bits = oracle.voxelize(v, tr, s)
         got = bits.sum() * 8.0 ** -s
         assert abs(got / vol - 1) < (0.06 if s == 1 else 0.03), (s, got, vol)
+
+
+# ------------------------------------------------------ R2: centre-only mapping (NEXT rank 3) ---
+@pytest.mark.parametrize("s", [0, 1, 2])
+def test_r2_equals_r1_at_aligned_identity_pose(s):
+    """At identity pose with a lattice-vertex translation the centre-only block (R2) is exactly the
+    sub-sample set of R1: counts identical."""
+    v, t = pi.propeller_mesh(n_blades=3, scale=0.1, n_st=8, n_pts=16, hub_seg=16)
+    o = oracle.Oracle(32, 32, 32, 19, 0.8, (0, 0, 0), 1, 0)
+    o.set_mesh(1, v, t, s)
+    o.set_pose(1, np.eye(3), (16.0, 15.0, 17.0))
+    o.map()
+    c1 = o.fractions()[2]
+    o.set_mapping(1, "R2")
+    o.map()
+    c2 = o.fractions()[2]
+    assert np.array_equal(c1, c2) and c1.sum() > 0
+
+
+def test_r2_rot90_permutation_and_volume():
+    v, tr = pi.propeller_mesh(n_blades=3, scale=0.1, n_st=8, n_pts=16, hub_seg=16)
+    n = 32
+    tpos = np.array([16.0, 16.0, 16.0])
+    o = oracle.Oracle(n, n, n, 19, 0.8, (0, 0, 0), 1, 0)
+    o.set_mesh(1, v, tr, 1)
+    o.set_mapping(1, "R2")
+    o.set_pose(1, np.eye(3), tpos)
+    o.map()
+    c0 = o.fractions()[2]
+    R = pi.rot90(2, 1)
+    o.set_pose(1, R, tpos)
+    o.map()
+    cR = o.fractions()[2]
+    z, y, x = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    xc = np.stack([x, y, z], 0).reshape(3, -1) + 0.5
+    xp = np.rint(tpos[:, None] + R.T @ (xc - tpos[:, None]) - 0.5).astype(int) % n
+    assert np.array_equal(cR, c0[xp[2], xp[1], xp[0]].reshape(n, n, n))
+    # generic pose: the block average still estimates the volume
+    o.set_pose(1, pi.rotation_about([1, 2, 3], 0.7), tpos + 0.3)
+    o.map()
+    vol = np.einsum("ij,ij->i", v[tr[:, 0]], np.cross(v[tr[:, 1]], v[tr[:, 2]])).sum() / 6.0
+    assert abs(o.fractions()[2].sum() / 8 / vol - 1) < 0.1
