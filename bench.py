@@ -275,8 +275,12 @@ def main():
     ap.add_argument("--config", default="c5w", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--s", type=int, default=None, help="override the super-sampling exponent")
     args = ap.parse_args()
-    wl = WORKLOADS[args.config]
+    wl = dict(WORKLOADS[args.config])
+    if args.s is not None:
+        wl["s"] = args.s
+        wl["desc"] += f" [s overridden to {args.s}]"
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))

@@ -128,6 +128,7 @@ __global__ void k_remap_l2(const __grid_constant__ RemapParams r) {
       const int k = atomicAdd(r.counters + 2, 1);
       if (k < r.band_cap) {
         r.band[k] = ((uint32_t)tile << 8) | (uint32_t)(row * kTileX + sx * kSubX + c);
+        r.bandcnt[k] = 0;
         continue;
       }
       const int cnt = exact_count(b, x, y, G.z0 + z, L, G.wall);  // list full: count here
@@ -175,11 +176,15 @@ __global__ void k_remap_l3(const __grid_constant__ RemapParams r) {
       }
       long long wi[8];
       int bit[8];
+      if (m == 8) {
+        mesh_word_index8(b, x, y, zg, s0, L, G.wall, wi, bit);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        wi[j] = -1;
-        bit[j] = 0;
-        if (j < m) mesh_word_index(b, x, y, zg, s0 + j, L, G.wall, wi[j], bit[j]);
+        for (int j = 0; j < 8; ++j) {
+          wi[j] = -1;
+          bit[j] = 0;
+          if (j < m) mesh_word_index(b, x, y, zg, s0 + j, L, G.wall, wi[j], bit[j]);
+        }
       }
       unsigned long long w[8];
 #pragma unroll
@@ -187,6 +192,49 @@ __global__ void k_remap_l3(const __grid_constant__ RemapParams r) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) cnt += (int)((w[j] >> bit[j]) & 1ull);
     }
+    put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
+  }
+}
+
+// L3 for s >= 2 (64 or 512 sub-samples per cell): one thread per (band cell, 8-sample chunk),
+// batched geometry-bit loads, integer atomics into the cell's count (order-independent); L4
+// writes the words.
+__global__ void k_remap_l3_chunks(const __grid_constant__ RemapParams r) {
+  const Geom& G = r.g;
+  const BodyGeo& b = r.body;
+  const int n = min(r.counters[2], r.band_cap);
+  const int lch = 3 * b.s - 3;  // log2(chunks per cell)
+  const long long items = (long long)n << lch;
+  const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(it >> lch), ch = (int)(it & ((1ll << lch) - 1));
+    int x, y, z, tile;
+    band_cell(r, r.band[k], x, y, z, tile);
+    const int zg = G.z0 + z;
+    int cnt = 0;
+    if (b.kind == 0) {
+      for (int j = 0; j < 8; ++j) cnt += sample_inside(b, x, y, zg, ch * 8 + j, L, G.wall);
+    } else {
+      long long wi[8];
+      int bit[8];
+      mesh_word_index8(b, x, y, zg, ch * 8, L, G.wall, wi, bit);
+      unsigned long long w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j] = (wi[j] >= 0) ? __ldg(b.bits + wi[j]) : 0ull;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cnt += (int)((w[j] >> bit[j]) & 1ull);
+    }
+    if (cnt) atomicAdd(r.bandcnt + k, cnt);
+  }
+}
+
+__global__ void k_remap_l4(const __grid_constant__ RemapParams r) {
+  const int n = min(r.counters[2], r.band_cap);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    int x, y, z, tile;
+    band_cell(r, r.band[k], x, y, z, tile);
+    const int cnt = r.bandcnt[k];
     put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
   }
 }
@@ -201,7 +249,12 @@ cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cud
   k_remap_l0<<<(ntile + 255) / 256, 256, 0, st>>>(r);
   k_remap_l1<<<persistent_blocks, 256, 0, st>>>(r);
   k_remap_l2<<<persistent_blocks, 256, 0, st>>>(r);
-  k_remap_l3<<<persistent_blocks, 256, 0, st>>>(r);
+  if (r.body.s >= 2 && r.body.mapping == 0) {
+    k_remap_l3_chunks<<<persistent_blocks, 256, 0, st>>>(r);
+    k_remap_l4<<<persistent_blocks, 256, 0, st>>>(r);
+  } else {
+    k_remap_l3<<<persistent_blocks, 256, 0, st>>>(r);
+  }
   return cudaGetLastError();
 }
 

@@ -95,6 +95,7 @@ struct psm_ctx {
   uint32_t* r_segs = nullptr;
   float4* r_segq = nullptr;
   uint32_t* r_band = nullptr;
+  int* r_bandcnt = nullptr;
   int seg_cap = 0, band_cap = 0;
   double* pinned = nullptr;  // host staging (ft + err)
   // test-only dense fields
@@ -309,7 +310,7 @@ static cudaError_t record(psm_ctx* c, int phase, int which) {
 struct Plan {
   size_t off_A0, off_A1, off_word, off_flag, off_partial, off_overflow, off_err, off_scratch,
       off_ftout, off_ids, off_stage, stage_bytes, total;
-  size_t off_rcnt, off_rtiles, off_rsegs, off_rsegq, off_rband;
+  size_t off_rcnt, off_rtiles, off_rsegs, off_rsegq, off_rband, off_rbandcnt;
   int seg_cap, band_cap;
 };
 
@@ -342,6 +343,7 @@ static Plan make_plan(const psm_ctx* c) {
   p.off_rsegs = take((size_t)p.seg_cap * 4);
   p.off_rsegq = take((size_t)p.seg_cap * 16);
   p.off_rband = take((size_t)p.band_cap * 4);
+  p.off_rbandcnt = take((size_t)p.band_cap * 4);
   const size_t plane = (size_t)c->grid.nx * c->grid.ny * 8;
   const size_t per = plane * (size_t)c->Q;
   size_t planes = std::max<size_t>(3, kStageBudget / per);
@@ -384,6 +386,7 @@ static psm_status bind(psm_ctx* c, void* mem, size_t bytes) {
   c->r_segs = reinterpret_cast<uint32_t*>(m + p.off_rsegs);
   c->r_segq = reinterpret_cast<float4*>(m + p.off_rsegq);
   c->r_band = reinterpret_cast<uint32_t*>(m + p.off_rband);
+  c->r_bandcnt = reinterpret_cast<int*>(m + p.off_rbandcnt);
   c->seg_cap = p.seg_cap;
   c->band_cap = p.band_cap;
   c->stage_bytes = p.stage_bytes;
@@ -639,6 +642,7 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
       r.segs = c->r_segs;
       r.segq = c->r_segq;
       r.band = c->r_band;
+      r.bandcnt = c->r_bandcnt;
       r.seg_cap = c->seg_cap;
       r.band_cap = c->band_cap;
       CUDA_TRY(c, launch_remap_single(r, 148 * 8, c->st));

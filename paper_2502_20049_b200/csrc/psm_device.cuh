@@ -147,6 +147,7 @@ struct RemapParams {
   uint32_t* segs;       // listed segments: tile << 5 | segment
   float4* segq;         // body-frame segment centres
   uint32_t* band;       // narrow-band cells: tile << 8 | cell-in-tile
+  int* bandcnt;         // their inside counts (s >= 2 chunked path)
   int seg_cap, band_cap;
 };
 

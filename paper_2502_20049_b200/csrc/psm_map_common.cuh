@@ -212,4 +212,62 @@ __device__ __forceinline__ int exact_count(const BodyGeo& b, int x, int y, int z
   return cnt;
 }
 
+// Word index / bit of 8 consecutive sub-samples (si0 .. si0+7, same cell, si0 % 8 == 0) of a mesh
+// body.  Sample si0 is transformed with the exact A14 arithmetic; the others by adding the
+// rotated sub-sample offsets (error ~1e-13 cells).  A sample whose scaled coordinate lies within
+// 1e-9 of a geometry-cell face is recomputed exactly, so every floor() equals the exact one and the
+// result is bit-identical to mesh_word_index() per sample.
+__device__ __forceinline__ void mesh_word_index8(const BodyGeo& b, int x, int y, int zg, int si0,
+                                                 const double L[3], const int wall[3],
+                                                 long long wi[8], int bit[8]) {
+  const int n = 1 << b.s, msk = n - 1;
+  const double h = ldexp(1.0, -b.s), hs = ldexp(1.0, b.s);
+  const int gx0 = si0 & msk, gy0 = (si0 >> b.s) & msk, gz0 = si0 >> (2 * b.s);
+  const double p0[3] = {(double)x + (gx0 + 0.5) * h, (double)y + (gy0 + 0.5) * h,
+                        (double)zg + (gz0 + 0.5) * h};
+  double q0[3];
+  body_frame(b, p0, L, wall, q0);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int si = si0 + j;
+    const int gx = si & msk, gy = (si >> b.s) & msk, gz = si >> (2 * b.s);
+    const double dx = (gx - gx0) * h, dy = (gy - gy0) * h, dz = (gz - gz0) * h;
+    double f[3];
+    bool safe = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double qa = q0[a] + (b.Q[a] * dx + b.Q[3 + a] * dy + b.Q[6 + a] * dz);
+      f[a] = (qa - b.o[a]) * hs;
+      const double fr = f[a] - floor(f[a]);
+      if (fr < 1e-9 || fr > 1.0 - 1e-9) safe = false;
+    }
+    if (!safe) {
+      long long w;
+      int bp;
+      mesh_word_index(b, x, y, zg, si, L, wall, w, bp);
+      wi[j] = w;
+      bit[j] = bp;
+      continue;
+    }
+    int g[3];
+    bool in = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double xx = floor(f[a]);
+      if (!(xx >= 0.0) || xx >= (double)(b.dims_b[a] << b.s)) in = false;
+      g[a] = (int)xx;
+    }
+    if (!in) {
+      wi[j] = -1;
+      bit[j] = 0;
+      continue;
+    }
+    const long long brick =
+        ((long long)(g[2] >> b.s) * b.dims_b[1] + (g[1] >> b.s)) * b.dims_b[0] + (g[0] >> b.s);
+    const int bb = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
+    wi[j] = brick * b.words + (bb >> 6);
+    bit[j] = bb & 63;
+  }
+}
+
 }  // namespace psm
