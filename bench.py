@@ -58,6 +58,15 @@ WORKLOADS = {
     "c4f64": dict(nx=512, ny=512, nz=512, Q=19, prec="f64", tau=0.6, r=64.0, s=1,
                   v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
                   desc="c4 fp64: D3Q19 PSM fp64 512^3, moving sphere r=64, s=1"),
+    # the paper's performance operator (cumulant) on D3Q27 with the c3-shaped geometry
+    "c3cum": dict(nx=256, ny=256, nz=256, Q=27, prec="f64", tau=0.6, r=48.0, s=1,
+                  v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
+                  collision="cumulant",
+                  desc="c3-shaped, cumulant: D3Q27 PSM fp64 256^3, moving sphere r=48, s=1"),
+    "c5wcum": dict(nx=512, ny=512, nz=512, Q=27, prec="f32", tau=0.55, rotors=True, s=1,
+                   omega=0.05 / 220.0, pattern="two_array", sc=1, bmode=1, collision="cumulant",
+                   desc="c5 weak, cumulant: D3Q27 PSM fp32, 512^3 per GPU, CROR-like rotor pair "
+                        "per GPU, s=1, SC1, weighted B"),
     "c3f64": dict(nx=256, ny=256, nz=256, Q=27, prec="f64", tau=0.6, r=48.0, s=1,
                   v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
                   desc="c3-shaped: D3Q27 PSM fp64 256^3, moving sphere r=48, s=1"),
@@ -222,7 +231,7 @@ def build_workload(psm, wl: dict, rank: int, world: int, nccl_id=None):
     S = 8 if wl["prec"] == "f64" else 4
     sim = psm.Simulation(nx, ny, nzg, Q=wl["Q"], tau=wl["tau"], bc=(0, 0, 0), prec=wl["prec"],
                          pattern=wl["pattern"], sc=wl["sc"], bmode=wl["bmode"], rank=rank,
-                         world=world, nccl_id=nccl_id)
+                         world=world, nccl_id=nccl_id, collision=wl.get("collision", "srt"))
     sim.init_equilibrium(None, None)
     nbodies = 0
     body_poses = []  # (Q0, t0, v, w) per body, in id order

@@ -46,6 +46,7 @@ def lib():
             "orc_collide_cell": (I, [I, P, D, I, D, P, P, P, P]),
             "orc_collide_cell_trt": (I, [I, P, D, D, I, D, P, P, P, P]),
             "orc_set_collision": (None, [P, I, D]),
+            "orc_collide_cell_cum": (I, [I, P, D, I, D, P, P, P]),
             "orc_pose_advance": (None, [P, P, P, P, I64, P, P, P, P]),
             "orc_geometry_extent": (I64, [P, I64, I, P, P]),
             "orc_voxelize": (None, [P, I64, P, I64, I, P]),
@@ -136,6 +137,17 @@ def collide_cell_trt(Q, f, tau, magic, sc, B, us, g=(0.0, 0.0, 0.0)):
     return out, m, err
 
 
+def collide_cell_cum(Q, f, tau, sc, B, us):
+    """One-cell Eq.(4) collision with the cumulant fluid operator (D3Q27)."""
+    f = _f64(f)
+    us = _f64(us)
+    out = np.zeros(Q, np.float64)
+    m = np.zeros(3, np.float64)
+    err = lib().orc_collide_cell_cum(Q, _p(f), float(tau), int(sc), float(B), _p(us), _p(out),
+                                     _p(m))
+    return out, m, err
+
+
 def pose_advance(Q0, t0, v, w, n, L, periodic):
     """Closed-form prescribed pose after n steps (A13)."""
     Qn = np.zeros(9)
@@ -186,7 +198,7 @@ class Oracle:
         lib().orc_set_force(self._h, _p(g))
 
     def set_collision(self, kind: str = "srt", magic: float = 3.0 / 16.0):
-        lib().orc_set_collision(self._h, 1 if kind == "trt" else 0, float(magic))
+        lib().orc_set_collision(self._h, {"srt": 0, "trt": 1, "cumulant": 2}[kind], float(magic))
 
     def set_map_all_cells(self, on: bool):
         lib().orc_set_map_all_cells(self._h, int(bool(on)))

@@ -133,7 +133,8 @@ double orc_weight_fraction(double eps, double tau, int mode) {
  * m = B sum_i Omega^S_i c_i (the summand of Eq.(10)).  g is the test-only Guo body force (A-P12):
  * u = (j + g/2)/rho and Omega^F gains (1 - 1/(2 tau)) w_i [(c_i - u)/c_s^2 + (c_i.u) c_i/c_s^4].g.
  * Returns 0, or 1 if rho <= 0 or a value is non-finite (error rule of S:66/S:93). */
-/* Fluid operator kind: 0 = SRT, Eq.(2); 1 = TRT (two relaxation times, listed by the paper
+/* Fluid operator kind: 0 = SRT, Eq.(2); 2 = cumulant (D3Q27, see below); 1 = TRT (two relaxation
+ * times, listed by the paper
  * among lbmpy's operators; standard definition: with f^+-_i = (f_i +- f_ibar)/2,
  * Omega_i = -(1/tau)(f^+_i - f^eq+_i) - (1/tau_-)(f^-_i - f^eq-_i), tau_- = 1/2 + magic/(tau - 1/2);
  * the Guo source splits the same way with (1 - 1/(2 tau)) and (1 - 1/(2 tau_-))). */
@@ -149,6 +150,12 @@ int orc_collide_cell(int Q, const double* f, double tau, int sc, double B, const
 int orc_collide_cell_trt(int Q, const double* f, double tau, double magic, int sc, double B,
                          const double us[3], const double g[3], double* fstar, double m[3]) {
   return collide_cell_impl(Q, f, tau, sc, B, us, g, 1, magic, fstar, m);
+}
+
+int orc_collide_cell_cum(int Q, const double* f, double tau, int sc, double B, const double us[3],
+                         double* fstar, double m[3]) {
+  const double g[3] = {0.0, 0.0, 0.0};
+  return collide_cell_impl(Q, f, tau, sc, B, us, g, 2, 0.0, fstar, m);
 }
 
 static int collide_cell_impl(int Q, const double* f, double tau, int sc, double B,
@@ -183,7 +190,79 @@ static int collide_cell_impl(int Q, const double* f, double tau, int sc, double 
     src[i] = stencil_w(Q, i) * s;
   }
   const int forced = (g[0] != 0.0 || g[1] != 0.0 || g[2] != 0.0);
-  if (coll == 0) {
+  if (coll == 2) {
+    /* Cumulant collision (the operator of the paper's performance runs),
+     * D3Q27, with every relaxation rate of order >= 3 equal to 1 (those cumulants are set to their
+     * equilibrium 0), the bulk rate 1 and the shear rate 1/tau.  Plain form: second central
+     * moments by brute force; normalised cumulants C = kappa/rho relaxed; post-collision central
+     * moments of a distribution whose cumulants of order >= 3 vanish (Wick products of the C's);
+     * populations recovered by solving the 27x27 central-moment system. */
+    double k2[3][3] = {{0}};
+    for (int i = 0; i < Q; ++i) {
+      int c[3];
+      stencil_c(Q, i, c);
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) k2[a][b] += f[i] * (c[a] - u[a]) * (c[b] - u[b]);
+    }
+    double C[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) C[a][b] = k2[a][b] / rho;
+    const double w1 = 1.0 / tau, wb = 1.0;
+    double Cs = C[0][0] + C[1][1] + C[2][2];
+    double D1 = C[0][0] - C[1][1], D2 = C[0][0] - C[2][2];
+    Cs = Cs + wb * (1.0 - Cs); /* trace equilibrium 3 c_s^2 = 1 */
+    D1 = (1.0 - w1) * D1;
+    D2 = (1.0 - w1) * D2;
+    double Cxy = (1.0 - w1) * C[0][1], Cxz = (1.0 - w1) * C[0][2], Cyz = (1.0 - w1) * C[1][2];
+    double Cxx = (Cs + D1 + D2) / 3.0, Cyy = (Cs - 2.0 * D1 + D2) / 3.0,
+           Czz = (Cs + D1 - 2.0 * D2) / 3.0;
+    /* post-collision central moments kstar[a][b][c] (orders a, b, c in x, y, z) */
+    double ks[3][3][3];
+    memset(ks, 0, sizeof(ks));
+    ks[0][0][0] = rho;
+    ks[2][0][0] = rho * Cxx;
+    ks[0][2][0] = rho * Cyy;
+    ks[0][0][2] = rho * Czz;
+    ks[1][1][0] = rho * Cxy;
+    ks[1][0][1] = rho * Cxz;
+    ks[0][1][1] = rho * Cyz;
+    ks[2][2][0] = rho * (Cxx * Cyy + 2.0 * Cxy * Cxy);
+    ks[2][0][2] = rho * (Cxx * Czz + 2.0 * Cxz * Cxz);
+    ks[0][2][2] = rho * (Cyy * Czz + 2.0 * Cyz * Cyz);
+    ks[2][1][1] = rho * (Cxx * Cyz + 2.0 * Cxy * Cxz);
+    ks[1][2][1] = rho * (Cyy * Cxz + 2.0 * Cxy * Cyz);
+    ks[1][1][2] = rho * (Czz * Cxy + 2.0 * Cxz * Cyz);
+    ks[2][2][2] = rho * (Cxx * Cyy * Czz + 2.0 * (Cxx * Cyz * Cyz + Cyy * Cxz * Cxz +
+                                                  Czz * Cxy * Cxy) + 8.0 * Cxy * Cxz * Cyz);
+    /* solve sum_i (c_ix - ux)^a (c_iy - uy)^b (c_iz - uz)^c fc_i = ks[a][b][c] */
+    double M[27][28];
+    for (int r = 0; r < 27; ++r) {
+      int a = r % 3, b = (r / 3) % 3, cc = r / 9;
+      for (int i = 0; i < 27; ++i) {
+        int c[3];
+        stencil_c(Q, i, c);
+        M[r][i] = pow(c[0] - u[0], a) * pow(c[1] - u[1], b) * pow(c[2] - u[2], cc);
+      }
+      M[r][27] = ks[a][b][cc];
+    }
+    for (int col = 0; col < 27; ++col) { /* Gaussian elimination, partial pivoting */
+      int piv = col;
+      for (int r = col + 1; r < 27; ++r)
+        if (fabs(M[r][col]) > fabs(M[piv][col])) piv = r;
+      if (piv != col)
+        for (int k = 0; k < 28; ++k) {
+          double t = M[col][k];
+          M[col][k] = M[piv][k];
+          M[piv][k] = t;
+        }
+      for (int r = 0; r < 27; ++r) {
+        if (r == col) continue;
+        double fac = M[r][col] / M[col][col];
+        for (int k = col; k < 28; ++k) M[r][k] -= fac * M[col][k];
+      }
+    }
+    for (int i = 0; i < 27; ++i) omF[i] = M[i][27] / M[i][i] - f[i];
+  } else if (coll == 0) {
     /* Eq.(2): Omega^F_i = -(1/tau)(f_i - f_i^eq) */
     for (int i = 0; i < Q; ++i) {
       omF[i] = -(f[i] - feq[i]) / tau;

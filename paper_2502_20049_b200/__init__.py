@@ -29,7 +29,7 @@ PSM_F64, PSM_F32 = 0, 1
 PSM_TWO_ARRAY, PSM_AA = 0, 1
 PSM_PERIODIC, PSM_WALL = 0, 1
 PSM_SPHERE, PSM_MESH = 0, 1
-PSM_SRT, PSM_TRT = 0, 1
+PSM_SRT, PSM_TRT, PSM_CUMULANT = 0, 1, 2
 PSM_MAP_R1, PSM_MAP_R2 = 0, 1
 PSM_MAX_BODIES = 16
 PSM_NUM_PHASES = 4
@@ -303,7 +303,8 @@ class Simulation:
                         (C.c_double * 3)(*body_force), rank, world,
                         C.cast(self._idbuf, C.c_void_p) if self._idbuf is not None else None,
                         C.c_void_p(self._stream.cuda_stream),
-                        PSM_TRT if collision == "trt" else PSM_SRT, float(trt_magic))
+                        {"srt": PSM_SRT, "trt": PSM_TRT, "cumulant": PSM_CUMULANT}[collision],
+                        float(trt_magic))
         self.ctx = psm_create(g, Q, tau, o)
         nbytes = psm_required_bytes(self.ctx)
         self.mem = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)

@@ -202,6 +202,108 @@ __device__ __forceinline__ void fluid_update(T (&f)[Q], T rho, T ux, T uy, T uz,
   }
 }
 
+// D3Q27 stencil index of the velocity (cx, cy, cz)
+__host__ __device__ constexpr int idx27(int cx, int cy, int cz) {
+  for (int q = 0; q < 27; ++q)
+    if (stc_x(q) == cx && stc_y(q) == cy && stc_z(q) == cz) return q;
+  return -1;
+}
+
+// 1-D backward central-moment transform along one axis with velocity v: (k0, k1, k2) are the
+// central moments of orders 0, 1, 2 of the three populations c = -1, 0, +1.
+template <typename T>
+__device__ __forceinline__ void back1d(T k0, T k1, T k2, T v, T& fm, T& f0, T& fp) {
+  const T m1 = k1 + v * k0;                   // raw first moment  f+ - f-
+  const T m2 = k2 + v * (T(2) * k1 + v * k0);  // raw second moment f+ + f-
+  f0 = k0 - m2;
+  fp = T(0.5) * (m2 + m1);
+  fm = T(0.5) * (m2 - m1);
+}
+
+// Cumulant collision (the paper's performance operator), D3Q27, every rate of
+// order >= 3 and the bulk rate equal to 1, shear rate omega: normalised second cumulants
+// C = kappa / rho relaxed; post-collision central moments are those of a distribution whose
+// cumulants of order >= 3 vanish (Wick products); three 1-D backward transforms give f*.
+template <typename T>
+__device__ __forceinline__ void cumulant_update(T (&f)[27], T rho, T jx, T jy, T jz, T ux, T uy,
+                                                T uz, T om) {
+  T mxx = T(0), myy = T(0), mzz = T(0), mxy = T(0), mxz = T(0), myz = T(0);
+#pragma unroll
+  for (int q = 0; q < 27; ++q) {
+    const int cx = stc_x(q), cy = stc_y(q), cz = stc_z(q);
+    if (cx) mxx += f[q];
+    if (cy) myy += f[q];
+    if (cz) mzz += f[q];
+    if (cx * cy > 0) mxy += f[q]; else if (cx * cy < 0) mxy -= f[q];
+    if (cx * cz > 0) mxz += f[q]; else if (cx * cz < 0) mxz -= f[q];
+    if (cy * cz > 0) myz += f[q]; else if (cy * cz < 0) myz -= f[q];
+  }
+  const T ir = T(1) / rho;
+  const T Cxx0 = (mxx - ux * jx) * ir, Cyy0 = (myy - uy * jy) * ir, Czz0 = (mzz - uz * jz) * ir;
+  const T w1 = T(1) - om;
+  const T Cs = T(1);  // bulk rate 1: trace at its equilibrium 3 c_s^2
+  const T D1 = w1 * (Cxx0 - Cyy0), D2 = w1 * (Cxx0 - Czz0);
+  const T Cxy = w1 * (mxy - ux * jy) * ir, Cxz = w1 * (mxz - ux * jz) * ir,
+          Cyz = w1 * (myz - uy * jz) * ir;
+  const T Cxx = (Cs + D1 + D2) * T(1.0 / 3.0), Cyy = (Cs - T(2) * D1 + D2) * T(1.0 / 3.0),
+          Czz = (Cs + D1 - T(2) * D2) * T(1.0 / 3.0);
+  // post-collision central moments k[a][b][c] (orders a, b, c in x, y, z)
+  T k[3][3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) k[a][b][c] = T(0);
+  k[0][0][0] = rho;
+  k[2][0][0] = rho * Cxx;
+  k[0][2][0] = rho * Cyy;
+  k[0][0][2] = rho * Czz;
+  k[1][1][0] = rho * Cxy;
+  k[1][0][1] = rho * Cxz;
+  k[0][1][1] = rho * Cyz;
+  k[2][2][0] = rho * (Cxx * Cyy + T(2) * Cxy * Cxy);
+  k[2][0][2] = rho * (Cxx * Czz + T(2) * Cxz * Cxz);
+  k[0][2][2] = rho * (Cyy * Czz + T(2) * Cyz * Cyz);
+  k[2][1][1] = rho * (Cxx * Cyz + T(2) * Cxy * Cxz);
+  k[1][2][1] = rho * (Cyy * Cxz + T(2) * Cxy * Cyz);
+  k[1][1][2] = rho * (Czz * Cxy + T(2) * Cxz * Cyz);
+  k[2][2][2] = rho * (Cxx * Cyy * Czz +
+                      T(2) * (Cxx * Cyz * Cyz + Cyy * Cxz * Cxz + Czz * Cxy * Cxy) +
+                      T(8) * Cxy * Cxz * Cyz);
+  // backward transforms x, then y, then z (the 1-D transforms commute)
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      T fm, f0, fp;
+      back1d(k[0][b][c], k[1][b][c], k[2][b][c], ux, fm, f0, fp);
+      k[0][b][c] = fm;
+      k[1][b][c] = f0;
+      k[2][b][c] = fp;
+    }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      T fm, f0, fp;
+      back1d(k[a][0][c], k[a][1][c], k[a][2][c], uy, fm, f0, fp);
+      k[a][0][c] = fm;
+      k[a][1][c] = f0;
+      k[a][2][c] = fp;
+    }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      T fm, f0, fp;
+      back1d(k[a][b][0], k[a][b][1], k[a][b][2], uz, fm, f0, fp);
+      f[idx27(a - 1, b - 1, -1)] = fm;
+      f[idx27(a - 1, b - 1, 0)] = f0;
+      f[idx27(a - 1, b - 1, 1)] = fp;
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ T ld_stream(const T* p) {
   return __ldg(p);
@@ -209,14 +311,16 @@ __device__ __forceinline__ T ld_stream(const T* p) {
 
 // Minimum resident 256-thread blocks per SM (= register budget 65536 / (256 * n)): enough warps
 // in flight to cover HBM latency without spilling the populations.
-template <int Q, typename T, int PAT>
+template <int Q, typename T, int PAT, int COLL>
 constexpr int collide_min_blocks() {
+  // the cumulant keeps a 3x3x3 moment array live: fewer, fatter threads
+  if (COLL == 2) return sizeof(T) == 8 ? 1 : 2;
   // the AA odd step keeps the scatter offsets live as well: one block less for fp32
   return sizeof(T) == 8 ? 2 : (Q == 19 ? (PAT == 2 ? 3 : 4) : (PAT == 2 ? 2 : 3));
 }
 
-template <int Q, typename T, int PAT, bool WALLS, bool FORCE, bool DBG, bool TRT>
-__global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT>()))
+template <int Q, typename T, int PAT, bool WALLS, bool FORCE, bool DBG, int COLL>
+__global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COLL>()))
     k_collide(const __grid_constant__ CollideParams p) {
   const Geom& G = p.g;
   const int x = blockIdx.x * kTileX + threadIdx.x;
@@ -307,7 +411,8 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT>()))
   const T gpref = T(1) - T(0.5) * om, gmref = T(1) - T(0.5) * omm;
 
   if (!solid_tile) {
-    if (TRT) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
+    if constexpr (COLL == 2 && Q == 27) cumulant_update<T>(f, rho, jx, jy, jz, ux, uy, uz, om);
+    else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
     else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
   } else {
     // ---- PSM cell: B, u_s from the solid word (or the test-only dense fields) ----
@@ -352,6 +457,12 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT>()))
       const T sux = T(usd[0]), suy = T(usd[1]), suz = T(usd[2]);
       const T susq15 = T(1.5) * (sux * sux + suy * suy + suz * suz);
       T msx = T(0), msy = T(0), msz = T(0);
+      T fc[Q];  // cumulant post-collision state (COLL == 2 only)
+      if constexpr (COLL == 2 && Q == 27) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) fc[q] = f[q];
+        cumulant_update<T>(fc, rho, jx, jy, jz, ux, uy, uz, om);
+      }
 #pragma unroll
       for (int i = 0; i < Q; ++i) {
         const int j = stc_opp(i);
@@ -363,7 +474,10 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT>()))
         const T sj = feq_q<Q, T>(j, rho, sux, suy, suz, susq15);
         // fluid operator on the pair: SRT, or TRT on the symmetric/antisymmetric parts
         T oFi, oFj;
-        if (TRT) {
+        if constexpr (COLL == 2 && Q == 27) {
+          oFi = fc[i] - fi;
+          oFj = fc[j] - fj;
+        } else if (COLL == 1) {
           const T Pp = om * (T(0.5) * (ei + ej) - T(0.5) * (fi + fj));
           const T Mm = omm * (T(0.5) * (ei - ej) - T(0.5) * (fi - fj));
           oFi = Pp + Mm;
@@ -402,7 +516,8 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT>()))
       m[1] = Bd * (double)msy;
       m[2] = Bd * (double)msz;
     } else {
-      if (TRT) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
+      if constexpr (COLL == 2 && Q == 27) cumulant_update<T>(f, rho, jx, jy, jz, ux, uy, uz, om);
+      else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
       else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
     }
     // ---- per-body F/T partial of this tile (deterministic block reduction) ----
@@ -444,33 +559,47 @@ static cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool db
   if (ntz <= 0) return cudaSuccess;
   dim3 grid(p.g.gx, p.g.gy, ntz), block(kTileX, kTileY, kTileZ);
   const bool walls = p.g.wall[0] || p.g.wall[1] || p.g.wall[2];
-  if (p.trt) {
+  if (p.trt == 1) {
     // TRT: the general (runtime wall flags) variants only
     if (dbg || force) {
-      if (dbg && force) k_collide<Q, T, 0, true, true, true, true><<<grid, block, 0, st>>>(p);
-      else if (dbg) k_collide<Q, T, 0, true, false, true, true><<<grid, block, 0, st>>>(p);
-      else k_collide<Q, T, 0, true, true, false, true><<<grid, block, 0, st>>>(p);
+      if (dbg && force) k_collide<Q, T, 0, true, true, true, 1><<<grid, block, 0, st>>>(p);
+      else if (dbg) k_collide<Q, T, 0, true, false, true, 1><<<grid, block, 0, st>>>(p);
+      else k_collide<Q, T, 0, true, true, false, 1><<<grid, block, 0, st>>>(p);
     } else if (pat == 0) {
-      k_collide<Q, T, 0, true, false, false, true><<<grid, block, 0, st>>>(p);
+      k_collide<Q, T, 0, true, false, false, 1><<<grid, block, 0, st>>>(p);
     } else if (pat == 1) {
-      k_collide<Q, T, 1, false, false, false, true><<<grid, block, 0, st>>>(p);
+      k_collide<Q, T, 1, false, false, false, 1><<<grid, block, 0, st>>>(p);
     } else {
-      k_collide<Q, T, 2, true, false, false, true><<<grid, block, 0, st>>>(p);
+      k_collide<Q, T, 2, true, false, false, 1><<<grid, block, 0, st>>>(p);
     }
     return cudaGetLastError();
   }
+  if (p.trt == 2) {
+    // cumulant (D3Q27 only; no forcing): periodic fast path and the general variants
+    if constexpr (Q == 27) {
+      if (force) return cudaErrorInvalidValue;
+      if (dbg) k_collide<Q, T, 0, true, false, true, 2><<<grid, block, 0, st>>>(p);
+      else if (pat == 0 && !walls) k_collide<Q, T, 0, false, false, false, 2><<<grid, block, 0, st>>>(p);
+      else if (pat == 0) k_collide<Q, T, 0, true, false, false, 2><<<grid, block, 0, st>>>(p);
+      else if (pat == 1) k_collide<Q, T, 1, false, false, false, 2><<<grid, block, 0, st>>>(p);
+      else k_collide<Q, T, 2, true, false, false, 2><<<grid, block, 0, st>>>(p);
+      return cudaGetLastError();
+    } else {
+      return cudaErrorInvalidValue;
+    }
+  }
   if (dbg || force) {
-    if (dbg && force) k_collide<Q, T, 0, true, true, true, false><<<grid, block, 0, st>>>(p);
-    else if (dbg) k_collide<Q, T, 0, true, false, true, false><<<grid, block, 0, st>>>(p);
-    else k_collide<Q, T, 0, true, true, false, false><<<grid, block, 0, st>>>(p);
+    if (dbg && force) k_collide<Q, T, 0, true, true, true, 0><<<grid, block, 0, st>>>(p);
+    else if (dbg) k_collide<Q, T, 0, true, false, true, 0><<<grid, block, 0, st>>>(p);
+    else k_collide<Q, T, 0, true, true, false, 0><<<grid, block, 0, st>>>(p);
   } else if (pat == 0) {
-    if (walls) k_collide<Q, T, 0, true, false, false, false><<<grid, block, 0, st>>>(p);
-    else k_collide<Q, T, 0, false, false, false, false><<<grid, block, 0, st>>>(p);
+    if (walls) k_collide<Q, T, 0, true, false, false, 0><<<grid, block, 0, st>>>(p);
+    else k_collide<Q, T, 0, false, false, false, 0><<<grid, block, 0, st>>>(p);
   } else if (pat == 1) {
-    k_collide<Q, T, 1, false, false, false, false><<<grid, block, 0, st>>>(p);
+    k_collide<Q, T, 1, false, false, false, 0><<<grid, block, 0, st>>>(p);
   } else {
-    if (walls) k_collide<Q, T, 2, true, false, false, false><<<grid, block, 0, st>>>(p);
-    else k_collide<Q, T, 2, false, false, false, false><<<grid, block, 0, st>>>(p);
+    if (walls) k_collide<Q, T, 2, true, false, false, 0><<<grid, block, 0, st>>>(p);
+    else k_collide<Q, T, 2, false, false, false, 0><<<grid, block, 0, st>>>(p);
   }
   return cudaGetLastError();
 }

@@ -881,7 +881,7 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   if ((opt->prec != PSM_F64 && opt->prec != PSM_F32) ||
       (opt->pattern != PSM_TWO_ARRAY && opt->pattern != PSM_AA) || opt->sc < 1 || opt->sc > 3 ||
       (opt->bmode != PSM_B_DIRECT && opt->bmode != PSM_B_WEIGHTED) ||
-      (opt->collision != PSM_SRT && opt->collision != PSM_TRT))
+      (opt->collision != PSM_SRT && opt->collision != PSM_TRT && opt->collision != PSM_CUMULANT))
     FAIL((psm_ctx*)nullptr, PSM_E_ARG, "bad option enum");
   if (opt->collision == PSM_TRT && !(opt->trt_magic > 0.0 && std::isfinite(opt->trt_magic)))
     FAIL((psm_ctx*)nullptr, PSM_E_ARG, "TRT magic parameter must be finite and > 0");
@@ -894,6 +894,8 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
     FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "body force needs PSM_TWO_ARRAY");
   if (world > 1 && opt->pattern == PSM_AA)
     FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "multi-rank runs need PSM_TWO_ARRAY");
+  if (opt->collision == PSM_CUMULANT && (stencil != PSM_D3Q27 || force))
+    FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "the cumulant operator needs D3Q27 and no body force");
   if (world > 1 && !opt->nccl_unique_id)
     FAIL((psm_ctx*)nullptr, PSM_E_ARG, "world > 1 needs an ncclUniqueId");
   psm_ctx* c = new (std::nothrow) psm_ctx();
@@ -1265,7 +1267,7 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
   p.omega_m = (c->opt.collision == PSM_TRT)
                   ? 1.0 / (0.5 + c->opt.trt_magic / (c->tau - 0.5))
                   : p.omega;
-  p.trt = c->opt.collision == PSM_TRT ? 1 : 0;
+  p.trt = c->opt.collision == PSM_TRT ? 1 : (c->opt.collision == PSM_CUMULANT ? 2 : 0);
   for (int a = 0; a < 3; ++a) p.gforce[a] = c->opt.body_force[a];
   p.sc = c->opt.sc;
   p.bmode = c->opt.bmode;

@@ -106,7 +106,7 @@ struct CollideParams {
   const uint8_t* dbg_id;  // DBG: id [cell]
   double tau, omega;      // omega = 1/tau (symmetric rate w+)
   double omega_m;         // antisymmetric rate w- (TRT; == omega for SRT)
-  int trt;                // fluid operator: 0 SRT (Eq.(2)), 1 TRT
+  int trt;                // fluid operator: 0 SRT (Eq.(2)), 1 TRT, 2 cumulant (D3Q27)
   double gforce[3];       // test-only Guo force
   int sc;                 // 1, 2, 3
   int bmode;              // 0 direct, 1 weighted

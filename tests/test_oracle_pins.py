@@ -308,3 +308,41 @@ def test_trt_poiseuille_is_exact_at_magic_3_16():
     yc = np.arange(H) + 0.5
     ref = g * yc * (H - yc) / (2 * (tau - 0.5) / 3)
     assert np.max(np.abs(ux - ref)) / ref.max() < 1e-9
+
+
+# ------------------------------------------------- cumulant (NEXT rank 2) ---
+def test_cumulant_conservation_idempotence_and_fixed_point():
+    Q = 27
+    c, w, _ = oracle.stencil(Q)
+    cf = c.astype(float)
+    f = pi.random_pdfs(Q, (1,), 63, w=w, amp=0.2)[:, 0]
+    out, _, err = oracle.collide_cell_cum(Q, f, 0.7, 1, 0.0, [0, 0, 0])
+    assert err == 0
+    assert abs(out.sum() - f.sum()) < 1e-15 * 4
+    assert np.allclose(out @ cf, f @ cf, atol=2e-16 * 8, rtol=0)
+    # full relaxation (tau = 1) is idempotent, and its result is a fixed point for any tau
+    e1, _, _ = oracle.collide_cell_cum(Q, f, 1.0, 1, 0.0, [0, 0, 0])
+    e2, _, _ = oracle.collide_cell_cum(Q, e1, 1.0, 1, 0.0, [0, 0, 0])
+    e3, _, _ = oracle.collide_cell_cum(Q, e1, 0.63, 1, 0.0, [0, 0, 0])
+    assert np.allclose(e2, e1, atol=1e-15, rtol=0) and np.allclose(e3, e1, atol=1e-15, rtol=0)
+    # at rest with rho = 1 the cumulant equilibrium is the lattice weights
+    r, _, _ = oracle.collide_cell_cum(Q, w * 1.0, 0.9, 1, 0.0, [0, 0, 0])
+    assert np.allclose(r, w, atol=1e-16, rtol=0)
+
+
+@pytest.mark.parametrize("U0", [0.0, 0.1])
+def test_cumulant_shear_wave_viscosity_and_galilean_invariance(U0):
+    """Decay rate nu k^2 with nu = (tau - 1/2)/3, also for a wave advected at U0 = 0.1."""
+    L, U, tau, steps = 64, 1e-3, 0.8, 1000
+    o = oracle.Oracle(1, L, 1, 27, tau, (0, 0, 0), 1, 1)
+    o.set_collision("cumulant")
+    yc = np.arange(L) + 0.5
+    u = np.zeros((3, 1, L, 1))
+    u[0, 0, :, 0] = U0 + U * np.sin(2 * np.pi * yc / L)
+    o.init_equilibrium(np.ones((1, L, 1)), u)
+    o.step(steps)
+    _, uu = o.velocity()
+    amp = 2.0 / L * np.sum((uu[0, 0, :, 0] - U0) * np.sin(2 * np.pi * yc / L))
+    nu = (tau - 0.5) / 3.0
+    k = 2 * np.pi / L
+    assert abs(-math.log(amp / U) / steps / (nu * k * k) - 1.0) < 0.01
