@@ -313,8 +313,9 @@ __device__ __forceinline__ T ld_stream(const T* p) {
 // in flight to cover HBM latency without spilling the populations.
 template <int Q, typename T, int PAT, int COLL>
 constexpr int collide_min_blocks() {
-  // the cumulant keeps a 3x3x3 moment array live: fewer, fatter threads
-  if (COLL == 2) return sizeof(T) == 8 ? 1 : 2;
+  // the cumulant keeps a 3x3x3 moment array live (PSM cells stash f in shared memory instead of
+  // registers): two fp64 blocks (a few spilled words), three fp32 blocks (AA odd: two)
+  if (COLL == 2) return sizeof(T) == 8 ? 2 : (PAT == 2 ? 2 : 3);
   // the AA odd step keeps the scatter offsets live as well: one block less for fp32
   return sizeof(T) == 8 ? 2 : (Q == 19 ? (PAT == 2 ? 3 : 4) : (PAT == 2 ? 2 : 3));
 }
@@ -363,24 +364,24 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int b = 0; b < 3; ++b) RB[a][b] = self + OY[a] + OZ[b];
-  const long long qs = G.qstride;
 
   // ---- gather the pre-collision populations f_i(x) ----
   T f[Q];
   {
-    const T* A = static_cast<const T*>(p.src);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int cx = stc_x(q) + 1, cy = stc_y(q) + 1, cz = stc_z(q) + 1;
       const int src = RB[cy][cz] + OX[cx];
       const bool out = WALLS && (OUTX[cx] || OUTY[cy] || OUTZ[cz]);
+      const T* Aq = static_cast<const T*>(p.srcq[q]);
+      const T* Ao = static_cast<const T*>(p.srcq[stc_opp(q)]);
       if (PAT == 0) {
-        const T* ptr = out ? (A + stc_opp(q) * qs + self) : (A + q * qs + src);
+        const T* ptr = out ? (Ao + self) : (Aq + src);
         f[q] = ld_stream(ptr);
       } else if (PAT == 1) {
-        f[q] = A[q * qs + self];
+        f[q] = Aq[self];
       } else {
-        const T* ptr = out ? (A + q * qs + self) : (A + stc_opp(q) * qs + src);
+        const T* ptr = out ? (Aq + self) : (Ao + src);
         f[q] = *ptr;
       }
     }
@@ -452,22 +453,37 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
       }
     }
     double m[3] = {0.0, 0.0, 0.0};
+    // cumulant: every cell of the tile takes the fluid operator once, in place; a solid-covered
+    // cell first puts its pre-collision f into a shared-memory stash ([q][thread], conflict-free)
+    // so the PSM pair loop never holds both 27-vectors in registers (that peak would halve the
+    // occupancy of every tile)
+    T* stash = nullptr;
+    int tid = 0;
+    if constexpr (COLL == 2 && Q == 27) {
+      extern __shared__ __align__(16) unsigned char smem_raw[];
+      stash = reinterpret_cast<T*>(smem_raw);
+      tid = threadIdx.x + kTileX * (threadIdx.y + kTileY * threadIdx.z);
+      if (Bd > 0.0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) stash[q * kTileCells + tid] = f[q];
+      }
+      cumulant_update<T>(f, rho, jx, jy, jz, ux, uy, uz, om);
+    }
     if (Bd > 0.0) {
       const T B = T(Bd), B1 = T(1) - T(Bd);
       const T sux = T(usd[0]), suy = T(usd[1]), suz = T(usd[2]);
       const T susq15 = T(1.5) * (sux * sux + suy * suy + suz * suz);
       T msx = T(0), msy = T(0), msz = T(0);
-      T fc[Q];  // cumulant post-collision state (COLL == 2 only)
-      if constexpr (COLL == 2 && Q == 27) {
-#pragma unroll
-        for (int q = 0; q < Q; ++q) fc[q] = f[q];
-        cumulant_update<T>(fc, rho, jx, jy, jz, ux, uy, uz, om);
-      }
 #pragma unroll
       for (int i = 0; i < Q; ++i) {
         const int j = stc_opp(i);
         if (j < i) continue;  // each (i, ibar) pair once
-        const T fi = f[i], fj = f[j];
+        T fi = f[i], fj = f[j];
+        T fci = fi, fcj = fj;  // fluid post-collision state (cumulant only)
+        if constexpr (COLL == 2 && Q == 27) {
+          fi = stash[i * kTileCells + tid];
+          fj = stash[j * kTileCells + tid];
+        }
         const T ei = feq_q<Q, T>(i, rho, ux, uy, uz, usq15);
         const T ej = feq_q<Q, T>(j, rho, ux, uy, uz, usq15);
         const T si = feq_q<Q, T>(i, rho, sux, suy, suz, susq15);
@@ -475,8 +491,8 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
         // fluid operator on the pair: SRT, or TRT on the symmetric/antisymmetric parts
         T oFi, oFj;
         if constexpr (COLL == 2 && Q == 27) {
-          oFi = fc[i] - fi;
-          oFj = fc[j] - fj;
+          oFi = fci - fi;
+          oFj = fcj - fj;
         } else if (COLL == 1) {
           const T Pp = om * (T(0.5) * (ei + ej) - T(0.5) * (fi + fj));
           const T Mm = omm * (T(0.5) * (ei - ej) - T(0.5) * (fi - fj));
@@ -516,8 +532,9 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
       m[1] = Bd * (double)msy;
       m[2] = Bd * (double)msz;
     } else {
-      if constexpr (COLL == 2 && Q == 27) cumulant_update<T>(f, rho, jx, jy, jz, ux, uy, uz, om);
-      else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
+      if constexpr (COLL == 2 && Q == 27) {
+        // done above
+      } else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
       else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
     }
     // ---- per-body F/T partial of this tile (deterministic block reduction) ----
@@ -534,18 +551,19 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
 
   // ---- scatter ----
   if (act) {
-    T* Aout = static_cast<T*>(p.dst);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
+      T* Dq = static_cast<T*>(p.dstq[q]);
+      T* Do = static_cast<T*>(p.dstq[stc_opp(q)]);
       if (PAT == 0) {
-        __stcs(Aout + q * qs + self, f[q]);
+        __stcs(Dq + self, f[q]);
       } else if (PAT == 1) {
-        Aout[stc_opp(q) * qs + self] = f[q];
+        Do[self] = f[q];
       } else {
         // destination x + c_q == source position of the opposite direction
         const int cx = 1 - stc_x(q), cy = 1 - stc_y(q), cz = 1 - stc_z(q);
         const bool out = WALLS && (OUTX[cx] || OUTY[cy] || OUTZ[cz]);
-        T* ptr = out ? (Aout + stc_opp(q) * qs + self) : (Aout + q * qs + RB[cy][cz] + OX[cx]);
+        T* ptr = out ? (Do + self) : (Dq + (RB[cy][cz] + OX[cx]));
         *ptr = f[q];
       }
     }
@@ -554,10 +572,25 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
 
 // ------------------------------------------------------------------------------ launcher ---
 template <int Q, typename T>
+static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, bool dbg,
+                                  dim3 grid, dim3 block, cudaStream_t st);
+
+template <int Q, typename T>
 static cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool dbg, int ntz,
                             cudaStream_t st) {
   if (ntz <= 0) return cudaSuccess;
   dim3 grid(p.g.gx, p.g.gy, ntz), block(kTileX, kTileY, kTileZ);
+  CollideParams pq = p;
+  for (int q = 0; q < Q; ++q) {
+    pq.srcq[q] = static_cast<const T*>(p.src) + (size_t)q * p.g.qstride;
+    pq.dstq[q] = static_cast<T*>(p.dst) + (size_t)q * p.g.qstride;
+  }
+  return launch_variant<Q, T>(pq, pat, force, dbg, grid, block, st);
+}
+
+template <int Q, typename T>
+static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, bool dbg,
+                                  dim3 grid, dim3 block, cudaStream_t st) {
   const bool walls = p.g.wall[0] || p.g.wall[1] || p.g.wall[2];
   if (p.trt == 1) {
     // TRT: the general (runtime wall flags) variants only
@@ -578,11 +611,26 @@ static cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool db
     // cumulant (D3Q27 only; no forcing): periodic fast path and the general variants
     if constexpr (Q == 27) {
       if (force) return cudaErrorInvalidValue;
-      if (dbg) k_collide<Q, T, 0, true, false, true, 2><<<grid, block, 0, st>>>(p);
-      else if (pat == 0 && !walls) k_collide<Q, T, 0, false, false, false, 2><<<grid, block, 0, st>>>(p);
-      else if (pat == 0) k_collide<Q, T, 0, true, false, false, 2><<<grid, block, 0, st>>>(p);
-      else if (pat == 1) k_collide<Q, T, 1, false, false, false, 2><<<grid, block, 0, st>>>(p);
-      else k_collide<Q, T, 2, true, false, false, 2><<<grid, block, 0, st>>>(p);
+      const size_t sm = (size_t)Q * kTileCells * sizeof(T);  // PSM-cell stash
+      static bool attr = false;                             // once per instantiation
+      if (!attr) {
+        const void* fns[5] = {(const void*)k_collide<Q, T, 0, true, false, true, 2>,
+                              (const void*)k_collide<Q, T, 0, false, false, false, 2>,
+                              (const void*)k_collide<Q, T, 0, true, false, false, 2>,
+                              (const void*)k_collide<Q, T, 1, false, false, false, 2>,
+                              (const void*)k_collide<Q, T, 2, true, false, false, 2>};
+        for (const void* fn : fns) {
+          cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sm);
+          if (e != cudaSuccess) return e;
+        }
+        attr = true;
+      }
+      if (dbg) k_collide<Q, T, 0, true, false, true, 2><<<grid, block, sm, st>>>(p);
+      else if (pat == 0 && !walls) k_collide<Q, T, 0, false, false, false, 2><<<grid, block, sm, st>>>(p);
+      else if (pat == 0) k_collide<Q, T, 0, true, false, false, 2><<<grid, block, sm, st>>>(p);
+      else if (pat == 1) k_collide<Q, T, 1, false, false, false, 2><<<grid, block, sm, st>>>(p);
+      else k_collide<Q, T, 2, true, false, false, 2><<<grid, block, sm, st>>>(p);
       return cudaGetLastError();
     } else {
       return cudaErrorInvalidValue;

@@ -113,6 +113,11 @@ struct CollideParams {
   long long step;         // for the error word
   int tz0;                // first tile layer (z) of this launch: blockIdx.z + tz0
   BodyKin bodies[kMaxBodies + 1];
+  // per-direction plane bases src + q * qstride and dst + q * qstride (filled by the launcher):
+  // each access is then one 32-bit-offset LEA off a constant-bank pointer instead of a 64-bit
+  // q * qstride + offset product per load/store
+  const void* srcq[27];
+  void* dstq[27];
 };
 
 struct MapBox {
