@@ -53,6 +53,7 @@ def lib():
             "orc_create": (P, [I, I, I, I, D, P, I, I]),
             "orc_destroy": (None, [P]),
             "orc_set_force": (None, [P, P]),
+            "orc_set_open_boundary": (None, [P, P, D]),
             "orc_set_map_all_cells": (None, [P, I]),
             "orc_init_equilibrium": (None, [P, P, P]),
             "orc_set_pdfs": (None, [P, P]),
@@ -196,6 +197,12 @@ class Oracle:
     def set_force(self, g):
         g = _f64(g)
         lib().orc_set_force(self._h, _p(g))
+
+    def set_open_boundary(self, u_in=(0.0, 0.0, 0.0), rho_out: float = 1.0):
+        """bc[0] == 2: velocity inflow u_in at x = 0, pressure outflow rho_out at x = nx-1
+        (reading A30)."""
+        u = _f64(u_in)
+        lib().orc_set_open_boundary(self._h, _p(u), float(rho_out))
 
     def set_collision(self, kind: str = "srt", magic: float = 3.0 / 16.0):
         lib().orc_set_collision(self._h, {"srt": 0, "trt": 1, "cumulant": 2}[kind], float(magic))

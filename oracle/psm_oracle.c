@@ -455,7 +455,9 @@ typedef struct {
 typedef struct {
   int nx, ny, nz, Q;
   double tau;
-  int bc[3]; /* 0 periodic, 1 wall */
+  int bc[3]; /* 0 periodic, 1 wall, 2 (x only) velocity inflow at x = 0 / pressure outflow at
+                x = nx - 1 (reading A30) */
+  double u_in[3], rho_out; /* A30 inflow velocity and outflow density */
   int sc, bmode;
   double g[3];
   double *f, *fnew;
@@ -496,7 +498,15 @@ orc_sim* orc_create(int nx, int ny, int nz, int Q, double tau, const int bc[3], 
   S->id = (uint8_t*)calloc((size_t)N, 1);
   S->cnt = (int32_t*)calloc((size_t)N, sizeof(int32_t));
   S->err_cell = -1;
+  S->rho_out = 1.0;
   return S;
+}
+
+/* Reading A30 (P:584, P:593 name "boundary handling for inflow and outflow" without defining
+ * it): velocity inflow and pressure outflow on the x faces. */
+void orc_set_open_boundary(orc_sim* S, const double u_in[3], double rho_out) {
+  for (int a = 0; a < 3; ++a) S->u_in[a] = u_in[a];
+  S->rho_out = rho_out;
 }
 
 void orc_destroy(orc_sim* S) {
@@ -804,12 +814,47 @@ int orc_step(orc_sim* S) {
             pAT[z][id][a] += fabs(tq[a]);
           }
         }
+        /* post-collision velocity of this cell (used only by the A30 outflow) */
+        double ustar[3] = {0.0, 0.0, 0.0};
+        if (S->bc[0] == 2 && x == nx - 1) {
+          double rs = 0.0, js[3] = {0.0, 0.0, 0.0};
+          for (int i = 0; i < Q; ++i) {
+            int cc[3];
+            stencil_c(Q, i, cc);
+            rs += fs[i];
+            for (int a = 0; a < 3; ++a) js[a] += cc[a] * fs[i];
+          }
+          for (int a = 0; a < 3; ++a) ustar[a] = js[a] / rs;
+        }
         /* stream (push) */
         for (int i = 0; i < Q; ++i) {
           int cc[3];
           stencil_c(Q, i, cc);
           int xn[3] = {x + cc[0], y + cc[1], z + cc[2]};
           int n3[3] = {nx, ny, nz};
+          const int ib = TOPP[Q][i];
+          if (S->bc[0] == 2 && (xn[0] < 0 || xn[0] >= nx)) {
+            /* A30: the x faces take precedence over walls on the other axes (domain edges) */
+            int cb[3];
+            stencil_c(Q, ib, cb);
+            const double wb = stencil_w(Q, ib);
+            if (xn[0] < 0) {
+              /* velocity inflow, moving-wall bounce-back with rho_w = 1:
+               * f_ibar(x) = f*_i(x) + 2 w_ibar rho_w (c_ibar . u_in) / c_s^2 */
+              double cu = cb[0] * S->u_in[0] + cb[1] * S->u_in[1] + cb[2] * S->u_in[2];
+              S->fnew[(int64_t)ib * N + c] = fs[i] + 2.0 * wb * 1.0 * cu / CS2;
+            } else {
+              /* pressure outflow, anti-bounce-back with rho_out and the cell's post-collision
+               * velocity u*: f_ibar(x) = -f*_i(x) + 2 w_ibar rho_out [1 + (c_ibar.u*)^2/(2c_s^4)
+               *                                                   - u*^2/(2c_s^2)] */
+              double cu = cb[0] * ustar[0] + cb[1] * ustar[1] + cb[2] * ustar[2];
+              double uu = ustar[0] * ustar[0] + ustar[1] * ustar[1] + ustar[2] * ustar[2];
+              S->fnew[(int64_t)ib * N + c] =
+                  -fs[i] + 2.0 * wb * S->rho_out *
+                               (1.0 + (cu * cu) / (2.0 * CS2 * CS2) - uu / (2.0 * CS2));
+            }
+            continue;
+          }
           int wall = 0;
           for (int a = 0; a < 3; ++a) {
             if (xn[a] < 0 || xn[a] >= n3[a]) {
@@ -820,7 +865,7 @@ int orc_step(orc_sim* S) {
             }
           }
           if (wall)
-            S->fnew[(int64_t)TOPP[Q][i] * N + c] = fs[i];
+            S->fnew[(int64_t)ib * N + c] = fs[i];
           else
             S->fnew[(int64_t)i * N + cidx(S, xn[0], xn[1], xn[2])] = fs[i];
         }
