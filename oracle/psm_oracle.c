@@ -455,8 +455,8 @@ typedef struct {
 typedef struct {
   int nx, ny, nz, Q;
   double tau;
-  int bc[3]; /* 0 periodic, 1 wall, 2 (x only) velocity inflow at x = 0 / pressure outflow at
-                x = nx - 1 (reading A30) */
+  int bc[3]; /* 0 periodic, 1 wall, 2 (x only, nx >= 2) velocity inflow at x = 0 / pressure
+                outflow at x = nx - 1 (reading A30) */
   double u_in[3], rho_out; /* A30 inflow velocity and outflow density */
   int sc, bmode;
   double g[3];
@@ -814,18 +814,6 @@ int orc_step(orc_sim* S) {
             pAT[z][id][a] += fabs(tq[a]);
           }
         }
-        /* post-collision velocity of this cell (used only by the A30 outflow) */
-        double ustar[3] = {0.0, 0.0, 0.0};
-        if (S->bc[0] == 2 && x == nx - 1) {
-          double rs = 0.0, js[3] = {0.0, 0.0, 0.0};
-          for (int i = 0; i < Q; ++i) {
-            int cc[3];
-            stencil_c(Q, i, cc);
-            rs += fs[i];
-            for (int a = 0; a < 3; ++a) js[a] += cc[a] * fs[i];
-          }
-          for (int a = 0; a < 3; ++a) ustar[a] = js[a] / rs;
-        }
         /* stream (push) */
         for (int i = 0; i < Q; ++i) {
           int cc[3];
@@ -844,14 +832,9 @@ int orc_step(orc_sim* S) {
               double cu = cb[0] * S->u_in[0] + cb[1] * S->u_in[1] + cb[2] * S->u_in[2];
               S->fnew[(int64_t)ib * N + c] = fs[i] + 2.0 * wb * 1.0 * cu / CS2;
             } else {
-              /* pressure outflow, anti-bounce-back with rho_out and the cell's post-collision
-               * velocity u*: f_ibar(x) = -f*_i(x) + 2 w_ibar rho_out [1 + (c_ibar.u*)^2/(2c_s^4)
-               *                                                   - u*^2/(2c_s^2)] */
-              double cu = cb[0] * ustar[0] + cb[1] * ustar[1] + cb[2] * ustar[2];
-              double uu = ustar[0] * ustar[0] + ustar[1] * ustar[1] + ustar[2] * ustar[2];
-              S->fnew[(int64_t)ib * N + c] =
-                  -fs[i] + 2.0 * wb * S->rho_out *
-                               (1.0 + (cu * cu) / (2.0 * CS2 * CS2) - uu / (2.0 * CS2));
+              /* pressure outflow, anti-bounce-back: f_ibar(x) = -f*_i(x) + (equilibrium part,
+               * added by the outflow pass after streaming, which needs the new state) */
+              S->fnew[(int64_t)ib * N + c] = -fs[i];
             }
             continue;
           }
@@ -868,6 +851,34 @@ int orc_step(orc_sim* S) {
             S->fnew[(int64_t)ib * N + c] = fs[i];
           else
             S->fnew[(int64_t)i * N + cidx(S, xn[0], xn[1], xn[2])] = fs[i];
+        }
+      }
+  }
+  if (S->bc[0] == 2) {
+    /* A30 pressure outflow at x = nx-1, completed on the new state: the populations entering
+     * from outside (c_x = -1) are unknown; the known ones give, with rho = rho_out (Zou & He),
+     * u_x = (S_0 + 2 S_+) / rho_out - 1 (S_0: c_x = 0, S_+: c_x = +1), u_y = u_z = 0, and
+     * f_q = -f*_qbar + 2 w_q rho_out [1 + (c_q.u)^2/(2c_s^4) - u^2/(2c_s^2)]. */
+    for (int z = 0; z < nz; ++z)
+      for (int y = 0; y < ny; ++y) {
+        const int64_t c = cidx(S, nx - 1, y, z);
+        double S0 = 0.0, Sp = 0.0;
+        for (int i = 0; i < Q; ++i) {
+          int cc[3];
+          stencil_c(Q, i, cc);
+          if (cc[0] == 0) S0 += S->fnew[(int64_t)i * N + c];
+          if (cc[0] == 1) Sp += S->fnew[(int64_t)i * N + c];
+        }
+        const double u[3] = {(S0 + 2.0 * Sp) / S->rho_out - 1.0, 0.0, 0.0};
+        const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+        for (int i = 0; i < Q; ++i) {
+          int cc[3];
+          stencil_c(Q, i, cc);
+          if (cc[0] != -1) continue;
+          const double cu = cc[0] * u[0] + cc[1] * u[1] + cc[2] * u[2];
+          S->fnew[(int64_t)i * N + c] +=
+              2.0 * stencil_w(Q, i) * S->rho_out *
+              (1.0 + (cu * cu) / (2.0 * CS2 * CS2) - uu / (2.0 * CS2));
         }
       }
   }
