@@ -40,6 +40,13 @@ WORKLOADS = {
                 desc="c5 weak: D3Q19 PSM fp32, 512^3 per GPU, CROR-like counter-rotating rotor "
                      "pair per GPU (12+10 blades, ~1.1 M faces, s=1, remapped every step), SC1, "
                      "weighted B"),
+    # c5w as an application run: inflow U = 0.05 at x = 0, pressure outflow at
+    # x = nx-1 (reading A30), flow starting from rest
+    "c5app": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.55, rotors=True, s=1,
+                  omega=0.05 / 220.0, pattern="two_array", sc=1, bmode=1, bc=(2, 0, 0),
+                  open_bc=((0.05, 0.0, 0.0), 1.0),
+                  desc="c5 weak + open boundaries: c5w with velocity inflow U=0.05 at x=0 and "
+                       "pressure outflow rho=1 at x=nx-1 (A30), y/z periodic"),
     # c5 strong scaling: the whole ~1e9-cell CROR-like domain split over the GPUs (rotor axis x:
     # front 12 blades tip 220 at x=760, +Omega; rear 10 blades tip 200 at x=900, -Omega)
     "c5s": dict(nx=2048, ny=704, nz=704, Q=19, prec="f32", tau=0.55, rotors=True, s=1,
@@ -229,9 +236,12 @@ def build_workload(psm, wl: dict, rank: int, world: int, nccl_id=None):
     nx, ny = wl["nx"], wl["ny"]
     nzg = wl["nz"] if wl.get("strong") else wl["nz"] * world
     S = 8 if wl["prec"] == "f64" else 4
-    sim = psm.Simulation(nx, ny, nzg, Q=wl["Q"], tau=wl["tau"], bc=(0, 0, 0), prec=wl["prec"],
-                         pattern=wl["pattern"], sc=wl["sc"], bmode=wl["bmode"], rank=rank,
-                         world=world, nccl_id=nccl_id, collision=wl.get("collision", "srt"))
+    sim = psm.Simulation(nx, ny, nzg, Q=wl["Q"], tau=wl["tau"], bc=wl.get("bc", (0, 0, 0)),
+                         prec=wl["prec"], pattern=wl["pattern"], sc=wl["sc"], bmode=wl["bmode"],
+                         rank=rank, world=world, nccl_id=nccl_id,
+                         collision=wl.get("collision", "srt"))
+    if wl.get("open_bc"):
+        sim.set_open_boundary(*wl["open_bc"])
     sim.init_equilibrium(None, None)
     nbodies = 0
     body_poses = []  # (Q0, t0, v, w) per body, in id order

@@ -53,8 +53,12 @@ typedef enum { PSM_B_DIRECT = 0, PSM_B_WEIGHTED = 1 } psm_bmode;
 typedef enum { PSM_F64 = 0, PSM_F32 = 1 } psm_precision;
 /* Streaming realisation: two-field pull or in-place AA pattern. */
 typedef enum { PSM_TWO_ARRAY = 0, PSM_AA = 1 } psm_pattern;
-/* Domain boundary per axis: periodic, or half-way bounce-back resting wall. */
-typedef enum { PSM_PERIODIC = 0, PSM_WALL = 1 } psm_bc;
+/* Domain boundary per axis: periodic, half-way bounce-back resting wall, or (x axis
+ * only, nx >= 3, PSM_TWO_ARRAY only) the open boundaries of the paper's application runs
+ * ("boundary handling for inflow and outflow"; reading A30): velocity inflow
+ * at x = 0, pressure outflow at x = nx - 1, values set by psm_set_open_boundary.  On domain edges
+ * the x faces take precedence over walls. */
+typedef enum { PSM_PERIODIC = 0, PSM_WALL = 1, PSM_INOUT = 2 } psm_bc;
 typedef enum { PSM_SPHERE = 0, PSM_MESH = 1 } psm_shape_kind;
 /* Fluid collision operator: SRT (Eq.(2)), TRT (two relaxation times, one of the
  * operators the paper lists; symmetric rate 1/tau, antisymmetric 1/tau_- with
@@ -194,6 +198,21 @@ psm_status psm_get_body_state(const psm_ctx* ctx, int32_t body_id, psm_pose* pos
  * Errors: PSM_E_ARG (s out of 0..3, NULL arrays), PSM_E_MESH (as psm_set_body). */
 psm_status psm_voxelize(const double* verts, int64_t nverts, const int32_t* tris, int64_t ntris,
                         int32_t s, double origin[3], int64_t dims[3], uint8_t* bits);
+
+/* Open-boundary values for bc[0] == PSM_INOUT (reading A30; PAPER.md:584, 593 name the
+ * boundaries without defining them):
+ *   inflow  (x = 0):      f_q = f*_qbar + 6 w_q rho_w (c_q . u_in), rho_w = 1, for c_qx = +1
+ *                         (half-way bounce-back from a wall moving with u_in);
+ *   outflow (x = nx - 1): f_q = -f*_qbar + 2 w_q rho_out [1 + 9/2 (c_q . u)^2 - 3/2 u^2] for
+ *                         c_qx = -1 (anti-bounce-back), u = (u_x, 0, 0) with
+ *                         u_x = (S_0 + 2 S_+) / rho_out - 1 from the known populations of the
+ *                         cell (S_0: c_x = 0, S_+: c_x = +1; Zou & He's normal velocity).
+ * Defaults u_in = 0, rho_out = 1.  The device keeps the post-collision face sources f*_qbar, and
+ * the entering populations are formed with the values current when the state is next stepped or
+ * read — set them before psm_init_equilibrium / psm_write_pdfs so the written state is exact.
+ * Errors: PSM_E_ARG (NULL, non-finite u_in, rho_out not finite and > 0), PSM_E_UNSUPPORTED
+ * (bc[0] != PSM_INOUT). */
+psm_status psm_set_open_boundary(psm_ctx* ctx, const double u_in[3], double rho_out);
 
 /* Recompute the solid fraction field of every body at its current pose:
  * eps = (#inside sub-samples) / 2^(3s) (reading R1, A12), B by Eq.(5)/(6). */

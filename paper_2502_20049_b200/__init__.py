@@ -27,7 +27,7 @@ PSM_SC1, PSM_SC2, PSM_SC3 = 1, 2, 3
 PSM_B_DIRECT, PSM_B_WEIGHTED = 0, 1
 PSM_F64, PSM_F32 = 0, 1
 PSM_TWO_ARRAY, PSM_AA = 0, 1
-PSM_PERIODIC, PSM_WALL = 0, 1
+PSM_PERIODIC, PSM_WALL, PSM_INOUT = 0, 1, 2
 PSM_SPHERE, PSM_MESH = 0, 1
 PSM_SRT, PSM_TRT, PSM_CUMULANT = 0, 1, 2
 PSM_MAP_R1, PSM_MAP_R2 = 0, 1
@@ -40,6 +40,7 @@ EXPORTED = (
     "psm_init_equilibrium", "psm_write_pdfs", "psm_read_pdfs", "psm_read_pdfs_planes",
     "psm_read_velocity",
     "psm_set_body", "psm_remove_body", "psm_voxelize", "psm_set_dynamics",
+    "psm_set_open_boundary",
     "psm_get_body_state", "psm_map_fractions", "psm_step", "psm_force_torque",
     "psm_read_fractions", "psm_debug_set_fields", "psm_get_step", "psm_launch_count",
     "psm_profile", "psm_profile_read", "psm_nccl_id_bytes", "psm_nccl_get_unique_id",
@@ -108,6 +109,7 @@ def load(build_if_missing: bool = True):
         "psm_remove_body": [P, I32], "psm_map_fractions": [P],
         "psm_voxelize": [P, I64, P, I64, I32, P, P, P], "psm_step": [P, I64],
         "psm_set_dynamics": [P, I32, P], "psm_get_body_state": [P, I32, P, P],
+        "psm_set_open_boundary": [P, P, C.c_double],
         "psm_force_torque": [P, I32, P, P, P, P], "psm_read_fractions": [P, P, P, P],
         "psm_debug_set_fields": [P, P, P, P], "psm_get_step": [P, P],
         "psm_launch_count": [P, P], "psm_profile": [P, I32], "psm_profile_read": [P, P, P],
@@ -217,6 +219,11 @@ def psm_voxelize(verts, tris, s: int):
 
 def psm_set_dynamics(ctx, body_id: int, dyn):
     _check(load().psm_set_dynamics(ctx, body_id, None if dyn is None else C.byref(dyn)), ctx)
+
+
+def psm_set_open_boundary(ctx, u_in, rho_out: float = 1.0):
+    u = (C.c_double * 3)(*[float(v) for v in u_in])
+    _check(load().psm_set_open_boundary(ctx, u, float(rho_out)), ctx)
 
 
 def psm_get_body_state(ctx, body_id: int):
@@ -377,6 +384,10 @@ class Simulation:
 
     def body_state(self, bid):
         return psm_get_body_state(self.ctx, bid)
+
+    def set_open_boundary(self, u_in=(0.0, 0.0, 0.0), rho_out=1.0):
+        """bc[0] == PSM_INOUT: inflow velocity at x = 0, outflow density at x = nx-1 (A30)."""
+        psm_set_open_boundary(self.ctx, u_in, rho_out)
 
     def remove_body(self, bid):
         psm_remove_body(self.ctx, bid)

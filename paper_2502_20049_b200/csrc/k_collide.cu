@@ -320,7 +320,9 @@ constexpr int collide_min_blocks() {
   return sizeof(T) == 8 ? 2 : (Q == 19 ? (PAT == 2 ? 3 : 4) : (PAT == 2 ? 2 : 3));
 }
 
-template <int Q, typename T, int PAT, bool WALLS, bool FORCE, bool DBG, int COLL>
+// WALLS: 0 fully periodic; 1 runtime wall flags on every axis; 2 only x is non-periodic (open
+// x faces or x walls) with y, z periodic — the y/z flag logic compiles out
+template <int Q, typename T, int PAT, int WALLS, bool FORCE, bool DBG, int COLL>
 __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COLL>()))
     k_collide(const __grid_constant__ CollideParams p) {
   const Geom& G = p.g;
@@ -347,17 +349,17 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
        OUTZ[3] = {false, false, false};
   if (xc == 0) { if (WALLS && G.wall[0]) OUTX[2] = true; else OX[2] = nx - 1; }
   if (xc == nx - 1) { if (WALLS && G.wall[0]) OUTX[0] = true; else OX[0] = 1 - nx; }
-  if (yc == 0) { if (WALLS && G.wall[1]) OUTY[2] = true; else OY[2] = (ny - 1) * nx; }
-  if (yc == ny - 1) { if (WALLS && G.wall[1]) OUTY[0] = true; else OY[0] = (1 - ny) * nx; }
+  if (yc == 0) { if (WALLS == 1 && G.wall[1]) OUTY[2] = true; else OY[2] = (ny - 1) * nx; }
+  if (yc == ny - 1) { if (WALLS == 1 && G.wall[1]) OUTY[0] = true; else OY[0] = (1 - ny) * nx; }
   if (G.zghost) {
-    if (WALLS && G.wall[2]) {
+    if (WALLS == 1 && G.wall[2]) {
       const int zg = G.z0 + zc;
       OUTZ[2] = (zg == 0);
       OUTZ[0] = (zg == G.nz_global - 1);
     }
   } else {
-    if (zc == 0) { if (WALLS && G.wall[2]) OUTZ[2] = true; else OZ[2] = (G.nzl - 1) * plane; }
-    if (zc == G.nzl - 1) { if (WALLS && G.wall[2]) OUTZ[0] = true; else OZ[0] = (1 - G.nzl) * plane; }
+    if (zc == 0) { if (WALLS == 1 && G.wall[2]) OUTZ[2] = true; else OZ[2] = (G.nzl - 1) * plane; }
+    if (zc == G.nzl - 1) { if (WALLS == 1 && G.wall[2]) OUTZ[0] = true; else OZ[0] = (1 - G.nzl) * plane; }
   }
   int RB[3][3];  // self + OY[cy] + OZ[cz]
 #pragma unroll
@@ -383,6 +385,35 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
       } else {
         const T* ptr = out ? (Aq + self) : (Ao + src);
         f[q] = *ptr;
+      }
+    }
+  }
+
+  // ---- open x faces (reading A30): the populations entering at x = 0 / nx-1 were gathered
+  // from their bounce-back source A_qbar(x); apply the inflow / outflow rule ----
+  if constexpr (WALLS && PAT == 0) {
+    if (G.open_x) {
+      if (xc == 0) {
+        const T ux = T(p.u_in[0]), uy = T(p.u_in[1]), uz = T(p.u_in[2]);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (stc_x(q) == 1)
+            f[q] += T(6) * T(stc_w<Q>(q)) * (T(stc_x(q)) * ux + T(stc_y(q)) * uy +
+                                             T(stc_z(q)) * uz);
+      }
+      if (xc == nx - 1) {
+        T S0 = T(0), Sp = T(0);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          if (stc_x(q) == 0) S0 += f[q];
+          if (stc_x(q) == 1) Sp += f[q];
+        }
+        const T ro = T(p.rho_out);
+        const T ux = (S0 + T(2) * Sp) / ro - T(1);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (stc_x(q) == -1)
+            f[q] = T(2) * T(stc_w<Q>(q)) * ro * (T(1) + T(4.5) * ux * ux - T(1.5) * ux * ux) - f[q];
       }
     }
   }
@@ -592,6 +623,7 @@ template <int Q, typename T>
 static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, bool dbg,
                                   dim3 grid, dim3 block, cudaStream_t st) {
   const bool walls = p.g.wall[0] || p.g.wall[1] || p.g.wall[2];
+  const bool xonly = p.g.wall[0] && !p.g.wall[1] && !p.g.wall[2];  // e.g. open x faces
   if (p.trt == 1) {
     // TRT: the general (runtime wall flags) variants only
     if (dbg || force) {
@@ -614,9 +646,10 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
       const size_t sm = (size_t)Q * kTileCells * sizeof(T);  // PSM-cell stash
       static bool attr = false;                             // once per instantiation
       if (!attr) {
-        const void* fns[5] = {(const void*)k_collide<Q, T, 0, true, false, true, 2>,
+        const void* fns[6] = {(const void*)k_collide<Q, T, 0, true, false, true, 2>,
                               (const void*)k_collide<Q, T, 0, false, false, false, 2>,
                               (const void*)k_collide<Q, T, 0, true, false, false, 2>,
+                              (const void*)k_collide<Q, T, 0, 2, false, false, 2>,
                               (const void*)k_collide<Q, T, 1, false, false, false, 2>,
                               (const void*)k_collide<Q, T, 2, true, false, false, 2>};
         for (const void* fn : fns) {
@@ -628,6 +661,7 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
       }
       if (dbg) k_collide<Q, T, 0, true, false, true, 2><<<grid, block, sm, st>>>(p);
       else if (pat == 0 && !walls) k_collide<Q, T, 0, false, false, false, 2><<<grid, block, sm, st>>>(p);
+      else if (pat == 0 && xonly) k_collide<Q, T, 0, 2, false, false, 2><<<grid, block, sm, st>>>(p);
       else if (pat == 0) k_collide<Q, T, 0, true, false, false, 2><<<grid, block, sm, st>>>(p);
       else if (pat == 1) k_collide<Q, T, 1, false, false, false, 2><<<grid, block, sm, st>>>(p);
       else k_collide<Q, T, 2, true, false, false, 2><<<grid, block, sm, st>>>(p);
@@ -641,7 +675,8 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
     else if (dbg) k_collide<Q, T, 0, true, false, true, 0><<<grid, block, 0, st>>>(p);
     else k_collide<Q, T, 0, true, true, false, 0><<<grid, block, 0, st>>>(p);
   } else if (pat == 0) {
-    if (walls) k_collide<Q, T, 0, true, false, false, 0><<<grid, block, 0, st>>>(p);
+    if (xonly) k_collide<Q, T, 0, 2, false, false, 0><<<grid, block, 0, st>>>(p);
+    else if (walls) k_collide<Q, T, 0, true, false, false, 0><<<grid, block, 0, st>>>(p);
     else k_collide<Q, T, 0, false, false, false, 0><<<grid, block, 0, st>>>(p);
   } else if (pat == 1) {
     k_collide<Q, T, 1, false, false, false, 0><<<grid, block, 0, st>>>(p);

@@ -30,6 +30,22 @@ __device__ __forceinline__ bool nb_coord(int c, int n, bool wall, int& out) {
   return true;
 }
 
+// Reading A30 (open x faces), in the pull form f_q(x) = rule(A_qbar(x)) for the populations
+// entering through a face:
+//   inflow  x = 0,      c_qx = +1: f_q = A_qbar + ubb_q,             ubb_q = 6 w_q (c_q . u_in)
+//   outflow x = nx - 1, c_qx = -1: f_q = -A_qbar + abb_q(u_x),
+//           abb_q = 2 w_q rho_out (1 + 4.5 (c_qx u_x)^2 - 1.5 u_x^2),
+//           u_x = (S_0 + 2 S_+) / rho_out - 1 over the cell's known populations (c_x >= 0).
+template <int Q>
+__device__ __forceinline__ double open_ubb(int q, const double* u_in) {
+  return 6.0 * stc_w<Q>(q) * (stc_x(q) * u_in[0] + stc_y(q) * u_in[1] + stc_z(q) * u_in[2]);
+}
+template <int Q>
+__device__ __forceinline__ double open_abb(int q, double ux, double rho_out) {
+  const double cu = stc_x(q) * ux;
+  return 2.0 * stc_w<Q>(q) * rho_out * (1.0 + 4.5 * cu * cu - 1.5 * ux * ux);
+}
+
 template <int Q, typename T>
 __global__ void k_write_state(const StateParams p) {
   const Geom& G = p.g;
@@ -60,6 +76,26 @@ __global__ void k_write_state(const StateParams p) {
     if (p.pattern == 1) {  // AA after a write: even, A[j][x] = f_j(x)
       if (ghost_plane) continue;
       A[j * G.qstride + slot] = (T)fetch(j, x, y, z);
+      continue;
+    }
+    // A30: a slot whose reader y + c_j lies beyond an open x face is the source of the entering
+    // population q = jbar at y itself; invert the face rule
+    if (G.open_x && (x + stc_x(j) < 0 || x + stc_x(j) >= G.nx)) {
+      if (ghost_plane) continue;
+      const int q = stc_opp(j);
+      double v;
+      if (stc_x(j) < 0) {
+        v = fetch(q, x, y, z) - open_ubb<Q>(q, p.u_in);
+      } else {
+        double S0 = 0.0, Sp = 0.0;
+        for (int i = 0; i < Q; ++i) {
+          if (stc_x(i) == 0) S0 += fetch(i, x, y, z);
+          if (stc_x(i) == 1) Sp += fetch(i, x, y, z);
+        }
+        const double ux = (S0 + 2.0 * Sp) / p.rho_out - 1.0;
+        v = open_abb<Q>(q, ux, p.rho_out) - fetch(q, x, y, z);
+      }
+      A[j * G.qstride + slot] = (T)v;
       continue;
     }
     // the slot is read by y + c_j, or by y itself (bounce) if y + c_j crosses a wall
@@ -101,7 +137,7 @@ __global__ void k_read_state(const StateParams p) {
   const long long self = ((long long)zs * G.ny + y) * G.nx + x;
   const long long sp = (long long)p.stage_nz * G.nx * G.ny;
   const long long c = ((long long)(z - p.stage_z0) * G.ny + y) * G.nx + x;
-  double rho = 0, j[3] = {0, 0, 0};
+  double fq[Q];
   for (int q = 0; q < Q; ++q) {
     double v;
     if (p.pattern == 1 && !p.odd) {
@@ -123,6 +159,25 @@ __global__ void k_read_state(const StateParams p) {
       else
         v = in ? (double)A[stc_opp(q) * G.qstride + src] : (double)A[q * G.qstride + self];
     }
+    fq[q] = v;
+  }
+  if (G.open_x && x == 0) {  // A30 inflow
+    for (int q = 0; q < Q; ++q)
+      if (stc_x(q) == 1) fq[q] += open_ubb<Q>(q, p.u_in);
+  }
+  if (G.open_x && x == G.nx - 1) {  // A30 outflow: fq[q] holds A_qbar(x) for c_qx = -1
+    double S0 = 0.0, Sp = 0.0;
+    for (int q = 0; q < Q; ++q) {
+      if (stc_x(q) == 0) S0 += fq[q];
+      if (stc_x(q) == 1) Sp += fq[q];
+    }
+    const double ux = (S0 + 2.0 * Sp) / p.rho_out - 1.0;
+    for (int q = 0; q < Q; ++q)
+      if (stc_x(q) == -1) fq[q] = open_abb<Q>(q, ux, p.rho_out) - fq[q];
+  }
+  double rho = 0, j[3] = {0, 0, 0};
+  for (int q = 0; q < Q; ++q) {
+    const double v = fq[q];
     if (p.mode == 0) {
       p.stage[q * sp + c] = v;
     } else {

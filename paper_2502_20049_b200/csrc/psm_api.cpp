@@ -68,6 +68,8 @@ struct psm_ctx {
   int Q = 19;
   double tau = 0.8;
   psm_options opt{};
+  double u_in[3] = {0.0, 0.0, 0.0};  // A30 open boundaries (bc[0] == PSM_INOUT)
+  double rho_out = 1.0;
   int rank = 0, world = 1;
   int64_t z0 = 0, nzl = 0;
   Geom geom{};
@@ -730,6 +732,8 @@ static psm_status state_write(psm_ctx* c, const double* host, int mode) {
     p.pattern = c->opt.pattern == PSM_AA ? 1 : 0;
     p.mode = mode;
     p.ghosts = ghost ? 1 : 0;
+    for (int a = 0; a < 3; ++a) p.u_in[a] = c->u_in[a];
+    p.rho_out = c->rho_out;
     if (mode != 2) {
       // staging planes cover the readers of slots in [za, zb): local planes [za-1, zb+1)
       int64_t s0 = za - 1, s1 = zb + 1;
@@ -807,6 +811,8 @@ static psm_status state_read(psm_ctx* c, double* f, double* rho, double* u, int6
     p.zb = (int)zb;
     p.stage_z0 = (int)za;
     p.stage_nz = (int)(zb - za);
+    for (int a = 0; a < 3; ++a) p.u_in[a] = c->u_in[a];
+    p.rho_out = c->rho_out;
     p.pattern = c->opt.pattern == PSM_AA ? 1 : 0;
     p.odd = (int)(c->step & 1);
     p.mode = mode;
@@ -876,8 +882,13 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   if (grid->nx < 1 || grid->ny < 1 || grid->nz < 1)
     FAIL((psm_ctx*)nullptr, PSM_E_ARG, "grid extents must be >= 1");
   for (int a = 0; a < 3; ++a)
-    if (grid->bc[a] != PSM_PERIODIC && grid->bc[a] != PSM_WALL)
+    if (grid->bc[a] != PSM_PERIODIC && grid->bc[a] != PSM_WALL && grid->bc[a] != PSM_INOUT)
       FAIL((psm_ctx*)nullptr, PSM_E_ARG, "bad boundary kind");
+  if (grid->bc[1] == PSM_INOUT || grid->bc[2] == PSM_INOUT)
+    FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "inflow/outflow boundaries are on the x axis only");
+  if (grid->bc[0] == PSM_INOUT && (grid->nx < 3 || opt->pattern != PSM_TWO_ARRAY))
+    FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED,
+         "inflow/outflow boundaries need nx >= 3 and PSM_TWO_ARRAY");
   if ((opt->prec != PSM_F64 && opt->prec != PSM_F32) ||
       (opt->pattern != PSM_TWO_ARRAY && opt->pattern != PSM_AA) || opt->sc < 1 || opt->sc > 3 ||
       (opt->bmode != PSM_B_DIRECT && opt->bmode != PSM_B_WEIGHTED) ||
@@ -917,7 +928,9 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   g.nz_global = (int)grid->nz;
   g.z0 = (int)c->z0;
   g.zghost = world > 1 ? 1 : 0;
-  for (int a = 0; a < 3; ++a) g.wall[a] = grid->bc[a] == PSM_WALL;
+  // wall[a]: the axis is not periodic (half-way bounce-back sources; A30 patches the x faces)
+  for (int a = 0; a < 3; ++a) g.wall[a] = grid->bc[a] != PSM_PERIODIC;
+  g.open_x = grid->bc[0] == PSM_INOUT;
   g.qstride = (long long)(c->nzl + 2 * g.zghost) * grid->ny * grid->nx;
   g.gx = (int)((grid->nx + kTileX - 1) / kTileX);
   g.gy = (int)((grid->ny + kTileY - 1) / kTileY);
@@ -1136,6 +1149,17 @@ psm_status psm_voxelize(const double* verts, int64_t nverts, const int32_t* tris
   return PSM_OK;
 }
 
+psm_status psm_set_open_boundary(psm_ctx* c, const double u_in[3], double rho_out) {
+  if (!c || !u_in) FAIL(c, PSM_E_ARG, "null argument");
+  if (c->grid.bc[0] != PSM_INOUT) FAIL(c, PSM_E_UNSUPPORTED, "bc[0] is not PSM_INOUT");
+  if (!(std::isfinite(rho_out) && rho_out > 0.0) || !std::isfinite(u_in[0]) ||
+      !std::isfinite(u_in[1]) || !std::isfinite(u_in[2]))
+    FAIL(c, PSM_E_ARG, "u_in must be finite, rho_out finite and > 0");
+  for (int a = 0; a < 3; ++a) c->u_in[a] = u_in[a];
+  c->rho_out = rho_out;
+  return PSM_OK;
+}
+
 psm_status psm_set_dynamics(psm_ctx* c, int32_t id, const psm_dynamics* d) {
   if (!c) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null ctx");
   if (id < 1 || id > kMaxBodies || !c->bodies[id].present) FAIL(c, PSM_E_ARG, "unknown body");
@@ -1269,6 +1293,8 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
                   : p.omega;
   p.trt = c->opt.collision == PSM_TRT ? 1 : (c->opt.collision == PSM_CUMULANT ? 2 : 0);
   for (int a = 0; a < 3; ++a) p.gforce[a] = c->opt.body_force[a];
+  for (int a = 0; a < 3; ++a) p.u_in[a] = c->u_in[a];
+  p.rho_out = c->rho_out;
   p.sc = c->opt.sc;
   p.bmode = c->opt.bmode;
   CUDA_TRY(c, cudaMemsetAsync(c->overflow, 0, (kMaxBodies + 1) * kSlotVals * 8, c->st));

@@ -87,7 +87,8 @@ struct Geom {
   int nz_global;
   int z0;                 // global z of local plane 0
   int zghost;             // 1: ghost planes at local z = -1 and nzl (world > 1)
-  int wall[3];            // 1 = half-way bounce-back wall on this axis
+  int wall[3];            // 1 = not periodic: half-way bounce-back wall on this axis
+  int open_x;             // x faces are inflow (x = 0) / outflow (x = nx-1), reading A30
   long long qstride;      // elements between consecutive direction planes
   int gx, gy, gz;         // tile grid
 };
@@ -108,6 +109,8 @@ struct CollideParams {
   double omega_m;         // antisymmetric rate w- (TRT; == omega for SRT)
   int trt;                // fluid operator: 0 SRT (Eq.(2)), 1 TRT, 2 cumulant (D3Q27)
   double gforce[3];       // test-only Guo force
+  double u_in[3];         // A30 inflow velocity (g.open_x)
+  double rho_out;         // A30 outflow density (g.open_x)
   int sc;                 // 1, 2, 3
   int bmode;              // 0 direct, 1 weighted
   long long step;         // for the error word

@@ -30,6 +30,8 @@ struct StateParams {
   int mode;              // write: 0 = f from stage [Q][planes], 1 = feq from rho,u stage
                          //        [4][planes], 2 = uniform rho=1,u=0; read: 0 = f, 1 = rho,u
   int ghosts;            // write: also fill the ghost planes adjacent to [za, zb)
+  double u_in[3];        // A30 open x faces (g.open_x): inflow velocity
+  double rho_out;        //                              outflow density
 };
 cudaError_t launch_write_state(int Q, bool fp64, const StateParams& p, cudaStream_t st);
 cudaError_t launch_read_state(int Q, bool fp64, const StateParams& p, cudaStream_t st);

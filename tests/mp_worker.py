@@ -25,7 +25,8 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     failures = []
-    for (bc, Q, prec) in [((0, 0, 0), 19, "f64"), ((0, 1, 1), 27, "f64"), ((0, 0, 0), 19, "f32")]:
+    for (bc, Q, prec) in [((0, 0, 0), 19, "f64"), ((0, 1, 1), 27, "f64"), ((0, 0, 0), 19, "f32"),
+                          ((2, 1, 0), 19, "f64")]:  # last: open x faces (A30) + y walls
         # an ncclUniqueId serves exactly one communicator: a fresh one per context
         idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
@@ -37,6 +38,9 @@ def main():
         kw = dict(Q=Q, tau=0.7, bc=bc, prec=prec, sc=1, bmode=1)
         dsim = psm.Simulation(nx, ny, nz, rank=rank, world=world, nccl_id=nid, **kw)
         ref = psm.Simulation(nx, ny, nz, **kw)
+        if bc[0] == 2:
+            for s in (ref, dsim):
+                s.set_open_boundary((0.03, 0.0, 0.01), 1.0)
         rho, u = pi.perturbed_flow((nz, ny, nx), 99, u0=(0.03, 0.0, 0.01))
         z0, nzl = dsim.z0, dsim.nzl
         ref.init_equilibrium(rho, u)

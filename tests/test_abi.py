@@ -70,11 +70,33 @@ def test_create_validation_codes():
         (dict(coll=3), _grid(), 27, psm.PSM_E_ARG),
         (dict(coll=2), _grid(), 19, psm.PSM_E_UNSUPPORTED),  # cumulant needs D3Q27
         (dict(coll=1, magic=0.0), _grid(), 19, psm.PSM_E_ARG),
+        (dict(), _grid(8, 8, 8, (0, 2, 0)), 19, psm.PSM_E_UNSUPPORTED),  # open faces: x only
+        (dict(), _grid(2, 8, 8, (2, 0, 0)), 19, psm.PSM_E_UNSUPPORTED),  # nx >= 3
+        (dict(pattern=psm.PSM_AA), _grid(8, 8, 8, (2, 0, 0)), 19, psm.PSM_E_UNSUPPORTED),
     ]
     for kw, g, q, code in cases:
         with pytest.raises(psm.PSMError) as e:
             psm.psm_create(g, q, 0.8, _opts(**kw))
         assert e.value.code == code, (kw, e.value)
+
+
+def test_open_boundary_setter_codes():
+    ctx = psm.psm_create(_grid(8, 8, 8), 19, 0.7, _opts())
+    try:
+        with pytest.raises(psm.PSMError) as e:
+            psm.psm_set_open_boundary(ctx, (0.01, 0, 0), 1.0)
+        assert e.value.code == psm.PSM_E_UNSUPPORTED  # bc[0] is periodic
+    finally:
+        psm.psm_destroy(ctx)
+    ctx = psm.psm_create(_grid(8, 8, 8, (2, 1, 0)), 19, 0.7, _opts())
+    try:
+        psm.psm_set_open_boundary(ctx, (0.01, 0, 0), 1.0)
+        for u, r in (((0.01, 0, 0), 0.0), ((float("nan"), 0, 0), 1.0), ((0, 0, 0), float("inf"))):
+            with pytest.raises(psm.PSMError) as e:
+                psm.psm_set_open_boundary(ctx, u, r)
+            assert e.value.code == psm.PSM_E_ARG
+    finally:
+        psm.psm_destroy(ctx)
 
 
 def test_create_succeeds_host_only_and_reports_layout():

@@ -32,7 +32,7 @@ def _ft_close(g, o, rel=FT_REL):
 
 def _run_pair(nx, ny, nz, Q, tau, bc, sc, bmode, prec, pattern, bodies, steps, seed,
               u0=(0.05, 0.0, 0.0), ft_every=True, force=(0.0, 0.0, 0.0), collision="srt",
-              magic=3.0 / 16.0, ft_rel=FT_REL):
+              magic=3.0 / 16.0, ft_rel=FT_REL, open_bc=None):
     """bodies: list of dicts (id, kind, r | mesh, s, pose(k) -> (Q, t), v, w).  Explicit poses
     are passed every step to both sides (reading A13)."""
     shape = (nz, ny, nx)
@@ -42,6 +42,9 @@ def _run_pair(nx, ny, nz, Q, tau, bc, sc, bmode, prec, pattern, bodies, steps, s
     o.set_collision(collision, magic)
     g = _sim(nx=nx, ny=ny, nz=nz, Q=Q, tau=tau, bc=bc, prec=prec, pattern=pattern, sc=sc,
              bmode=bmode, body_force=force, collision=collision, trt_magic=magic)
+    if open_bc is not None:  # before the state is written (psm.h psm_set_open_boundary)
+        o.set_open_boundary(*open_bc)
+        g.set_open_boundary(*open_bc)
     o.init_equilibrium(rho, u)
     g.init_equilibrium(rho, u)
     for b in bodies:
@@ -418,3 +421,63 @@ def test_cumulant_psm_rotating_mesh(pattern, bc, prec):
                      ft_rel=FT_REL if prec == "f64" else 1e-4)  # fp32: ~30 steps of 1e-7 drift
     tol = F64_TOL if prec == "f64" else F32_TOL
     assert np.max(np.abs(o.pdfs() - g.pdfs())) <= tol
+
+
+# ---- open boundaries (reading A30): velocity inflow at x = 0, pressure outflow at x = nx-1 ----
+OPEN = ((0.05, 0.01, -0.005), 1.002)
+
+
+@pytest.mark.parametrize("sc", [1, 2])
+def test_open_channel_moving_sphere_fp64(sc):
+    """Channel with inflow/outflow on x, no-slip walls on y (domain edges: x faces win), periodic
+    z; a sphere crosses the channel; D3Q19 fp64, 100 steps, F/T every step."""
+    o, g = _run_pair(48, 20, 18, 19, 0.7, (2, 1, 0), sc, 1, "f64", "two_array",
+                     [dict(id=1, kind="sphere", r=5.0, s=1, v=(0.02, 0.0, 0.0),
+                           pose=lambda k: (np.eye(3), (14.0 + 0.02 * k, 10.3, 9.1)))],
+                     100, 31, u0=(0.05, 0.0, 0.0), open_bc=OPEN)
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+
+
+@pytest.mark.parametrize("collision,Q", [("trt", 19), ("cumulant", 27), ("srt", 27)])
+def test_open_channel_rotating_mesh_operators(collision, Q):
+    v, tr = pi.propeller_mesh(n_blades=3, scale=0.07, n_st=8, n_pts=16, hub_seg=16)
+    w = np.array([0.025, 0.0, 0.0])
+
+    def pose(k):
+        return oracle.pose_advance(np.eye(3), [20.0, 11.0, 9.5], [0, 0, 0], w, k, [40, 22, 19],
+                                   [0, 1, 0])
+
+    o, g = _run_pair(40, 22, 19, Q, 0.62, (2, 1, 1), 1, 1, "f64", "two_array",
+                     [dict(id=1, kind="mesh", verts=v, tris=tr, s=1, pose=pose, w=w)], 30, 23,
+                     u0=(0.04, 0.0, 0.0), collision=collision, open_bc=OPEN)
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+
+
+def test_open_channel_fp32():
+    o, g = _run_pair(64, 16, 12, 19, 0.6, (2, 1, 0), 1, 1, "f32", "two_array",
+                     [dict(id=1, kind="sphere", r=4.0, s=2,
+                           pose=lambda k: (np.eye(3), (20.0, 8.0, 6.0)))],
+                     60, 37, u0=(0.05, 0.0, 0.0), ft_every=False, ft_rel=1e-4,
+                     open_bc=((0.05, 0.0, 0.0), 1.0))
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F32_TOL
+
+
+def test_open_state_roundtrip():
+    """write_pdfs inverts the face rules (A30) exactly: reading back gives the state written."""
+    for Q in (19, 27):
+        s = _sim(nx=9, ny=6, nz=5, bc=(2, 1, 0), Q=Q)
+        s.set_open_boundary((0.03, -0.01, 0.02), 0.98)
+        f = pi.random_pdfs(Q, (5, 6, 9), 5, w=oracle.stencil(Q)[1])
+        s.write_pdfs(f)
+        assert np.max(np.abs(s.pdfs() - f)) <= 1e-15
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_open_x_only_periodic_yz(prec):
+    """Open x faces with periodic y, z: the launcher's x-only wall variant."""
+    o, g = _run_pair(40, 12, 12, 19, 0.65, (2, 0, 0), 1, 1, prec, "two_array",
+                     [dict(id=1, kind="sphere", r=3.5, s=1, v=(0.0, 0.01, 0.0),
+                           pose=lambda k: (np.eye(3), (20.0, 3.0 + 0.01 * k, 6.0)))],
+                     40, 41, u0=(0.05, 0.0, 0.0), ft_every=(prec == "f64"),
+                     ft_rel=FT_REL if prec == "f64" else 1e-4, open_bc=OPEN)
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= (F64_TOL if prec == "f64" else F32_TOL)
