@@ -29,6 +29,13 @@ constexpr int kFtChunks = 296;           // 2 x 148 SMs, pass-1 blocks of the F/
 constexpr size_t kStageBudget = 256ull << 20;
 constexpr size_t kGeomCapBytes = 1ull << 30;
 
+struct MapState {
+  double Qc[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, tc[3] = {0, 0, 0};  // pose of the mapping
+  int64_t mapped_step = -1;
+  bool has_box = false;
+  int64_t box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};  // mapped box (global, unwrapped)
+};
+
 struct Body {
   bool present = false;
   int kind = 0, s = 0, mapping = 0;
@@ -45,11 +52,9 @@ struct Body {
   double v[3] = {0, 0, 0}, w[3] = {0, 0, 0};
   int64_t step0 = 0;
   bool moving = false;
-  // pose of the current mapping
-  double Qc[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, tc[3] = {0, 0, 0};
-  int64_t mapped_step = -1;
-  bool has_box = false;
-  int64_t box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};  // last mapped box (global, unwrapped)
+  // mapping state of the active solid-word buffer (ms) and of the spare one (alt, used by the
+  // remap-ahead pipeline of psm_step; swapped together with the buffers)
+  MapState ms, alt;
   // two-way coupling: state advanced by the host integrator after every step
   bool dynamic = false;
   double mass = 0, Ib[9] = {0}, fext[3] = {0, 0, 0}, text[3] = {0, 0, 0};
@@ -81,8 +86,15 @@ struct psm_ctx {
   bool own_mem = false, bound = false;
   void* A[2] = {nullptr, nullptr};
   int cur = 0;
-  uint32_t* word = nullptr;
+  uint32_t* word = nullptr;          // active solid-word buffer (read by the next collide)
   uint8_t* tile_flag = nullptr;
+  uint32_t* word_alt = nullptr;      // spare buffer: the remap of step n+1 runs into it while
+  uint8_t* tile_flag_alt = nullptr;  // the collide of step n reads the active one
+  bool alt_valid = false;            // the spare buffer's words match every body's alt state
+  cudaStream_t mst = nullptr;        // stream the remap launches go to (st, or map_st ahead)
+  cudaStream_t map_st = nullptr;     // remap-ahead stream (high priority)
+  cudaEvent_t ev_map = nullptr, ev_coll = nullptr;
+  int ahead_blocks = 148;            // persistent remap blocks when overlapped with the collide
   double* partial = nullptr;
   double* overflow = nullptr;
   unsigned long long* err = nullptr;
@@ -260,42 +272,42 @@ static void remap_region(const psm_ctx* c, Body& b, const double Q[9], const dou
                          std::vector<Box>& boxes) {
   int64_t lo[3], hi[3];
   body_box(c, b, Q, t, lo, hi);
-  if (b.has_box) {
+  if (b.ms.has_box) {
     bool overlap = true;
     int64_t slo[3], shi[3];
     for (int a = 0; a < 3; ++a) {
       int64_t shift = 0;
       if (c->grid.bc[a] == PSM_PERIODIC) {
         const int64_t L = (int64_t)extent(c, a);
-        const double dc = 0.5 * ((lo[a] + hi[a]) - (b.box_lo[a] + b.box_hi[a]));
+        const double dc = 0.5 * ((lo[a] + hi[a]) - (b.ms.box_lo[a] + b.ms.box_hi[a]));
         shift = -(int64_t)std::llround(dc / (double)L) * L;
       }
       slo[a] = lo[a] + shift;
       shi[a] = hi[a] + shift;
-      if (slo[a] >= b.box_hi[a] || shi[a] <= b.box_lo[a]) overlap = false;
+      if (slo[a] >= b.ms.box_hi[a] || shi[a] <= b.ms.box_lo[a]) overlap = false;
     }
     if (overlap) {
       int64_t ulo[3], uhi[3];
       for (int a = 0; a < 3; ++a) {
-        ulo[a] = std::min(slo[a], b.box_lo[a]);
-        uhi[a] = std::max(shi[a], b.box_hi[a]);
+        ulo[a] = std::min(slo[a], b.ms.box_lo[a]);
+        uhi[a] = std::max(shi[a], b.ms.box_hi[a]);
       }
       add_box(c, ulo, uhi, boxes);
     } else {
-      add_box(c, b.box_lo, b.box_hi, boxes);
+      add_box(c, b.ms.box_lo, b.ms.box_hi, boxes);
       add_box(c, lo, hi, boxes);
     }
   } else {
     add_box(c, lo, hi, boxes);
   }
   for (int a = 0; a < 3; ++a) {
-    b.box_lo[a] = lo[a];
-    b.box_hi[a] = hi[a];
+    b.ms.box_lo[a] = lo[a];
+    b.ms.box_hi[a] = hi[a];
   }
-  b.has_box = true;
+  b.ms.has_box = true;
 }
 
-static cudaError_t record(psm_ctx* c, int phase, int which) {
+static cudaError_t record(psm_ctx* c, int phase, int which, cudaStream_t s = nullptr) {
   if (!c->prof) return cudaSuccess;
   if (which == 0) {
     std::array<cudaEvent_t, 2> e{};
@@ -305,12 +317,12 @@ static cudaError_t record(psm_ctx* c, int phase, int which) {
     if (r != cudaSuccess) return r;
     c->ev[phase].push_back(e);
   }
-  return cudaEventRecord(c->ev[phase].back()[which], c->st);
+  return cudaEventRecord(c->ev[phase].back()[which], s ? s : c->st);
 }
 
 // ------------------------------------------------------------------------- memory plan -----
 struct Plan {
-  size_t off_A0, off_A1, off_word, off_flag, off_partial, off_overflow, off_err, off_scratch,
+  size_t off_A0, off_A1, off_word, off_flag, off_word_alt, off_flag_alt, off_partial, off_overflow, off_err, off_scratch,
       off_ftout, off_ids, off_stage, stage_bytes, total;
   size_t off_rcnt, off_rtiles, off_rsegs, off_rsegq, off_rband, off_rbandcnt;
   int seg_cap, band_cap;
@@ -331,6 +343,8 @@ static Plan make_plan(const psm_ctx* c) {
   p.off_A1 = (c->opt.pattern == PSM_TWO_ARRAY) ? take(arr) : 0;
   p.off_word = take((size_t)c->ncell_local * 4);
   p.off_flag = take((size_t)c->ntiles);
+  p.off_word_alt = take((size_t)c->ncell_local * 4);
+  p.off_flag_alt = take((size_t)c->ntiles);
   p.off_partial = take((size_t)c->ntiles * 2 * (1 + kSlotVals) * 8);
   p.off_overflow = take((kMaxBodies + 1) * kSlotVals * 8);
   p.off_err = take(8);
@@ -376,6 +390,9 @@ static psm_status bind(psm_ctx* c, void* mem, size_t bytes) {
   c->A[1] = (c->opt.pattern == PSM_TWO_ARRAY) ? (void*)(m + p.off_A1) : nullptr;
   c->word = reinterpret_cast<uint32_t*>(m + p.off_word);
   c->tile_flag = reinterpret_cast<uint8_t*>(m + p.off_flag);
+  c->word_alt = reinterpret_cast<uint32_t*>(m + p.off_word_alt);
+  c->tile_flag_alt = reinterpret_cast<uint8_t*>(m + p.off_flag_alt);
+  c->alt_valid = false;
   c->partial = reinterpret_cast<double*>(m + p.off_partial);
   c->overflow = reinterpret_cast<double*>(m + p.off_overflow);
   c->err = reinterpret_cast<unsigned long long*>(m + p.off_err);
@@ -482,7 +499,7 @@ static void fill_kin(const psm_ctx* c, CollideParams& p, int64_t step) {
     (void)Q;
     (void)t;
     for (int a = 0; a < 3; ++a) {
-      k.t[a] = b.tc[a];  // pose of the current mapping (remapped before this collide)
+      k.t[a] = b.ms.tc[a];  // pose of the current mapping (remapped before this collide)
       k.v[a] = b.dynamic ? b.vd[a] : b.v[a];
       k.w[a] = b.dynamic ? b.wd[a] : b.w[a];
     }
@@ -559,8 +576,8 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
     const Body& b = c->bodies[id];
     BodyGeo& g = mp.bodies[id];
     if (!b.present) continue;
-    std::memcpy(g.Q, b.Qc, sizeof(g.Q));
-    std::memcpy(g.t, b.tc, sizeof(g.t));
+    std::memcpy(g.Q, b.ms.Qc, sizeof(g.Q));
+    std::memcpy(g.t, b.ms.tc, sizeof(g.t));
     for (int a = 0; a < 3; ++a) {
       g.lo1[a] = b.bmin[a] - 1.0;
       g.hi1[a] = b.bmax[a] + 1.0;
@@ -601,9 +618,9 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
     m.bodymask = 0;
     for (int id = 1; id <= kMaxBodies; ++id) {
       const Body& bd = c->bodies[id];
-      if (!bd.present || !bd.has_box) continue;
+      if (!bd.present || !bd.ms.has_box) continue;
       std::vector<Box> pieces;
-      add_box(c, bd.box_lo, bd.box_hi, pieces);
+      add_box(c, bd.ms.box_lo, bd.ms.box_hi, pieces);
       for (const Box& pc : pieces) {
         bool ov = true;
         for (int a = 0; a < 3; ++a)
@@ -623,10 +640,10 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
   unsigned long long* dstats = nullptr;
   if (stats_on) {
     CUDA_TRY(c, cudaMalloc(&dstats, 8 * 8));
-    CUDA_TRY(c, cudaMemsetAsync(dstats, 0, 8 * 8, c->st));
+    CUDA_TRY(c, cudaMemsetAsync(dstats, 0, 8 * 8, c->mst));
   }
   mp.stats = dstats;
-  if (record(c, 0, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+  if (record(c, 0, 0, c->mst) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
   static const bool force_general = std::getenv("PSM_REMAP_GENERAL") != nullptr;
   for (size_t i = 0; i < tb.size(); ++i) {
     if (__builtin_popcount(tb[i].bodymask) == 1 && !force_general) {
@@ -647,7 +664,7 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
       r.bandcnt = c->r_bandcnt;
       r.seg_cap = c->seg_cap;
       r.band_cap = c->band_cap;
-      CUDA_TRY(c, launch_remap_single(r, 148 * 8, c->st));
+      CUDA_TRY(c, launch_remap_single(r, c->mst == c->st ? 148 * 8 : c->ahead_blocks, c->mst));
       c->launches += 4;
       continue;
     }
@@ -655,20 +672,37 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
     mp.box[0] = tb[i];
     mp.nbox = 1;
     mp.ntiles = tb[i].n[0] * tb[i].n[1] * tb[i].n[2];
-    CUDA_TRY(c, launch_map(mp, c->st));
+    CUDA_TRY(c, launch_map(mp, c->mst));
     c->launches += 1;
   }
-  if (record(c, 0, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+  if (record(c, 0, 1, c->mst) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
   if (dstats) {
     unsigned long long h[8];
-    CUDA_TRY(c, cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, c->st));
-    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    CUDA_TRY(c, cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, c->mst));
+    CUDA_TRY(c, cudaStreamSynchronize(c->mst));
     cudaFree(dstats);
     std::fprintf(stderr,
                  "[psm map] boxes %zu  8-cell segments: out %llu in %llu cell %llu | "
                  "cells: out %llu in %llu band %llu | tiles skipped %llu\n",
                  tb.size(), h[0], h[1], h[2], h[3], h[4], h[5], h[7]);
   }
+  return PSM_OK;
+}
+
+// the active and spare solid-word buffers trade places (with every body's mapping state)
+static void swap_buffers(psm_ctx* c) {
+  std::swap(c->word, c->word_alt);
+  std::swap(c->tile_flag, c->tile_flag_alt);
+  for (int id = 1; id <= kMaxBodies; ++id) std::swap(c->bodies[id].ms, c->bodies[id].alt);
+}
+
+static psm_status ensure_pipeline(psm_ctx* c) {
+  if (c->map_st) return PSM_OK;
+  int lo_prio = 0, hi_prio = 0;
+  CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  CUDA_TRY(c, cudaStreamCreateWithPriority(&c->map_st, cudaStreamNonBlocking, hi_prio));
+  CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_map, cudaEventDisableTiming));
+  CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_coll, cudaEventDisableTiming));
   return PSM_OK;
 }
 
@@ -688,21 +722,21 @@ static psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
       std::memcpy(Q, b.Q0, sizeof(Q));
       std::memcpy(t, b.t0, sizeof(t));
     }
-    std::memcpy(b.Qc, Q, sizeof(Q));
-    std::memcpy(b.tc, t, sizeof(t));
+    std::memcpy(b.ms.Qc, Q, sizeof(Q));
+    std::memcpy(b.ms.tc, t, sizeof(t));
     remap_region(c, b, Q, t, boxes);
-    b.mapped_step = step;
+    b.ms.mapped_step = step;
   }
   if (boxes.empty()) return PSM_OK;
   if (c->dbg) {  // leaving the debug field mode: the words are authoritative again
     c->dbg = false;
-    CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->st));
+    CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->mst));
     psm_status s = PSM_OK;
     std::vector<Box> all;
     for (int id = 1; id <= kMaxBodies; ++id)
-      if (c->bodies[id].present && c->bodies[id].has_box)
-        add_box(c, c->bodies[id].box_lo, c->bodies[id].box_hi, all);
-    CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->st));
+      if (c->bodies[id].present && c->bodies[id].ms.has_box)
+        add_box(c, c->bodies[id].ms.box_lo, c->bodies[id].ms.box_hi, all);
+    CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->mst));
     s = run_map(c, all);
     if (s != PSM_OK) return s;
   }
@@ -921,6 +955,8 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   c->z0 = (grid->nz * c->rank) / world;
   c->nzl = (grid->nz * (c->rank + 1)) / world - c->z0;
   c->st = static_cast<cudaStream_t>(opt->cuda_stream);
+  c->mst = c->st;
+  if (const char* e = std::getenv("PSM_AHEAD_BLOCKS")) c->ahead_blocks = std::max(1, std::atoi(e));
   Geom& g = c->geom;
   g.nx = (int)grid->nx;
   g.ny = (int)grid->ny;
@@ -950,6 +986,7 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
 psm_status psm_destroy(psm_ctx* c) {
   if (!c) return PSM_OK;
   cudaStreamSynchronize(c->st);
+  if (c->map_st) cudaStreamSynchronize(c->map_st);
   for (int id = 0; id <= kMaxBodies; ++id) {
     cudaFree(c->bodies[id].d_bits);
     cudaFree(c->bodies[id].d_mask);
@@ -968,6 +1005,9 @@ psm_status psm_destroy(psm_ctx* c) {
   if (c->comm_st) cudaStreamDestroy(c->comm_st);
   if (c->ev_bnd) cudaEventDestroy(c->ev_bnd);
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->map_st) cudaStreamDestroy(c->map_st);
+  if (c->ev_map) cudaEventDestroy(c->ev_map);
+  if (c->ev_coll) cudaEventDestroy(c->ev_coll);
   delete c;
   return PSM_OK;
 }
@@ -1100,10 +1140,10 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
       if (c->grid.bc[a] == PSM_PERIODIC && nb.rbound + 1.0 >= 0.5 * extent(c, a))
         FAIL(c, PSM_E_ARG, "body bounding radius + 1 must be < half a periodic extent");
     // keep the previous mapped box so the old footprint gets cleared
-    nb.has_box = b.has_box;
+    nb.ms.has_box = b.ms.has_box;
     for (int a = 0; a < 3; ++a) {
-      nb.box_lo[a] = b.box_lo[a];
-      nb.box_hi[a] = b.box_hi[a];
+      nb.ms.box_lo[a] = b.ms.box_lo[a];
+      nb.ms.box_hi[a] = b.ms.box_hi[a];
     }
     cudaStreamSynchronize(c->st);
     cudaFree(b.d_bits);
@@ -1129,6 +1169,7 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
     std::memcpy(b.wd, b.w, sizeof(b.wd));
   }
   c->ft_valid = false;
+  c->alt_valid = false;  // the spare word buffer no longer matches the bodies
   return remap(c, std::vector<int>{id}, c->step);
 }
 
@@ -1248,11 +1289,12 @@ psm_status psm_remove_body(psm_ctx* c, int32_t id) {
   Body& b = c->bodies[id];
   if (!b.present) return PSM_OK;
   std::vector<Box> boxes;
-  if (b.has_box) add_box(c, b.box_lo, b.box_hi, boxes);
+  if (b.ms.has_box) add_box(c, b.ms.box_lo, b.ms.box_hi, boxes);
   cudaStreamSynchronize(c->st);
   cudaFree(b.d_bits);
   cudaFree(b.d_mask);
   b = Body();
+  c->alt_valid = false;
   return run_map(c, boxes);
 }
 
@@ -1264,6 +1306,39 @@ psm_status psm_map_fractions(psm_ctx* c) {
   for (int id = 1; id <= kMaxBodies; ++id)
     if (c->bodies[id].present) ids.push_back(id);
   return remap(c, ids, c->step);
+}
+
+// Remap-ahead (prescribed motion only): enqueue the remap for step `next` into the spare buffer
+// on map_st, after the collide that last read that buffer (ev_coll); ev_map marks completion.
+// The remap is latency/ALU-bound and the collide HBM-bound, so the two overlap.
+static psm_status remap_ahead(psm_ctx* c, int64_t next) {
+  CUDA_TRY(c, cudaStreamWaitEvent(c->map_st, c->ev_coll, 0));
+  swap_buffers(c);
+  c->mst = c->map_st;
+  std::vector<int> ids;
+  if (!c->alt_valid) {  // start the spare buffer from scratch: every body mapped afresh
+    CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->mst));
+    CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->mst));
+    for (int id = 1; id <= kMaxBodies; ++id) {
+      c->bodies[id].ms = MapState();
+      if (c->bodies[id].present) ids.push_back(id);
+    }
+    c->alt_valid = true;
+  } else {
+    for (int id = 1; id <= kMaxBodies; ++id) {
+      const Body& b = c->bodies[id];
+      if (b.present && b.ms.mapped_step != next &&
+          (b.moving || b.ms.mapped_step < 0))
+        ids.push_back(id);
+    }
+  }
+  psm_status st = PSM_OK;
+  if (!ids.empty()) st = remap(c, ids, next);
+  c->mst = c->st;
+  swap_buffers(c);
+  if (st != PSM_OK) return st;
+  CUDA_TRY(c, cudaEventRecord(c->ev_map, c->map_st));
+  return PSM_OK;
 }
 
 psm_status psm_step(psm_ctx* c, int64_t n) {
@@ -1298,15 +1373,40 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
   p.sc = c->opt.sc;
   p.bmode = c->opt.bmode;
   CUDA_TRY(c, cudaMemsetAsync(c->overflow, 0, (kMaxBodies + 1) * kSlotVals * 8, c->st));
+  // remap-ahead pipeline: several steps in this call, bodies in prescribed motion only
+  bool any_moving = false, any_dynamic = false;
+  for (int id = 1; id <= kMaxBodies; ++id) {
+    const Body& b = c->bodies[id];
+    if (!b.present) continue;
+    any_moving |= b.moving;
+    any_dynamic |= b.dynamic;
+  }
+  static const bool no_ahead = std::getenv("PSM_NO_REMAP_AHEAD") != nullptr;
+  const bool ahead = n > 1 && any_moving && !any_dynamic && !c->dbg && !no_ahead;
+  if (ahead) {
+    st = ensure_pipeline(c);
+    if (st != PSM_OK) return st;
+  }
   for (int64_t k = 0; k < n; ++k) {
-    // 1. closed-form pose advance + remap of the bodies that moved
-    std::vector<int> moved;
-    for (int id = 1; id <= kMaxBodies; ++id) {
-      const Body& b = c->bodies[id];
-      if (b.present && b.moving && b.mapped_step != c->step) moved.push_back(id);
+    // 1. closed-form pose advance + remap of the bodies that moved; in the
+    // pipeline the remap for this step was enqueued during the previous one into the spare buffer
+    if (ahead && k > 0) {
+      swap_buffers(c);
+      CUDA_TRY(c, cudaStreamWaitEvent(c->st, c->ev_map, 0));
+    } else {
+      std::vector<int> moved;
+      for (int id = 1; id <= kMaxBodies; ++id) {
+        const Body& b = c->bodies[id];
+        if (b.present && b.moving && b.ms.mapped_step != c->step) moved.push_back(id);
+      }
+      if (!moved.empty() && !c->dbg) {
+        st = remap(c, moved, c->step);
+        if (st != PSM_OK) return st;
+      }
+      if (ahead) CUDA_TRY(c, cudaEventRecord(c->ev_coll, c->st));  // spare buffer is free
     }
-    if (!moved.empty() && !c->dbg) {
-      st = remap(c, moved, c->step);
+    if (ahead && k + 1 < n) {
+      st = remap_ahead(c, c->step + 1);
       if (st != PSM_OK) return st;
     }
     // 2. fused PSM stream-collide (Eq.(4)) + F/T partials
@@ -1316,6 +1416,8 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
     if (k == n - 1 || any_dyn)
       CUDA_TRY(c, cudaMemsetAsync(c->overflow, 0, (kMaxBodies + 1) * kSlotVals * 8, c->st));
     fill_kin(c, p, c->step);
+    p.word = c->word;  // the active buffer (the pipeline swaps buffers between steps)
+    p.tile_flag = c->tile_flag;
     p.step = c->step;
     int pat = 0;
     if (c->opt.pattern == PSM_TWO_ARRAY) {
@@ -1360,6 +1462,7 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
       CUDA_TRY(c, cudaStreamWaitEvent(c->st, c->ev_halo, 0));
       c->cur ^= 1;
     }
+    if (ahead) CUDA_TRY(c, cudaEventRecord(c->ev_coll, c->st));  // this buffer read: done
     c->step += 1;
     // 4. two-way coupling: this step's force/torque drives the dynamic bodies' next pose
     if (any_dyn && !c->dbg) {
@@ -1465,6 +1568,7 @@ psm_status psm_debug_set_fields(psm_ctx* c, const double* B, const double* us,
   psm_status st = ensure_mem(c);
   if (st != PSM_OK) return st;
   const size_t N = (size_t)c->ncell_local;
+  c->alt_valid = false;
   if (!c->dbg_B) {
     CUDA_TRY(c, cudaMalloc(&c->dbg_B, N * 8));
     CUDA_TRY(c, cudaMalloc(&c->dbg_us, 3 * N * 8));

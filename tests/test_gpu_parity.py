@@ -481,3 +481,46 @@ def test_open_x_only_periodic_yz(prec):
                      40, 41, u0=(0.05, 0.0, 0.0), ft_every=(prec == "f64"),
                      ft_rel=FT_REL if prec == "f64" else 1e-4, open_bc=OPEN)
     assert np.max(np.abs(o.pdfs() - g.pdfs())) <= (F64_TOL if prec == "f64" else F32_TOL)
+
+
+def test_remap_ahead_pipeline_equals_stepwise():
+    """psm_step(n > 1) remaps step k+1 into the spare word buffer while step k collides; the
+    result must be bitwise the same as n calls of psm_step(1) (no pipeline), including after
+    body changes that invalidate the spare buffer (set_body, remove_body) and a body crossing
+    the periodic boundary."""
+    v, tr = pi.propeller_mesh(n_blades=3, scale=0.09, n_st=8, n_pts=16, hub_seg=16)
+    kw = dict(nx=64, ny=40, nz=36, Q=19, tau=0.62, prec="f64", sc=1, bmode=1)
+    rho, u = pi.perturbed_flow((36, 40, 64), 61, u0=(0.03, 0.0, 0.01))
+    sims = [_sim(**kw), _sim(**kw)]
+    for s in sims:
+        s.init_equilibrium(rho, u)
+        s.set_mesh(1, v, tr, 1, pi.rotation_about([0, 1, 1], 0.3), (20.0, 20.0, 18.0),
+                   (0.02, 0.0, 0.0), (0.03, 0.0, 0.01))
+        s.set_sphere(2, 4.5, 2, np.eye(3), (50.0, 20.0, 1.0), (0.0, 0.05, -0.1))
+    a, b = sims
+
+    def run(n):
+        a.step(n)
+        for _ in range(n):
+            b.step(1)
+        assert np.array_equal(a.pdfs(), b.pdfs())
+        for i in range(3):
+            assert np.array_equal(a.fractions()[i], b.fractions()[i])
+        for bid in (1, 2):
+            if bid in present:
+                for x, y in zip(a.force_torque(bid), b.force_torque(bid)):
+                    assert np.array_equal(x, y)
+
+    present = {1, 2}
+    run(7)
+    for s in sims:  # new pose/velocity of the sphere: the spare buffer is stale
+        s.set_sphere(2, 4.5, 2, np.eye(3), (40.0, 30.0, 30.0), (0.1, 0.0, 0.0))
+    run(5)
+    for s in sims:
+        s.remove_body(1)
+    present = {2}
+    run(4)
+    for s in sims:
+        s.set_mesh(3, v, tr, 1, np.eye(3), (15.0, 15.0, 15.0), (0.0, 0.0, 0.0), (0.0, 0.02, 0.0))
+    present = {2, 3}
+    run(6)
