@@ -156,18 +156,21 @@ def profiles_traffic(workload: str):
 
 
 # ------------------------------------------------------------------------ CPU oracle leg ---
-def oracle_sample(wl: dict, steps: int, budget_s: float, seed: int):
+def oracle_sample(wl: dict, steps, budget_s: float, seed: int, warmup: int = 0):
     """Time the CPU oracle (as it stands) on a bounded sub-box of the same workload: same
-    stencil/tau/operator, bodies scaled with the box, moving, remapped every step."""
+    stencil/tau/operator, bodies scaled with the box, moving, remapped every step.  `warmup`
+    untimed steps first; steps=None sizes the timed steps to about `budget_s` seconds."""
     import oracle
     import psm_inputs as pi
     cores = os.cpu_count() or 1
-    # oracle throughput is ~0.6 MLUPS per core for D3Q19; size the box for the budget
+    # oracle throughput is ~0.6-1 MLUPS per core for D3Q19; size the box for the budget
     est = 0.6e6 * cores * (19.0 / wl["Q"])
-    cells = max(32 ** 3, min(256 ** 3, int(budget_s * est / max(1, steps))))
+    per_step = budget_s / max(1, steps or 10)
+    cells = max(32 ** 3, min(256 ** 3, int(per_step * est)))
     n = max(32, int(round(cells ** (1 / 3) / 16)) * 16)
     scale = n / wl["nx"]
     o = oracle.Oracle(n, n, n, wl["Q"], wl["tau"], (0, 0, 0), wl["sc"], wl["bmode"])
+    o.set_collision(wl.get("collision", "srt"))
     rho, u = pi.perturbed_flow((n, n, n), seed, u0=(0.02, 0.0, 0.0), u_amp=0.001)
     o.init_equilibrium(rho, u)
     if wl.get("rotors"):
@@ -183,8 +186,8 @@ def oracle_sample(wl: dict, steps: int, budget_s: float, seed: int):
         o.set_sphere(1, max(2.0, wl["r"] * scale), wl["s"])
         bodies = [(1, None, None)]
         what = f"sphere r={max(2.0, wl['r'] * scale):g}"
-    t0 = time.perf_counter()
-    for k in range(steps):
+
+    def one(k):
         for bid, pos, w in bodies:
             if pos is None:
                 o.set_pose(1, np.eye(3), (n / 2 + k * wl["v"][0], n / 2, n / 2), wl["v"])
@@ -193,21 +196,37 @@ def oracle_sample(wl: dict, steps: int, budget_s: float, seed: int):
                 o.set_pose(bid, Qk, pos, (0, 0, 0), w)
         o.map()
         o.step(1)
+
+    k = 0
+    t_w = time.perf_counter()
+    for _ in range(max(warmup, 0 if steps else 1)):
+        one(k)
+        k += 1
+    if steps is None:  # size the timed run from the measured warm-up step
+        t1 = (time.perf_counter() - t_w) / max(1, k)
+        steps = int(min(200, max(2, budget_s / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one(k)
+        k += 1
     dt = time.perf_counter() - t0
     mlups = n ** 3 * steps / dt / 1e6
     sample = (f"oracle fp64 on a {n}^3 periodic sub-box of {wl['desc'].split(':')[0]} "
               f"({what}, scaled by {scale:g}, moving, remap+collide every step), "
-              f"{steps} steps, {dt:.1f} s")
-    return {"value": mlups, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+              f"{steps} timed steps after {k - steps} untimed, {dt:.1f} s")
+    return {"value": mlups, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+            "ms_per_step": 1e3 * dt / steps}
 
 
 def run_reference(args, wl, rank, world):
     if rank != 0:
         return 0
     per_step_budget = 150.0 / max(1, args.steps + args.warmup)
-    cb = oracle_sample(wl, max(1, args.steps), per_step_budget * args.steps, 7)
+    cb = oracle_sample(wl, max(1, args.steps), per_step_budget * args.steps, 7,
+                       warmup=args.warmup)
+    ms = cb.pop("ms_per_step")
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong" if wl.get("strong") else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": workload_config(wl, world),
@@ -416,7 +435,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_sample(wl, 2, 20.0, 7)
+        cpu = oracle_sample(wl, None, 12.0, 7)
+        cpu.pop("ms_per_step", None)
 
     if rank == 0:
         line = {
