@@ -438,13 +438,19 @@ def main():
         cpu = oracle_sample(wl, None, 12.0, 7)
         cpu.pop("ms_per_step", None)
 
+    halo_cfg = {}
+    if world > 1:
+        hm = psm.psm_halo_mode(sim.ctx)
+        halo_cfg = {"parallelism": f"z-slab x{world} + " + (
+            "fused halo (k_collide stores into the neighbours' ghost planes over NVLink)"
+            if hm == 2 else "NCCL send/recv halo")}
     if rank == 0:
         line = {
             "metric": METRIC, "value": mlups, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong" if wl.get("strong") else "weak",
             "vs_baseline": None, "dtype": wl["prec"], "data": "synthetic",
-            "config": workload_config(wl, world),
+            "config": dict(workload_config(wl, world), **halo_cfg),
             "mlups_per_gpu": mlups / world,
             "roofline_frac_step": step_gbs / peak,
             "roofline": {"bound": "hbm", "kernel": "k_collide (fused PSM stream-collide)",

@@ -254,6 +254,13 @@ psm_status psm_profile(psm_ctx* ctx, int32_t enable);
 psm_status psm_profile_read(psm_ctx* ctx, double ms[PSM_NUM_PHASES],
                             int64_t count[PSM_NUM_PHASES]);
 
+/* How the z halo moves between ranks (world > 1, decided collectively at the first psm_step):
+ * 0 = single rank, 1 = NCCL grouped send/recv after the collide, 2 = fused: the collide kernel
+ * stores the outgoing populations straight into the neighbours' ghost planes (peer memory over
+ * NVLink, CUDA IPC), with a per-step flag handshake.  2 needs peer access between every pair of
+ * neighbours and PSM_TWO_ARRAY; the environment variable PSM_HALO=nccl forces 1. */
+psm_status psm_halo_mode(const psm_ctx* ctx, int32_t* mode);
+
 /* Size of an ncclUniqueId (128) and a fresh one for rank 0 to broadcast (world > 1). */
 int32_t psm_nccl_id_bytes(void);
 psm_status psm_nccl_get_unique_id(void* out128);

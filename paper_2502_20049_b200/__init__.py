@@ -44,6 +44,7 @@ EXPORTED = (
     "psm_get_body_state", "psm_map_fractions", "psm_step", "psm_force_torque",
     "psm_read_fractions", "psm_debug_set_fields", "psm_get_step", "psm_launch_count",
     "psm_profile", "psm_profile_read", "psm_nccl_id_bytes", "psm_nccl_get_unique_id",
+    "psm_halo_mode",
     "psm_last_error",
 )
 
@@ -113,7 +114,7 @@ def load(build_if_missing: bool = True):
         "psm_force_torque": [P, I32, P, P, P, P], "psm_read_fractions": [P, P, P, P],
         "psm_debug_set_fields": [P, P, P, P], "psm_get_step": [P, P],
         "psm_launch_count": [P, P], "psm_profile": [P, I32], "psm_profile_read": [P, P, P],
-        "psm_nccl_get_unique_id": [P],
+        "psm_nccl_get_unique_id": [P], "psm_halo_mode": [P, P],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -259,6 +260,14 @@ def psm_launch_count(ctx) -> int:
     n = C.c_int64()
     _check(load().psm_launch_count(ctx, C.byref(n)), ctx)
     return n.value
+
+
+def psm_halo_mode(ctx) -> int:
+    """0 single rank, 1 NCCL send/recv halo, 2 fused peer-store halo (decided at the first
+    psm_step of a multi-rank context)."""
+    m = C.c_int32()
+    _check(load().psm_halo_mode(ctx, C.byref(m)), ctx)
+    return m.value
 
 
 def psm_get_step(ctx) -> int:

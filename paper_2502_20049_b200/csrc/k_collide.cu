@@ -580,6 +580,22 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
     tile_partial_reduce(myid, v, p.partial + (size_t)tile * 2 * (1 + kSlotVals), p.overflow);
   }
 
+  // ---- fused halo: the populations leaving the slab through z go straight into the
+  // neighbours' ghost planes (peer stores over NVLink), replacing the separate exchange ----
+  if (act && p.p2p) {
+    const int pl = yc * nx + xc;
+    if (z == G.nzl - 1) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (stc_z(q) > 0 && p.gup[q]) static_cast<T*>(p.gup[q])[pl] = f[q];
+    }
+    if (z == 0) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (stc_z(q) < 0 && p.gdn[q]) static_cast<T*>(p.gdn[q])[pl] = f[q];
+    }
+  }
+
   // ---- scatter ----
   if (act) {
 #pragma unroll
@@ -684,6 +700,49 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
     if (walls) k_collide<Q, T, 2, true, false, false, 0><<<grid, block, 0, st>>>(p);
     else k_collide<Q, T, 2, false, false, false, 0><<<grid, block, 0, st>>>(p);
   }
+  return cudaGetLastError();
+}
+
+// ---- fused-halo step handshake between neighbouring ranks (peer memory) ----
+// signal: after this rank's collide (stream order: its peer stores are complete), publish the
+// step count into each neighbour's flag word with system-scope release semantics
+__global__ void k_p2p_signal(unsigned long long* up_flag, unsigned long long* dn_flag,
+                             unsigned long long v) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  if (up_flag) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(up_flag), "l"(v) : "memory");
+  if (dn_flag) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dn_flag), "l"(v) : "memory");
+}
+
+// wait: before the next collide reads the ghost planes (and overwrites the neighbours' other
+// array), both neighbours must have signalled step v; bounded spin (2 s) so a lost peer cannot
+// hang the device — then the error word records it and the step fails
+__global__ void k_p2p_wait(const unsigned long long* from_dn, const unsigned long long* from_up,
+                           unsigned long long v, unsigned long long* err) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long a = v, b = v;
+    if (from_dn) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(from_dn) : "memory");
+    if (from_up) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(b) : "l"(from_up) : "memory");
+    if (a >= v && b >= v) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 2000000000ull) {
+      atomicExch(err, 1ull);  // the host turns this into PSM_E_NCCL
+      return;
+    }
+    __nanosleep(200);
+  }
+}
+
+cudaError_t launch_p2p_signal(unsigned long long* up_flag, unsigned long long* dn_flag,
+                              unsigned long long v, cudaStream_t st) {
+  k_p2p_signal<<<1, 1, 0, st>>>(up_flag, dn_flag, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_wait(const unsigned long long* from_dn, const unsigned long long* from_up,
+                            unsigned long long v, unsigned long long* err, cudaStream_t st) {
+  k_p2p_wait<<<1, 1, 0, st>>>(from_dn, from_up, v, err);
   return cudaGetLastError();
 }
 

@@ -124,6 +124,18 @@ struct psm_ctx {
   ncclComm_t comm = nullptr;
   cudaStream_t comm_st = nullptr;     // halo stream (overlaps the interior collide)
   cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
+  // fused peer-store halo (psm_halo_mode 2)
+  bool p2p_checked = false, p2p = false;
+  bool has_up = false, has_dn = false;
+  void* ipc_up = nullptr;            // opened IPC base of the upper / lower neighbour's memory
+  void* ipc_dn = nullptr;
+  char* up_A[2] = {nullptr, nullptr};
+  char* dn_A[2] = {nullptr, nullptr};
+  int64_t up_qs = 0, dn_qs = 0, dn_nzl = 0;
+  unsigned long long* up_flag = nullptr;  // the upper neighbour's "from below" flag word
+  unsigned long long* dn_flag = nullptr;  // the lower neighbour's "from above" flag word
+  unsigned long long* flags = nullptr;    // mine: [0] from below, [1] from above, [2] hs error
+  unsigned long long epoch = 0;
   unsigned char nccl_id[128] = {};
   std::string err_msg;
   int64_t launches = 0;
@@ -323,7 +335,7 @@ static cudaError_t record(psm_ctx* c, int phase, int which, cudaStream_t s = nul
 // ------------------------------------------------------------------------- memory plan -----
 struct Plan {
   size_t off_A0, off_A1, off_word, off_flag, off_word_alt, off_flag_alt, off_partial, off_overflow, off_err, off_scratch,
-      off_ftout, off_ids, off_stage, stage_bytes, total;
+      off_ftout, off_ids, off_stage, off_flags, stage_bytes, total;
   size_t off_rcnt, off_rtiles, off_rsegs, off_rsegq, off_rband, off_rbandcnt;
   int seg_cap, band_cap;
 };
@@ -351,6 +363,7 @@ static Plan make_plan(const psm_ctx* c) {
   p.off_scratch = take((size_t)kFtChunks * kMaxBodies * kSlotVals * 8);
   p.off_ftout = take(kMaxBodies * kSlotVals * 8);
   p.off_ids = take(kMaxBodies * 4);
+  p.off_flags = take(64);
   // narrow-band remap lists (k_remap.cu); overflow is handled in-kernel (serial fallback)
   p.seg_cap = (int)std::min<int64_t>(32 * c->ntiles, 1 << 22);
   p.band_cap = (int)std::min<int64_t>(c->ncell_local, 1 << 23);
@@ -399,6 +412,7 @@ static psm_status bind(psm_ctx* c, void* mem, size_t bytes) {
   c->ft_scratch = reinterpret_cast<double*>(m + p.off_scratch);
   c->ft_out = reinterpret_cast<double*>(m + p.off_ftout);
   c->ft_ids = reinterpret_cast<int*>(m + p.off_ids);
+  c->flags = reinterpret_cast<unsigned long long*>(m + p.off_flags);
   c->stage = reinterpret_cast<double*>(m + p.off_stage);
   c->r_counters = reinterpret_cast<int*>(m + p.off_rcnt);
   c->r_tiles = reinterpret_cast<int*>(m + p.off_rtiles);
@@ -413,6 +427,7 @@ static psm_status bind(psm_ctx* c, void* mem, size_t bytes) {
   CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->st));
   CUDA_TRY(c, cudaMemsetAsync(c->overflow, 0, (kMaxBodies + 1) * kSlotVals * 8, c->st));
   CUDA_TRY(c, cudaMemsetAsync(c->err, 0xFF, 8, c->st));
+  CUDA_TRY(c, cudaMemsetAsync(c->flags, 0, 64, c->st));
   c->bound = true;
   return PSM_OK;
 }
@@ -1001,6 +1016,8 @@ psm_status psm_destroy(psm_ctx* c) {
       cudaEventDestroy(e[0]);
       cudaEventDestroy(e[1]);
     }
+  if (c->ipc_up) cudaIpcCloseMemHandle(c->ipc_up);
+  if (c->ipc_dn && c->ipc_dn != c->ipc_up) cudaIpcCloseMemHandle(c->ipc_dn);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_st) cudaStreamDestroy(c->comm_st);
   if (c->ev_bnd) cudaEventDestroy(c->ev_bnd);
@@ -1308,6 +1325,120 @@ psm_status psm_map_fractions(psm_ctx* c) {
   return remap(c, ids, c->step);
 }
 
+// Fused halo setup (collective over the ranks, once): exchange CUDA IPC handles of every rank's
+// device memory through NCCL, check peer access to both z neighbours on every rank, open the
+// neighbours' memory.  Any failure anywhere keeps the NCCL send/recv halo on all ranks.
+struct P2PInfo {
+  cudaIpcMemHandle_t h;
+  unsigned long long off_A0, off_A1, off_flags;
+  long long nzl, qstride;
+  int dev, ok;
+};
+
+static psm_status ensure_p2p(psm_ctx* c) {
+  if (c->p2p_checked) return PSM_OK;
+  c->p2p_checked = true;
+  if (c->world == 1 || c->opt.pattern != PSM_TWO_ARRAY) return PSM_OK;
+  const char* env = std::getenv("PSM_HALO");
+  const bool want = !(env && std::strcmp(env, "nccl") == 0);
+  const int P = c->world, r = c->rank;
+  const bool zwall = c->grid.bc[2] == PSM_WALL;
+  const int up = (r + 1) % P, dn = (r - 1 + P) % P;
+  c->has_up = !(zwall && r == P - 1);
+  c->has_dn = !(zwall && r == 0);
+  P2PInfo mine;
+  std::memset(&mine, 0, sizeof(mine));
+  CUDA_TRY(c, cudaGetDevice(&mine.dev));
+  // base of the allocation that holds the context memory (it may be a sub-block of a caller's
+  // allocation, psm_bind_memory): driver cuMemGetAddressRange through the runtime entry point
+  unsigned long long base = 0;
+  size_t size = 0;
+  typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (want && cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) ==
+                  cudaSuccess && fn && q == cudaDriverEntryPointSuccess &&
+      reinterpret_cast<GetRange>(fn)(&base, &size, (unsigned long long)c->mem) == 0 &&
+      cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)) == cudaSuccess) {
+    const unsigned long long m = (unsigned long long)c->mem;
+    mine.off_A0 = (unsigned long long)c->A[0] - base;
+    mine.off_A1 = (unsigned long long)c->A[1] - base;
+    mine.off_flags = (unsigned long long)c->flags - base;
+    (void)m;
+    mine.ok = 1;
+  }
+  cudaGetLastError();
+  mine.nzl = c->nzl;
+  mine.qstride = c->geom.qstride;
+  std::vector<P2PInfo> all(P);
+  char* d = nullptr;
+  CUDA_TRY(c, cudaMalloc(&d, sizeof(P2PInfo) * (P + 1)));
+  CUDA_TRY(c, cudaMemcpyAsync(d, &mine, sizeof(mine), cudaMemcpyHostToDevice, c->st));
+  NCCL_TRY(c, ncclAllGather(d, d + sizeof(P2PInfo), sizeof(P2PInfo), ncclChar, c->comm, c->st));
+  CUDA_TRY(c, cudaMemcpyAsync(all.data(), d + sizeof(P2PInfo), sizeof(P2PInfo) * P,
+                              cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  // every rank must be able to reach both its neighbours
+  int ok = 1;
+  for (int k = 0; k < P; ++k) ok &= all[k].ok;
+  if (ok) {
+    for (int nb : {up, dn}) {
+      if (nb == r) continue;
+      int can = 0;
+      if (all[nb].dev == mine.dev) can = 1;  // same device (two ranks on one GPU): IPC works
+      else if (cudaDeviceCanAccessPeer(&can, mine.dev, all[nb].dev) != cudaSuccess) can = 0;
+      ok &= can;
+    }
+  }
+  int* dok = reinterpret_cast<int*>(d);
+  CUDA_TRY(c, cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, c->st));
+  NCCL_TRY(c, ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->comm, c->st));
+  CUDA_TRY(c, cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  cudaFree(d);
+  if (!ok || up == r) return PSM_OK;
+  auto open = [&](int nb, void** out) -> bool {
+    if (cudaIpcOpenMemHandle(out, all[nb].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      *out = nullptr;
+      return false;
+    }
+    return true;
+  };
+  bool good = true;
+  if (c->has_up) good &= open(up, &c->ipc_up);
+  if (c->has_dn) {
+    if (dn == up && c->has_up) c->ipc_dn = c->ipc_up;
+    else good &= open(dn, &c->ipc_dn);
+  }
+  // all ranks must agree again (an open can fail)
+  int g = good ? 1 : 0;
+  CUDA_TRY(c, cudaMalloc(&dok, sizeof(int)));
+  CUDA_TRY(c, cudaMemcpyAsync(dok, &g, sizeof(int), cudaMemcpyHostToDevice, c->st));
+  NCCL_TRY(c, ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->comm, c->st));
+  CUDA_TRY(c, cudaMemcpyAsync(&g, dok, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  cudaFree(dok);
+  if (!g) return PSM_OK;  // (opened handles are closed in psm_destroy)
+  if (c->has_up) {
+    char* b = static_cast<char*>(c->ipc_up);
+    c->up_A[0] = b + all[up].off_A0;
+    c->up_A[1] = b + all[up].off_A1;
+    c->up_qs = all[up].qstride;
+    c->up_flag = reinterpret_cast<unsigned long long*>(b + all[up].off_flags) + 0;
+  }
+  if (c->has_dn) {
+    char* b = static_cast<char*>(c->ipc_dn);
+    c->dn_A[0] = b + all[dn].off_A0;
+    c->dn_A[1] = b + all[dn].off_A1;
+    c->dn_qs = all[dn].qstride;
+    c->dn_nzl = all[dn].nzl;
+    c->dn_flag = reinterpret_cast<unsigned long long*>(b + all[dn].off_flags) + 1;
+  }
+  c->p2p = true;
+  return PSM_OK;
+}
+
 // Remap-ahead (prescribed motion only): enqueue the remap for step `next` into the spare buffer
 // on map_st, after the collide that last read that buffer (ev_coll); ev_map marks completion.
 // The remap is latency/ALU-bound and the collide HBM-bound, so the two overlap.
@@ -1381,6 +1512,10 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
     any_moving |= b.moving;
     any_dynamic |= b.dynamic;
   }
+  if (c->world > 1) {
+    st = ensure_p2p(c);
+    if (st != PSM_OK) return st;
+  }
   static const bool no_ahead = std::getenv("PSM_NO_REMAP_AHEAD") != nullptr;
   const bool ahead = n > 1 && any_moving && !any_dynamic && !c->dbg && !no_ahead;
   if (ahead) {
@@ -1429,7 +1564,34 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
       pat = (c->step & 1) ? 2 : 1;
     }
     const int gz = c->geom.gz;
-    if (c->world == 1 || gz < 3) {
+    if (c->p2p) {
+      // fused halo: wait for both neighbours' previous step, one launch over all tile layers
+      // whose z-boundary cells also store into the neighbours' ghost planes, then signal
+      if (c->epoch > 0)
+        CUDA_TRY(c, launch_p2p_wait(c->has_dn ? c->flags + 0 : nullptr,
+                                    c->has_up ? c->flags + 1 : nullptr, c->epoch, c->flags + 2,
+                                    c->st));
+      const int d = c->cur ^ 1;
+      const size_t plane = (size_t)c->grid.nx * c->grid.ny;
+      p.p2p = 1;
+      for (int q = 0; q < c->Q; ++q) {
+        p.gup[q] = (stc_z(q) > 0 && c->has_up)
+                       ? (void*)(c->up_A[d] + (size_t)q * c->up_qs * c->S) : nullptr;
+        p.gdn[q] = (stc_z(q) < 0 && c->has_dn)
+                       ? (void*)(c->dn_A[d] + ((size_t)q * c->dn_qs +
+                                               (size_t)(c->dn_nzl + 1) * plane) * c->S)
+                       : nullptr;
+      }
+      if (record(c, 1, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+      p.tz0 = 0;
+      CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, gz, c->st));
+      if (record(c, 1, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
+      c->epoch += 1;
+      CUDA_TRY(c, launch_p2p_signal(c->has_up ? c->up_flag : nullptr,
+                                    c->has_dn ? c->dn_flag : nullptr, c->epoch, c->st));
+      c->launches += (c->epoch > 1) ? 3 : 2;
+      c->cur ^= 1;
+    } else if (c->world == 1 || gz < 3) {
       if (record(c, 1, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
       p.tz0 = 0;
       CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, gz, c->st));
@@ -1490,9 +1652,12 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
   unsigned long long* herr =
       reinterpret_cast<unsigned long long*>(c->pinned + (kMaxBodies + 1) * kSlotVals);
   CUDA_TRY(c, cudaMemcpyAsync(herr, c->err, 8, cudaMemcpyDeviceToHost, c->st));
+  if (c->p2p) CUDA_TRY(c, cudaMemcpyAsync(herr + 1, c->flags + 2, 8, cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
   (void)nb;
   ft_store(c, ids);
+  if (c->p2p && herr[1] != 0)
+    FAIL(c, PSM_E_NCCL, "fused halo: a neighbour did not signal its step within 2 s");
   if (*herr != ~0ull) {
     const long long ncell = (long long)c->grid.nx * c->grid.ny * c->grid.nz;
     const long long stp = (long long)(*herr / (unsigned long long)ncell);
@@ -1586,6 +1751,12 @@ psm_status psm_debug_set_fields(psm_ctx* c, const double* B, const double* us,
 psm_status psm_get_step(const psm_ctx* c, int64_t* step) {
   if (!c || !step) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null argument");
   *step = c->step;
+  return PSM_OK;
+}
+
+psm_status psm_halo_mode(const psm_ctx* c, int32_t* mode) {
+  if (!c || !mode) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null argument");
+  *mode = c->world == 1 ? 0 : (c->p2p ? 2 : 1);
   return PSM_OK;
 }
 

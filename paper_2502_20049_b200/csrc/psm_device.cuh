@@ -121,6 +121,12 @@ struct CollideParams {
   // q * qstride + offset product per load/store
   const void* srcq[27];
   void* dstq[27];
+  // fused halo (world > 1, peer memory over NVLink): plane bases of the neighbours' ghost planes
+  // in THEIR destination array, per direction (c_z = +1: upper neighbour's plane below its slab;
+  // c_z = -1: lower neighbour's plane above its slab); null where there is no such neighbour
+  int p2p;
+  void* gup[27];
+  void* gdn[27];
 };
 
 struct MapBox {

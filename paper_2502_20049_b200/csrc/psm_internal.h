@@ -13,6 +13,12 @@ namespace psm {
 cudaError_t launch_collide(int Q, bool fp64, const CollideParams& p, int pat, bool force,
                            bool dbg, int ntz, cudaStream_t st);
 
+// fused-halo handshake (k_collide.cu)
+cudaError_t launch_p2p_signal(unsigned long long* up_flag, unsigned long long* dn_flag,
+                              unsigned long long v, cudaStream_t st);
+cudaError_t launch_p2p_wait(const unsigned long long* from_dn, const unsigned long long* from_up,
+                            unsigned long long v, unsigned long long* err, cudaStream_t st);
+
 // k_map.cu (general boxes) and k_remap.cu (boxes holding one body)
 cudaError_t launch_map(const MapParams& p, cudaStream_t st);
 cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cudaStream_t st);

@@ -63,6 +63,8 @@ def main():
                 if not (np.all(np.abs(Fr - Fd) <= 1e-12 * np.maximum(np.abs(Fr), aF)) and
                         np.all(np.abs(Tr - Td) <= 1e-12 * np.maximum(np.abs(Tr), aT))):
                     failures.append(f"F/T body {b} {bc} Q{Q} {prec}: {Fr} {Fd} {Tr} {Td}")
+        if rank == 0:
+            print(f"halo mode {psm.psm_halo_mode(dsim.ctx)} ({bc} Q{Q} {prec})", flush=True)
         fr = ref.pdfs()[:, z0:z0 + nzl]
         fd = dsim.pdfs()
         if not np.array_equal(fr, fd):
