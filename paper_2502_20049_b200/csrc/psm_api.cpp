@@ -1141,15 +1141,77 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
         }
       }
       nb.rbound = rb;
-      std::vector<uint8_t> field, mask;
-      std::vector<unsigned long long> words;
-      voxelize_mesh(shape->verts, shape->nverts, shape->tris, shape->ntris, shape->s, nb.o,
-                    nb.dims, field);
-      pack_bricks(field, shape->s, nb.dims, words, mask, &nb.words);
-      CUDA_TRY(c, cudaMalloc(&nb.d_bits, words.size() * 8));
-      CUDA_TRY(c, cudaMalloc(&nb.d_mask, mask.size()));
-      CUDA_TRY(c, cudaMemcpy(nb.d_bits, words.data(), words.size() * 8, cudaMemcpyHostToDevice));
-      CUDA_TRY(c, cudaMemcpy(nb.d_mask, mask.data(), mask.size(), cudaMemcpyHostToDevice));
+      // geometry field (reading A15/A17): GPU voxeliser by default (k_voxelize.cu); the host
+      // implementation with PSM_VOXELIZE=host; PSM_VOXELIZE_CHECK=1 runs both and compares
+      const int sl = shape->s, n = 1 << sl;
+      const size_t nbk = (size_t)(nb.dims[0] * nb.dims[1] * nb.dims[2]);
+      nb.words = std::max(1, (n * n * n) / 64);
+      CUDA_TRY(c, cudaMalloc(&nb.d_bits, nbk * nb.words * 8));
+      CUDA_TRY(c, cudaMalloc(&nb.d_mask, nbk));
+      const char* vx = std::getenv("PSM_VOXELIZE");
+      const bool host_vox = vx && std::strcmp(vx, "host") == 0;
+      const bool check = std::getenv("PSM_VOXELIZE_CHECK") != nullptr;
+      if (!host_vox) {
+        std::vector<long long> V((size_t)(3 * shape->nverts));
+        const double sc = std::ldexp(1.0, sl + 12);
+        for (int64_t k = 0; k < shape->nverts; ++k)
+          for (int a = 0; a < 3; ++a)
+            V[3 * k + a] = std::llround((shape->verts[3 * k + a] - nb.o[a]) * sc);
+        VoxParams vp;
+        std::memset(&vp, 0, sizeof(vp));
+        vp.nt = shape->ntris;
+        vp.s = sl;
+        vp.bx = nb.dims[0];
+        vp.by = nb.dims[1];
+        vp.bz = nb.dims[2];
+        vp.NX = vp.bx << sl;
+        vp.NY = vp.by << sl;
+        vp.NZ = vp.bz << sl;
+        vp.W = nb.words;
+        vp.words = nb.d_bits;
+        vp.wpr = (vp.NX + 1 + 31) / 32;
+        long long* dV = nullptr;
+        int* dT = nullptr;
+        void* scratch = nullptr;
+        const size_t sbytes = voxelize_scratch_bytes(vp);
+        CUDA_TRY(c, cudaMalloc(&dV, V.size() * 8));
+        CUDA_TRY(c, cudaMalloc(&dT, (size_t)shape->ntris * 12));
+        CUDA_TRY(c, cudaMalloc(&scratch, sbytes));
+        CUDA_TRY(c, cudaMemcpyAsync(dV, V.data(), V.size() * 8, cudaMemcpyHostToDevice, c->st));
+        CUDA_TRY(c, cudaMemcpyAsync(dT, shape->tris, (size_t)shape->ntris * 12,
+                                    cudaMemcpyHostToDevice, c->st));
+        vp.V = dV;
+        vp.tris = dT;
+        CUDA_TRY(c, launch_voxelize(vp, scratch, nb.d_mask, c->st));
+        c->launches += 6 + 18 + 1;
+        CUDA_TRY(c, cudaStreamSynchronize(c->st));
+        cudaFree(dV);
+        cudaFree(dT);
+        cudaFree(scratch);
+      }
+      if (host_vox || check) {
+        std::vector<uint8_t> field, mask;
+        std::vector<unsigned long long> words;
+        voxelize_mesh(shape->verts, shape->nverts, shape->tris, shape->ntris, sl, nb.o,
+                      nb.dims, field);
+        int W = 0;
+        pack_bricks(field, sl, nb.dims, words, mask, &W);
+        if (host_vox) {
+          CUDA_TRY(c, cudaMemcpy(nb.d_bits, words.data(), words.size() * 8,
+                                 cudaMemcpyHostToDevice));
+          CUDA_TRY(c, cudaMemcpy(nb.d_mask, mask.data(), mask.size(), cudaMemcpyHostToDevice));
+        } else {
+          std::vector<unsigned long long> gw(words.size());
+          std::vector<uint8_t> gm(mask.size());
+          CUDA_TRY(c, cudaMemcpy(gw.data(), nb.d_bits, gw.size() * 8, cudaMemcpyDeviceToHost));
+          CUDA_TRY(c, cudaMemcpy(gm.data(), nb.d_mask, gm.size(), cudaMemcpyDeviceToHost));
+          if (gw != words || gm != mask) {
+            cudaFree(nb.d_bits);
+            cudaFree(nb.d_mask);
+            FAIL(c, PSM_E_STATE, "PSM_VOXELIZE_CHECK: GPU and host voxelisers differ");
+          }
+        }
+      }
     } else {
       FAIL(c, PSM_E_ARG, "unknown shape kind");
     }

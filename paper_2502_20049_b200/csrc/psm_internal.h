@@ -19,6 +19,22 @@ cudaError_t launch_p2p_signal(unsigned long long* up_flag, unsigned long long* d
 cudaError_t launch_p2p_wait(const unsigned long long* from_dn, const unsigned long long* from_up,
                             unsigned long long v, unsigned long long* err, cudaStream_t st);
 
+// k_voxelize.cu — GPU voxeliser (reading A15), writes the packed bricks and the brick flags
+struct VoxParams {
+  const long long* V;        // snapped vertices [nv][3], fixed point 2^-(s+12) from the origin
+  const int* tris;           // [nt][3]
+  long long nt;
+  int s;                     // super-sampling level: 2^s samples per LBM cell and axis
+  long long NX, NY, NZ;      // geometry cells (= LBM cells << s)
+  long long bx, by, bz;      // bricks (= LBM cells of the field)
+  int W;                     // uint64 words per brick
+  unsigned long long* words; // [bricks][W] output
+  unsigned* tog;             // scratch: toggle bits, wpr words per (gy, gz) row
+  long long wpr;
+};
+size_t voxelize_scratch_bytes(const VoxParams& p);
+cudaError_t launch_voxelize(VoxParams p, void* scratch, uint8_t* mask, cudaStream_t st);
+
 // k_map.cu (general boxes) and k_remap.cu (boxes holding one body)
 cudaError_t launch_map(const MapParams& p, cudaStream_t st);
 cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cudaStream_t st);

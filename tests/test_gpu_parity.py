@@ -524,3 +524,48 @@ def test_remap_ahead_pipeline_equals_stepwise():
         s.set_mesh(3, v, tr, 1, np.eye(3), (15.0, 15.0, 15.0), (0.0, 0.0, 0.0), (0.0, 0.02, 0.0))
     present = {2, 3}
     run(6)
+
+
+@pytest.mark.parametrize("s", [0, 1, 2, 3])
+def test_gpu_voxelizer_equals_host_bricks_and_flags(s, monkeypatch):
+    """The GPU voxeliser (k_voxelize.cu, default in psm_set_body) and the host implementation of
+    reading A15 produce identical brick words and early-out flags (PSM_VOXELIZE_CHECK compares
+    them inside the library), for a cube, a UV sphere, a propeller and the large CROR rotor."""
+    import time
+    import psm_inputs.meshgen as mg
+    monkeypatch.setenv("PSM_VOXELIZE_CHECK", "1")
+    meshes = [pi.box_mesh([-5.3, -4.1, -6.2], [5.7, 4.9, 3.3]),
+              mg.uv_sphere_mesh(7.3, 24, 16),
+              pi.propeller_mesh(n_blades=5, scale=0.15, n_st=12, n_pts=16, hub_seg=24)]
+    g = _sim(nx=64, ny=64, nz=64, Q=19, prec="f32")
+    for k, (v, tr) in enumerate(meshes):
+        g.set_mesh(1, v, tr, s, pi.rotation_about([1, 2, 3], 0.4), (32.0, 31.0, 30.5))
+        g.remove_body(1)
+    g.close()
+    if s <= 2:  # the ~0.6 M-face rotor (tip radius 200 cells) in a grid that holds it
+        v, tr = pi.cror_rotor(True)
+        g = _sim(nx=448, ny=448, nz=448, Q=19, prec="f32")
+        t0 = time.perf_counter()
+        g.set_mesh(1, v, tr, s, np.eye(3), (224.0, 224.0, 224.0))
+        print(f"CROR rotor s={s}: GPU + host voxelisation and compare {time.perf_counter() - t0:.2f} s")
+        g.close()
+
+
+def test_gpu_voxelizer_speed_large_rotor(monkeypatch):
+    """Setup cost of the ~0.6 M-face rotor at s = 3 (7.7e9 geometry cells): GPU vs host."""
+    import time
+    v, tr = pi.cror_rotor(True)
+    g = _sim(nx=448, ny=448, nz=448, Q=19, prec="f32")
+    t0 = time.perf_counter()
+    g.set_mesh(1, v, tr, 3, np.eye(3), (224.0, 224.0, 224.0))
+    t_gpu = time.perf_counter() - t0
+    _, _, cnt_gpu = g.fractions()
+    g.remove_body(1)
+    monkeypatch.setenv("PSM_VOXELIZE", "host")
+    t0 = time.perf_counter()
+    g.set_mesh(1, v, tr, 3, np.eye(3), (224.0, 224.0, 224.0))
+    t_host = time.perf_counter() - t0
+    _, _, cnt_host = g.fractions()
+    print(f"set_mesh s=3, {len(tr)} faces: GPU voxeliser {t_gpu:.2f} s, host {t_host:.2f} s")
+    assert np.array_equal(cnt_gpu, cnt_host)
+    g.close()
