@@ -59,6 +59,18 @@ WORKLOADS = {
                v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
                desc="c4: D3Q19 PSM fp32 512^3/GPU periodic, sphere r=64 translating "
                     "v=(1/32,0,0), s=1, remapped every step, SC1, weighted B"),
+    # NEXT-row workloads: TRT fluid operator, two-way coupled sphere, paper-literal R2 mapping
+    "c4trt": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.6, r=64.0, s=1,
+                  v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1, collision="trt",
+                  desc="c4 TRT: D3Q19 PSM fp32 512^3, moving sphere r=64, s=1, TRT (magic 3/16)"),
+    "c4dyn": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.6, r=64.0, s=1,
+                  v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
+                  dynamic=(2.0, -1e-5),
+                  desc="c4 two-way coupled: D3Q19 PSM fp32 512^3, sphere r=64 (density ratio 2, "
+                       "gravity -1e-5 x) integrated from its own force/torque every step"),
+    "c5wr2": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.55, rotors=True, s=1,
+                  omega=0.05 / 220.0, pattern="two_array", sc=1, bmode=1, mapping="R2",
+                  desc="c5 weak with the paper-literal centre-only mapping R2 (A12)"),
     "c4aa": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.6, r=64.0, s=1,
                  v=(1.0 / 32.0, 0.0, 0.0), pattern="aa", sc=1, bmode=1,
                  desc="c4 (AA pattern): D3Q19 PSM fp32 512^3, moving sphere r=64, s=1"),
@@ -275,13 +287,21 @@ def build_workload(psm, wl: dict, rank: int, world: int, nccl_id=None):
                                          n_st=200, n_pts=128, hub_seg=256)
                 w = (wl["omega"] if front else -wl["omega"], 0.0, 0.0)
                 tpos = (wl.get("rotor_x", (200.0, 330.0))[k], ny / 2, zc)
-                sim.set_mesh(1 + 2 * r + k, v, t, wl["s"], np.eye(3), tpos, (0, 0, 0), w)
+                sim.set_mesh(1 + 2 * r + k, v, t, wl["s"], np.eye(3), tpos, (0, 0, 0), w,
+                             mapping=wl.get("mapping", "R1"))
                 body_poses.append((np.eye(3), tpos, (0.0, 0.0, 0.0), w))
                 nbodies += 1
         else:
             sim.set_sphere(1 + r, wl["r"], wl["s"], np.eye(3), (nx / 2, ny / 2, zc), wl["v"])
             body_poses.append((np.eye(3), (nx / 2, ny / 2, zc), wl["v"], (0.0, 0.0, 0.0)))
             nbodies += 1
+            if wl.get("dynamic"):
+                # two-way coupled (NEXT rank 1): density ratio rho_s/rho_f, gravity along -x
+                ratio, gx = wl["dynamic"]
+                vol = 4.0 / 3.0 * np.pi * wl["r"] ** 3
+                m = ratio * vol
+                sim.set_dynamics(1 + r, m, 0.4 * m * wl["r"] ** 2 * np.eye(3),
+                                 ext_force=((m - vol) * gx, 0.0, 0.0))
     return sim, body_poses, nbodies, S
 
 
@@ -405,6 +425,8 @@ def main():
         t_b = time.perf_counter()
         for k in range(args.steps):
             for b, (Q0, t0, v, w) in enumerate(body_poses):
+                if wl.get("dynamic"):
+                    break  # the library integrates two-way coupled bodies itself
                 ang = k * math.sqrt(w[0] ** 2 + w[1] ** 2 + w[2] ** 2)
                 Qk = pi.rotation_about(w, ang) @ Q0 if ang else Q0
                 tk = tuple(t0[a] + k * v[a] for a in range(3))

@@ -48,6 +48,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-o", LIB + ".tmp"] + sources() + [
            "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
            "-Xlinker", "-rpath," + os.path.join(nccl, "lib"), "-lgomp"]
+    extra = os.environ.get("PSM_NVCC_EXTRA")  # tuning experiments only, e.g. -DPSM_CUM32_BLOCKS=4
+    if extra:
+        cmd[1:1] = extra.split()
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -315,7 +315,10 @@ template <int Q, typename T, int PAT, int COLL>
 constexpr int collide_min_blocks() {
   // the cumulant keeps a 3x3x3 moment array live (PSM cells stash f in shared memory instead of
   // registers): two fp64 blocks (a few spilled words), three fp32 blocks (AA odd: two)
-  if (COLL == 2) return sizeof(T) == 8 ? 2 : (PAT == 2 ? 2 : 3);
+#ifndef PSM_CUM32_BLOCKS
+#define PSM_CUM32_BLOCKS 3
+#endif
+  if (COLL == 2) return sizeof(T) == 8 ? 2 : (PAT == 2 ? 2 : PSM_CUM32_BLOCKS);
   // the AA odd step keeps the scatter offsets live as well: one block less for fp32
   return sizeof(T) == 8 ? 2 : (Q == 19 ? (PAT == 2 ? 3 : 4) : (PAT == 2 ? 2 : 3));
 }
@@ -641,13 +644,15 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
   const bool walls = p.g.wall[0] || p.g.wall[1] || p.g.wall[2];
   const bool xonly = p.g.wall[0] && !p.g.wall[1] && !p.g.wall[2];  // e.g. open x faces
   if (p.trt == 1) {
-    // TRT: the general (runtime wall flags) variants only
+    // TRT: periodic and x-only fast paths for the pull pattern, general variants otherwise
     if (dbg || force) {
       if (dbg && force) k_collide<Q, T, 0, true, true, true, 1><<<grid, block, 0, st>>>(p);
       else if (dbg) k_collide<Q, T, 0, true, false, true, 1><<<grid, block, 0, st>>>(p);
       else k_collide<Q, T, 0, true, true, false, 1><<<grid, block, 0, st>>>(p);
     } else if (pat == 0) {
-      k_collide<Q, T, 0, true, false, false, 1><<<grid, block, 0, st>>>(p);
+      if (!walls) k_collide<Q, T, 0, false, false, false, 1><<<grid, block, 0, st>>>(p);
+      else if (xonly) k_collide<Q, T, 0, 2, false, false, 1><<<grid, block, 0, st>>>(p);
+      else k_collide<Q, T, 0, true, false, false, 1><<<grid, block, 0, st>>>(p);
     } else if (pat == 1) {
       k_collide<Q, T, 1, false, false, false, 1><<<grid, block, 0, st>>>(p);
     } else {
