@@ -9,6 +9,9 @@
 //   L2  one thread per cell                : fp32 centre test against dilated-by-one bricks
 //   L3  one thread per narrow-band cell    : exact fp64 inside test of each sub-sample
 //                                            (reading R1, A14 order), count -> word
+// Cached band (margin = 1): L0-L2 decide with one cell of slack (radius-2 brick flags, widened
+// reaches), so their decisions hold for every pose within one cell of the build pose; until the
+// body has moved that far, a step re-runs only L3 over the cached band list.
 // Every early decision is conservative (it only claims "all sub-samples outside/inside" when the
 // brick flags prove it), so the words equal the brute-force counts bit for bit.  Tile flags ("any word nonzero") are
 // reset for every tile that reaches L1 and set by whichever level writes a nonzero word.
@@ -49,7 +52,7 @@ __global__ void k_remap_l0(const __grid_constant__ RemapParams r) {
   const double pt[3] = {tx * kTileX + 0.5 * kTileX, ty * kTileY + 0.5 * kTileY,
                         G.z0 + tz * kTileZ + 0.5 * kTileZ};
   double qt[3];
-  const int dec = tile_decision<kTileReach, 4, 8>(r.body, pt, L, G.wall, qt);
+  const int dec = tile_decision<kTileReach, 4, 8>(r.body, pt, L, G.wall, qt, r.margin);
   if (dec == 0 && r.tile_flag[tile] == 0) return;  // far outside and already all zero
   r.tile_flag[tile] = 0;
   const int k = atomicAdd(r.counters + 0, 1);
@@ -74,7 +77,7 @@ __global__ void k_remap_l1(const __grid_constant__ RemapParams r) {
     const int x0 = tx * kTileX + sx * kSubX;
     const double ps[3] = {x0 + 0.5 * kSubX, y + 0.5, G.z0 + z + 0.5};
     double qs[3];
-    const int dec = tile_decision<kSubReach, 16, 32>(b, ps, L, G.wall, qs);
+    const int dec = tile_decision<kSubReach, 16, 32>(b, ps, L, G.wall, qs, r.margin);
     if (dec == 2) {
       const int k = atomicAdd(r.counters + 1, 1);
       if (k < r.seg_cap) {
@@ -82,13 +85,19 @@ __global__ void k_remap_l1(const __grid_constant__ RemapParams r) {
         r.segq[k] = make_float4((float)qs[0], (float)qs[1], (float)qs[2], 0.f);
         continue;
       }
-      // list full: finish the segment here (exact, serial)
+      // list full: finish the segment here (exact, serial; a cached band gets its cells)
       for (int c = 0; c < kSubX; ++c) {
         if (x0 + c >= G.nx) continue;
         const float off = (float)c + 0.5f - 0.5f * kSubX;
         const float qc[3] = {(float)qs[0] + (float)b.Q[0] * off, (float)qs[1] + (float)b.Q[1] * off,
                              (float)qs[2] + (float)b.Q[2] * off};
-        const int cd = cell_decision(b, qc);
+        const int cd = cell_decision(b, qc, r.margin);
+        if (cd == 2 && r.margin) {  // the cached band holds every cell of the box: no overflow
+          const int k = atomicAdd(r.bandn, 1);
+          r.band[k] = ((uint32_t)tile << 8) | (uint32_t)(row * kTileX + sx * kSubX + c);
+          r.bandcnt[k] = 0;
+          continue;
+        }
         int cnt = cd == 1 ? (1 << (3 * b.s)) : 0;
         if (cd == 2) cnt = exact_count(b, x0 + c, y, G.z0 + z, L, G.wall);
         put_word(r, x0 + c, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
@@ -123,9 +132,9 @@ __global__ void k_remap_l2(const __grid_constant__ RemapParams r) {
     const float off = (float)c + 0.5f - 0.5f * kSubX;
     const float qc[3] = {q.x + (float)b.Q[0] * off, q.y + (float)b.Q[1] * off,
                          q.z + (float)b.Q[2] * off};
-    const int cd = cell_decision(b, qc);
+    const int cd = cell_decision(b, qc, r.margin);
     if (cd == 2) {
-      const int k = atomicAdd(r.counters + 2, 1);
+      const int k = atomicAdd(r.bandn, 1);
       if (k < r.band_cap) {
         r.band[k] = ((uint32_t)tile << 8) | (uint32_t)(row * kTileX + sx * kSubX + c);
         r.bandcnt[k] = 0;
@@ -155,7 +164,7 @@ __device__ __forceinline__ void band_cell(const RemapParams& r, uint32_t e, int&
 __global__ void k_remap_l3(const __grid_constant__ RemapParams r) {
   const Geom& G = r.g;
   const BodyGeo& b = r.body;
-  const int n = min(r.counters[2], r.band_cap);
+  const int n = min(*r.bandn, r.band_cap);
   const int nsamp = 1 << (3 * b.s);
   const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -202,7 +211,7 @@ __global__ void k_remap_l3(const __grid_constant__ RemapParams r) {
 __global__ void k_remap_l3_chunks(const __grid_constant__ RemapParams r) {
   const Geom& G = r.g;
   const BodyGeo& b = r.body;
-  const int n = min(r.counters[2], r.band_cap);
+  const int n = min(*r.bandn, r.band_cap);
   const int lch = 3 * b.s - 3;  // log2(chunks per cell)
   const long long items = (long long)n << lch;
   const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
@@ -230,30 +239,45 @@ __global__ void k_remap_l3_chunks(const __grid_constant__ RemapParams r) {
 }
 
 __global__ void k_remap_l4(const __grid_constant__ RemapParams r) {
-  const int n = min(r.counters[2], r.band_cap);
+  const int n = min(*r.bandn, r.band_cap);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     int x, y, z, tile;
     band_cell(r, r.band[k], x, y, z, tile);
     const int cnt = r.bandcnt[k];
+    r.bandcnt[k] = 0;  // ready for the next pass over a cached band
     put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
   }
 }
 
 }  // namespace
 
-cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cudaStream_t st) {
+// the exact pass alone over a cached band (poses within one cell of the band's build pose)
+cudaError_t launch_remap_band(const RemapParams& r, int persistent_blocks, cudaStream_t st,
+                              int threads) {
+  if (r.body.s >= 2 && r.body.mapping == 0) {
+    k_remap_l3_chunks<<<persistent_blocks, threads, 0, st>>>(r);
+    k_remap_l4<<<persistent_blocks, threads, 0, st>>>(r);
+  } else {
+    k_remap_l3<<<persistent_blocks, threads, 0, st>>>(r);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cudaStream_t st,
+                                int threads) {
   const int ntile = r.box.n[0] * r.box.n[1] * r.box.n[2];
   if (ntile <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(r.counters, 0, 4 * sizeof(int), st);
   if (e != cudaSuccess) return e;
+  // (a cached band's count is reset by the host once per rebuild, before the body's first box)
   k_remap_l0<<<(ntile + 255) / 256, 256, 0, st>>>(r);
-  k_remap_l1<<<persistent_blocks, 256, 0, st>>>(r);
-  k_remap_l2<<<persistent_blocks, 256, 0, st>>>(r);
+  k_remap_l1<<<persistent_blocks, threads, 0, st>>>(r);
+  k_remap_l2<<<persistent_blocks, threads, 0, st>>>(r);
   if (r.body.s >= 2 && r.body.mapping == 0) {
-    k_remap_l3_chunks<<<persistent_blocks, 256, 0, st>>>(r);
-    k_remap_l4<<<persistent_blocks, 256, 0, st>>>(r);
+    k_remap_l3_chunks<<<persistent_blocks, threads, 0, st>>>(r);
+    k_remap_l4<<<persistent_blocks, threads, 0, st>>>(r);
   } else {
-    k_remap_l3<<<persistent_blocks, 256, 0, st>>>(r);
+    k_remap_l3<<<persistent_blocks, threads, 0, st>>>(r);
   }
   return cudaGetLastError();
 }

@@ -14,7 +14,7 @@
 //                each run of 2^s samples of one brick is OR-ed into the brick's bit words
 //   k_vox_any    per brick: any sample inside / any sample outside
 //   k_box_pass   separable running-window OR (radius r along one axis, beyond the field = 0)
-//   k_vox_mask   the six early-out bits
+//   k_vox_mask   the eight early-out bits
 #include "psm_device.cuh"
 #include "psm_internal.h"
 
@@ -151,7 +151,8 @@ __global__ void k_box_pass(const uint8_t* v_in, uint8_t* v_out, long long n, lon
 
 __global__ void k_vox_mask(long long bx, long long by, long long bz, const uint8_t* in1,
                            const uint8_t* out1, const uint8_t* inK, const uint8_t* outK,
-                           const uint8_t* inS, const uint8_t* outS, uint8_t* mask) {
+                           const uint8_t* inS, const uint8_t* outS, const uint8_t* in2,
+                           const uint8_t* out2, uint8_t* mask) {
   const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= bx * by * bz) return;
   const long long ix = b % bx, iy = (b / bx) % by, iz = b / (bx * by);
@@ -166,6 +167,8 @@ __global__ void k_vox_mask(long long bx, long long by, long long bz, const uint8
   if (!outK[b] && inside_field(kTileReach)) m |= 8;
   if (!inS[b]) m |= 16;
   if (!outS[b] && inside_field(kSubReach)) m |= 32;
+  if (!in2[b]) m |= 64;
+  if (!out2[b] && inside_field(2)) m |= 128;
   mask[b] = m;
 }
 
@@ -184,7 +187,7 @@ static cudaError_t box_or_dev(uint8_t* v, uint8_t* tmp, long long bx, long long 
 
 size_t voxelize_scratch_bytes(const VoxParams& p) {
   const size_t nb = (size_t)(p.bx * p.by * p.bz);
-  return (size_t)(p.NY * p.NZ * p.wpr) * 4 + 8 * nb + 256;
+  return (size_t)(p.NY * p.NZ * p.wpr) * 4 + 10 * nb + 256;
 }
 
 cudaError_t launch_voxelize(VoxParams p, void* scratch, uint8_t* mask, cudaStream_t st) {
@@ -193,7 +196,7 @@ cudaError_t launch_voxelize(VoxParams p, void* scratch, uint8_t* mask, cudaStrea
   p.tog = reinterpret_cast<unsigned*>(sc);
   uint8_t* f = reinterpret_cast<uint8_t*>(sc + (size_t)(p.NY * p.NZ * p.wpr) * 4);
   uint8_t *in1 = f, *out1 = f + nb, *inK = f + 2 * nb, *outK = f + 3 * nb, *inS = f + 4 * nb,
-          *outS = f + 5 * nb, *tmp = f + 6 * nb;
+          *outS = f + 5 * nb, *in2 = f + 6 * nb, *out2 = f + 7 * nb, *tmp = f + 8 * nb;
   cudaError_t e = cudaMemsetAsync(p.tog, 0, (size_t)(p.NY * p.NZ * p.wpr) * 4, st);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(p.words, 0, nb * (size_t)p.W * 8, st);
@@ -208,15 +211,17 @@ cudaError_t launch_voxelize(VoxParams p, void* scratch, uint8_t* mask, cudaStrea
   if (e == cudaSuccess) e = cudaMemcpyAsync(outK, out1, nb, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(inS, in1, nb, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(outS, out1, nb, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(in2, in1, nb, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out2, out1, nb, cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return e;
-  uint8_t* fields[6] = {in1, out1, inK, outK, inS, outS};
-  const int radii[6] = {1, 1, kTileReach, kTileReach, kSubReach, kSubReach};
-  for (int k = 0; k < 6; ++k) {
+  uint8_t* fields[8] = {in1, out1, inK, outK, inS, outS, in2, out2};
+  const int radii[8] = {1, 1, kTileReach, kTileReach, kSubReach, kSubReach, 2, 2};
+  for (int k = 0; k < 8; ++k) {
     e = box_or_dev(fields[k], tmp, p.bx, p.by, p.bz, radii[k], st);
     if (e != cudaSuccess) return e;
   }
   k_vox_mask<<<(unsigned)((nb + T - 1) / T), T, 0, st>>>(p.bx, p.by, p.bz, in1, out1, inK, outK,
-                                                          inS, outS, mask);
+                                                          inS, outS, in2, out2, mask);
   return cudaGetLastError();
 }
 

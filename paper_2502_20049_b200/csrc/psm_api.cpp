@@ -34,6 +34,10 @@ struct MapState {
   int64_t mapped_step = -1;
   bool has_box = false;
   int64_t box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};  // mapped box (global, unwrapped)
+  // cached narrow band (k_remap.cu, margin 1): valid for poses within one cell of (Qrb, trb)
+  int slot = 0;        // which of the body's two band stores belongs to this word buffer
+  bool cache = false;
+  double Qrb[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, trb[3] = {0, 0, 0};
 };
 
 struct Body {
@@ -55,6 +59,13 @@ struct Body {
   // mapping state of the active solid-word buffer (ms) and of the spare one (alt, used by the
   // remap-ahead pipeline of psm_step; swapped together with the buffers)
   MapState ms, alt;
+  // band stores (device), indexed by MapState::slot; capacity in cells
+  uint32_t* cband[2] = {nullptr, nullptr};
+  int* ccnt[2] = {nullptr, nullptr};
+  int* cn[2] = {nullptr, nullptr};
+  size_t ccap[2] = {0, 0};
+  bool want_cache = false;  // transient: the current remap rebuilds this body's band
+  Body() { alt.slot = 1; }
   // two-way coupling: state advanced by the host integrator after every step
   bool dynamic = false;
   double mass = 0, Ib[9] = {0}, fext[3] = {0, 0, 0}, text[3] = {0, 0, 0};
@@ -95,6 +106,7 @@ struct psm_ctx {
   cudaStream_t map_st = nullptr;     // remap-ahead stream (high priority)
   cudaEvent_t ev_map = nullptr, ev_coll = nullptr;
   int ahead_blocks = 148;            // persistent remap blocks when overlapped with the collide
+  int ahead_threads = 256;
   double* partial = nullptr;
   double* overflow = nullptr;
   unsigned long long* err = nullptr;
@@ -170,6 +182,18 @@ static std::string g_last_error;
   } while (0)
 
 // ---------------------------------------------------------------------------- helpers ------
+static void free_bands(Body& b) {  // callers have synchronised the streams
+  for (int k = 0; k < 2; ++k) {
+    if (b.cband[k]) cudaFreeAsync(b.cband[k], 0);
+    if (b.ccnt[k]) cudaFreeAsync(b.ccnt[k], 0);
+    if (b.cn[k]) cudaFreeAsync(b.cn[k], 0);
+    b.cband[k] = nullptr;
+    b.ccnt[k] = nullptr;
+    b.cn[k] = nullptr;
+    b.ccap[k] = 0;
+  }
+}
+
 static void rodrigues(const double w[3], double n, const double Q0[9], double out[9]) {
   // Q_n = Rot(w/|w|, n|w|) Q_0 (A13: host libm sin/cos)
   const double wn = std::sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
@@ -660,6 +684,44 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
   mp.stats = dstats;
   if (record(c, 0, 0, c->mst) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
   static const bool force_general = std::getenv("PSM_REMAP_GENERAL") != nullptr;
+  // cached bands: bodies rebuilt in single-body boxes only; capacity = every cell of their boxes
+  size_t need[kMaxBodies + 1] = {};
+  int nsingle[kMaxBodies + 1] = {}, ngeneral[kMaxBodies + 1] = {};
+  for (size_t i = 0; i < tb.size(); ++i) {
+    const int pc = __builtin_popcount(tb[i].bodymask);
+    if (pc == 1 && !force_general) {
+      const int id = __builtin_ctz(tb[i].bodymask);
+      need[id] += (size_t)tb[i].n[0] * tb[i].n[1] * tb[i].n[2] * kTileCells;
+      nsingle[id] += 1;
+    } else {
+      for (int id = 1; id <= kMaxBodies; ++id)
+        if (tb[i].bodymask & (1u << id)) ngeneral[id] += 1;
+    }
+  }
+  for (int id = 1; id <= kMaxBodies; ++id) {
+    Body& bd = c->bodies[id];
+    if (ngeneral[id]) bd.ms.cache = false;  // shares a box with another body: no band cache
+    if (!bd.want_cache || ngeneral[id] || !nsingle[id]) {
+      bd.want_cache = false;
+      continue;
+    }
+    const int sl = bd.ms.slot;
+    if (bd.ccap[sl] < need[id]) {
+      // stream-ordered (no device-wide sync in the middle of a pipelined step), with headroom
+      // so that the slowly changing box of a moving body rarely regrows it
+      const size_t cap = need[id] + need[id] / 4;
+      if (bd.cband[sl]) CUDA_TRY(c, cudaFreeAsync(bd.cband[sl], c->mst));
+      if (bd.ccnt[sl]) CUDA_TRY(c, cudaFreeAsync(bd.ccnt[sl], c->mst));
+      bd.cband[sl] = nullptr;
+      bd.ccnt[sl] = nullptr;
+      bd.ccap[sl] = 0;
+      CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&bd.cband[sl]), cap * 4, c->mst));
+      CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&bd.ccnt[sl]), cap * 4, c->mst));
+      bd.ccap[sl] = cap;
+    }
+    if (!bd.cn[sl]) CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&bd.cn[sl]), sizeof(int), c->mst));
+    CUDA_TRY(c, cudaMemsetAsync(bd.cn[sl], 0, sizeof(int), c->mst));
+  }
   for (size_t i = 0; i < tb.size(); ++i) {
     if (__builtin_popcount(tb[i].bodymask) == 1 && !force_general) {
       // one body in the box: narrow-band pipeline (k_remap.cu)
@@ -677,9 +739,20 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
       r.segq = c->r_segq;
       r.band = c->r_band;
       r.bandcnt = c->r_bandcnt;
+      r.bandn = c->r_counters + 2;
       r.seg_cap = c->seg_cap;
       r.band_cap = c->band_cap;
-      CUDA_TRY(c, launch_remap_single(r, c->mst == c->st ? 148 * 8 : c->ahead_blocks, c->mst));
+      Body& bd = c->bodies[r.id];
+      if (bd.want_cache) {  // build the body's cached band (decisions with one cell of slack)
+        const int sl = bd.ms.slot;
+        r.margin = 1;
+        r.band = bd.cband[sl];
+        r.bandcnt = bd.ccnt[sl];
+        r.bandn = bd.cn[sl];
+        r.band_cap = (int)std::min<size_t>(bd.ccap[sl], (size_t)INT32_MAX);
+      }
+      CUDA_TRY(c, launch_remap_single(r, c->mst == c->st ? 148 * 8 : c->ahead_blocks, c->mst,
+                                      c->mst == c->st ? 256 : c->ahead_threads));
       c->launches += 4;
       continue;
     }
@@ -689,6 +762,14 @@ static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
     mp.ntiles = tb[i].n[0] * tb[i].n[1] * tb[i].n[2];
     CUDA_TRY(c, launch_map(mp, c->mst));
     c->launches += 1;
+  }
+  for (int id = 1; id <= kMaxBodies; ++id) {
+    Body& bd = c->bodies[id];
+    if (!bd.want_cache) continue;
+    bd.want_cache = false;
+    bd.ms.cache = true;
+    std::memcpy(bd.ms.Qrb, bd.ms.Qc, sizeof(bd.ms.Qrb));
+    std::memcpy(bd.ms.trb, bd.ms.tc, sizeof(bd.ms.trb));
   }
   if (record(c, 0, 1, c->mst) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
   if (dstats) {
@@ -721,9 +802,47 @@ static psm_status ensure_pipeline(psm_ctx* c) {
   return PSM_OK;
 }
 
-// remap the given bodies at the pose of `step` (or all present bodies if ids empty)
+// Upper bound on how far any point of body b moves between the band's build pose and (Q, t):
+// |mi(t - t_rb)| + r_bound * |Q - Q_rb|_F / sqrt(2)  (the chord of a rotation by theta is
+// 2 r sin(theta/2) = r |Q - Q_rb|_F / sqrt(2)).
+static double band_displacement(const psm_ctx* c, const Body& b, const double Q[9],
+                                 const double t[3]) {
+  double dt2 = 0.0, dq2 = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    double d = t[a] - b.ms.trb[a];
+    if (c->grid.bc[a] == PSM_PERIODIC) {
+      const double L = extent(c, a);
+      d -= L * std::nearbyint(d / L);
+    }
+    dt2 += d * d;
+  }
+  for (int k = 0; k < 9; ++k) dq2 += (Q[k] - b.ms.Qrb[k]) * (Q[k] - b.ms.Qrb[k]);
+  return std::sqrt(dt2) + b.rbound * std::sqrt(dq2 * 0.5);
+}
+
+static bool boxes_overlap(const psm_ctx* c, const Body& b, const std::vector<Box>& boxes) {
+  std::vector<Box> mine;
+  add_box(c, b.ms.box_lo, b.ms.box_hi, mine);
+  for (const Box& m : mine)
+    for (const Box& o : boxes) {
+      bool ov = true;
+      for (int a = 0; a < 3; ++a)
+        if (m.hi[a] <= o.lo[a] || m.lo[a] >= o.hi[a]) ov = false;
+      if (ov) return true;
+    }
+  return false;
+}
+
+// remap the given bodies at the pose of `step` (or all present bodies if ids empty).  A body with
+// a valid cached band that has moved less than one cell since the band was built (and whose box
+// no other remapped body touches) only re-runs the exact pass over its band.
 static psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
+  static const bool no_cache = [] {
+    const char* e = std::getenv("PSM_BAND_CACHE");
+    return e && std::strcmp(e, "0") == 0;
+  }();
   std::vector<Box> boxes;
+  std::vector<int> incr;
   for (int id : ids) {
     Body& b = c->bodies[id];
     if (!b.present) continue;
@@ -739,23 +858,85 @@ static psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
     }
     std::memcpy(b.ms.Qc, Q, sizeof(Q));
     std::memcpy(b.ms.tc, t, sizeof(t));
-    remap_region(c, b, Q, t, boxes);
     b.ms.mapped_step = step;
+    if (!no_cache && !c->dbg && b.ms.cache && b.ms.has_box &&
+        band_displacement(c, b, Q, t) < 1.0 - 1e-6) {
+      incr.push_back(id);
+      continue;
+    }
+    b.ms.cache = false;
+    b.want_cache = !no_cache && !c->dbg;
+    remap_region(c, b, Q, t, boxes);
   }
-  if (boxes.empty()) return PSM_OK;
-  if (c->dbg) {  // leaving the debug field mode: the words are authoritative again
+  // an incremental body whose (build) box meets a box remapped now goes the full way
+  for (bool changed = true; changed;) {
+    changed = false;
+    for (size_t k = 0; k < incr.size(); ++k) {
+      Body& b = c->bodies[incr[k]];
+      if (!boxes_overlap(c, b, boxes)) continue;
+      b.ms.cache = false;
+      b.want_cache = true;
+      remap_region(c, b, b.ms.Qc, b.ms.tc, boxes);
+      incr.erase(incr.begin() + (long)k);
+      changed = true;
+      break;
+    }
+  }
+  if (c->dbg && !boxes.empty()) {  // leaving the debug field mode: the words are authoritative
     c->dbg = false;
     CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->mst));
-    psm_status s = PSM_OK;
     std::vector<Box> all;
     for (int id = 1; id <= kMaxBodies; ++id)
       if (c->bodies[id].present && c->bodies[id].ms.has_box)
         add_box(c, c->bodies[id].ms.box_lo, c->bodies[id].ms.box_hi, all);
     CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->mst));
-    s = run_map(c, all);
+    psm_status s = run_map(c, all);
     if (s != PSM_OK) return s;
   }
-  return run_map(c, boxes);
+  if (!boxes.empty()) {
+    psm_status s = run_map(c, boxes);
+    if (s != PSM_OK) return s;
+  }
+  if (!incr.empty() && record(c, 0, 0, c->mst) != cudaSuccess)
+    FAIL(c, PSM_E_CUDA, "event record failed");
+  for (int id : incr) {
+    Body& b = c->bodies[id];
+    const int sl = b.ms.slot;
+    RemapParams r;
+    std::memset(&r, 0, sizeof(r));
+    r.g = c->geom;
+    r.id = id;
+    BodyGeo& g = r.body;
+    std::memcpy(g.Q, b.ms.Qc, sizeof(g.Q));
+    std::memcpy(g.t, b.ms.tc, sizeof(g.t));
+    for (int a = 0; a < 3; ++a) {
+      g.lo1[a] = b.bmin[a] - 1.0;
+      g.hi1[a] = b.bmax[a] + 1.0;
+      g.o[a] = b.o[a];
+      g.dims_b[a] = (int)b.dims[a];
+    }
+    g.r2 = b.radius * b.radius;
+    g.kind = b.kind;
+    g.s = b.s;
+    g.words = b.words;
+    g.present = 1;
+    g.mapping = b.mapping;
+    g.bits = b.d_bits;
+    g.mask = b.d_mask;
+    r.word = c->word;
+    r.tile_flag = c->tile_flag;
+    r.band = b.cband[sl];
+    r.bandcnt = b.ccnt[sl];
+    r.bandn = b.cn[sl];
+    r.band_cap = (int)std::min<size_t>(b.ccap[sl], (size_t)INT32_MAX);
+    r.margin = 1;
+    CUDA_TRY(c, launch_remap_band(r, c->mst == c->st ? 148 * 8 : c->ahead_blocks, c->mst,
+                                  c->mst == c->st ? 256 : c->ahead_threads));
+    c->launches += (b.s >= 2 && b.mapping == 0) ? 2 : 1;
+  }
+  if (!incr.empty() && record(c, 0, 1, c->mst) != cudaSuccess)
+    FAIL(c, PSM_E_CUDA, "event record failed");
+  return PSM_OK;
 }
 
 static psm_status state_write(psm_ctx* c, const double* host, int mode) {
@@ -972,6 +1153,8 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   c->st = static_cast<cudaStream_t>(opt->cuda_stream);
   c->mst = c->st;
   if (const char* e = std::getenv("PSM_AHEAD_BLOCKS")) c->ahead_blocks = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PSM_AHEAD_THREADS"))
+    c->ahead_threads = std::min(1024, std::max(32, std::atoi(e)));
   Geom& g = c->geom;
   g.nx = (int)grid->nx;
   g.ny = (int)grid->ny;
@@ -1005,6 +1188,7 @@ psm_status psm_destroy(psm_ctx* c) {
   for (int id = 0; id <= kMaxBodies; ++id) {
     cudaFree(c->bodies[id].d_bits);
     cudaFree(c->bodies[id].d_mask);
+    free_bands(c->bodies[id]);
   }
   cudaFree(c->dbg_B);
   cudaFree(c->dbg_us);
@@ -1227,6 +1411,7 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
     cudaStreamSynchronize(c->st);
     cudaFree(b.d_bits);
     cudaFree(b.d_mask);
+    free_bands(b);
     b = nb;
   }
   b.present = true;
@@ -1249,6 +1434,7 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
   }
   c->ft_valid = false;
   c->alt_valid = false;  // the spare word buffer no longer matches the bodies
+  // (a pose change keeps the cached band: remap() checks the displacement bound itself)
   return remap(c, std::vector<int>{id}, c->step);
 }
 
@@ -1372,6 +1558,7 @@ psm_status psm_remove_body(psm_ctx* c, int32_t id) {
   cudaStreamSynchronize(c->st);
   cudaFree(b.d_bits);
   cudaFree(b.d_mask);
+  free_bands(b);
   b = Body();
   c->alt_valid = false;
   return run_map(c, boxes);
@@ -1513,7 +1700,9 @@ static psm_status remap_ahead(psm_ctx* c, int64_t next) {
     CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->mst));
     CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->mst));
     for (int id = 1; id <= kMaxBodies; ++id) {
+      const int sl = c->bodies[id].ms.slot;
       c->bodies[id].ms = MapState();
+      c->bodies[id].ms.slot = sl;
       if (c->bodies[id].present) ids.push_back(id);
     }
     c->alt_valid = true;

@@ -162,7 +162,9 @@ struct RemapParams {
   float4* segq;         // body-frame segment centres
   uint32_t* band;       // narrow-band cells: tile << 8 | cell-in-tile
   int* bandcnt;         // their inside counts (s >= 2 chunked path)
+  int* bandn;           // number of band cells (counters + 2, or a cached band's count)
   int seg_cap, band_cap;
+  int margin;           // 1: decisions valid for any pose within one cell (cached band)
 };
 
 #if defined(__CUDACC__)

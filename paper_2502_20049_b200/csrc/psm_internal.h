@@ -37,7 +37,10 @@ cudaError_t launch_voxelize(VoxParams p, void* scratch, uint8_t* mask, cudaStrea
 
 // k_map.cu (general boxes) and k_remap.cu (boxes holding one body)
 cudaError_t launch_map(const MapParams& p, cudaStream_t st);
-cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cudaStream_t st);
+cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cudaStream_t st,
+                                int threads = 256);
+cudaError_t launch_remap_band(const RemapParams& r, int persistent_blocks, cudaStream_t st,
+                              int threads = 256);
 
 // k_state.cu — conversions between the Eq.(4) state and the storage pattern, z-chunked.
 struct StateParams {

@@ -122,17 +122,19 @@ __device__ __forceinline__ int sample_inside(const BodyGeo& b, int x, int y, int
 // sub-sample is inside, 2 = decide per cell.  Every sub-sample lies within 16.16 cells of the
 // tile centre, i.e. within kTileReach - 1 bricks of the centre's brick.  qt = body-frame tile
 // centre (used as the base of the per-cell fp32 decisions).
+// margin = 1: valid for poses within one cell of this one (the brick reaches keep >= 1.84 cells
+// of slack for meshes; the sphere test widens by the margin).
 template <int REACH, int BIT_OUT, int BIT_IN>
 __device__ __forceinline__ int tile_decision(const BodyGeo& b, const double pt[3],
                                              const double L[3], const int wall[3],
-                                             double qt[3]) {
+                                             double qt[3], int margin = 0) {
   constexpr int kTileReach = REACH;  // brick reach of the region's sub-samples + 1
   body_frame(b, pt, L, wall, qt);
   if (b.kind != 1) {
     const double dist = sqrt(qt[0] * qt[0] + qt[1] * qt[1] + qt[2] * qt[2]);
     const double r = sqrt(b.r2);
-    if (dist - (double)(kTileReach - 1) > r) return 0;
-    if (dist + (double)(kTileReach - 1) < r) {
+    if (dist - (double)(kTileReach - 1 + margin) > r) return 0;
+    if (dist + (double)(kTileReach - 1 + margin) < r) {
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const double d = min_image(pt[a] - b.t[a], L[a], !wall[a]);
@@ -169,15 +171,20 @@ __device__ __forceinline__ int tile_decision(const BodyGeo& b, const double pt[3
 
 // Conservative per-cell decision in fp32 from the tile-centre transform (error << 0.1 cell):
 // 0 outside, 1 inside, 2 needs exact sampling.  Sub-samples lie within sqrt(3)/2 of the centre.
-__device__ __forceinline__ int cell_decision(const BodyGeo& b, const float qc[3]) {
+// margin = 1: the decision must also hold after the body moves by up to one cell (every body
+// point displaced by < 1): radius-2 brick flags, bounding box and reach widened by one — the
+// cached narrow band of the remap.
+__device__ __forceinline__ int cell_decision(const BodyGeo& b, const float qc[3],
+                                             int margin = 0) {
   constexpr float kEps = 0.01f;  // >> fp32 error of qc
+  const float M = (float)margin;
 #pragma unroll
   for (int a = 0; a < 3; ++a)
-    if (qc[a] < (float)b.lo1[a] - kEps || qc[a] > (float)b.hi1[a] + kEps) return 0;
+    if (qc[a] < (float)b.lo1[a] - M - kEps || qc[a] > (float)b.hi1[a] + M + kEps) return 0;
   if (b.kind == 0) {
     const float dist = sqrtf(qc[0] * qc[0] + qc[1] * qc[1] + qc[2] * qc[2]);
     const float r = sqrtf((float)b.r2);
-    const float reach = 0.8660254f + kEps;
+    const float reach = 0.8660254f + M + kEps;
     if (dist + reach < r) return 1;
     if (dist - reach > r) return 0;
     return 2;
@@ -186,7 +193,8 @@ __device__ __forceinline__ int cell_decision(const BodyGeo& b, const float qc[3]
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const float xb = floorf(qc[a] - (float)b.o[a]);
-    if (xb < -1.0f || xb > (float)b.dims_b[a]) return 0;  // every sample beyond the field
+    // every sample (plus the margin) beyond the field
+    if (xb < -1.0f - M || xb > (float)b.dims_b[a] + M) return 0;
     bc[a] = (int)xb;
   }
 #pragma unroll
@@ -194,8 +202,8 @@ __device__ __forceinline__ int cell_decision(const BodyGeo& b, const float qc[3]
     if (bc[a] < 0 || bc[a] >= b.dims_b[a]) return 2;
   const uint8_t m =
       __ldg(b.mask + ((long long)bc[2] * b.dims_b[1] + bc[1]) * b.dims_b[0] + bc[0]);
-  if (m & 2) return 1;
-  if (m & 1) return 0;
+  if (m & (margin ? 128 : 2)) return 1;
+  if (m & (margin ? 64 : 1)) return 0;
   return 2;
 }
 

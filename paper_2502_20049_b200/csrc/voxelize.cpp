@@ -175,6 +175,8 @@ void voxelize_mesh(const double* verts, int64_t nv, const int32_t* tris, int64_t
 //   bit2: every brick within Chebyshev distance kTileReach is all-outside (a whole tile)
 //   bit3: every brick within Chebyshev distance kTileReach is all-inside
 //   bit4/bit5: the same within kSubReach (an 8x4x2 sub-tile)
+//   bit6/bit7: the same within 2 (one cell's sub-samples after a pose change of up to one cell:
+//              the remap's cached narrow band)
 static void box_or(std::vector<uint8_t>& v, int64_t bx, int64_t by, int64_t bz, int r) {
   // in place: v := OR of v over the L-infinity ball of radius r (separable running counts);
   // cells beyond the grid contribute 0
@@ -229,7 +231,9 @@ void pack_bricks(const std::vector<uint8_t>& bits, int s, const int64_t dims_cel
   // "beyond the field" is outside: any_out must be 1 there, which box_or cannot see, so the
   // all-inside flags additionally require the whole ball to lie inside the field
   std::vector<uint8_t> in1 = any_in, out1 = any_out, inK = any_in, outK = any_out;
-  std::vector<uint8_t> inS = any_in, outS = any_out;
+  std::vector<uint8_t> inS = any_in, outS = any_out, in2 = any_in, out2 = any_out;
+  box_or(in2, bx, by, bz, 2);
+  box_or(out2, bx, by, bz, 2);
   box_or(in1, bx, by, bz, 1);
   box_or(out1, bx, by, bz, 1);
   box_or(inK, bx, by, bz, kTileReach);
@@ -251,6 +255,8 @@ void pack_bricks(const std::vector<uint8_t>& bits, int s, const int64_t dims_cel
     if (!outK[(size_t)b] && inside_field(kTileReach)) m |= 8;
     if (!inS[(size_t)b]) m |= 16;
     if (!outS[(size_t)b] && inside_field(kSubReach)) m |= 32;
+    if (!in2[(size_t)b]) m |= 64;
+    if (!out2[(size_t)b] && inside_field(2)) m |= 128;
     mask[(size_t)b] = m;
   }
 }
