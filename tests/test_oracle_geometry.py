@@ -274,3 +274,42 @@ def test_r2_rot90_permutation_and_volume():
     o.map()
     vol = np.einsum("ij,ij->i", v[tr[:, 0]], np.cross(v[tr[:, 1]], v[tr[:, 2]])).sum() / 6.0
     assert abs(o.fractions()[2].sum() / 8 / vol - 1) < 0.1
+
+
+def _golden_table1():
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "table1_rotating_cube.txt")
+    rows = {}
+    for line in open(path):
+        if line.strip() and not line.startswith("#"):
+            v = line.split()
+            rows[int(v[0])] = [float(x) for x in v[1:]]
+    return rows
+
+
+@pytest.mark.parametrize("N,s", [(10, 1), (20, 1), (20, 2)])
+def test_table1_rotating_cube_magnitudes_r2(N, s):
+    """Golden fixture tests/golden/table1_rotating_cube.txt (paper Table I):
+    the oracle's centre-only mapping R2 (A12) reproduces the printed volume-error magnitudes
+    (read as the squared relative error of the 100-step time-averaged volume, A20) within a
+    factor of 3; R1 (every sub-sample mapped) is at least 10x more accurate for s >= 1."""
+    paper = _golden_table1()[N][s]
+    n = int(np.ceil(N * np.sqrt(3))) + 8
+    v, t = pi.box_mesh([-N / 2] * 3, [N / 2] * 3)
+    axis = np.array([1.0, 2.0, 3.0])
+    c = np.array([n / 2 + 0.13, n / 2 + 0.29, n / 2 + 0.41])
+    err = {}
+    for mapping in ("R2", "R1"):
+        o = oracle.Oracle(n, n, n, 19, 0.8, (0, 0, 0), 1, 1)
+        o.set_mesh(1, v, t, s)
+        o.set_mapping(1, mapping)
+        vols = []
+        for k in range(100):
+            Q = pi.rotation_about(axis, k * (np.pi / 2) / 100) @ pi.rotation_about([1, 0, 0], 0.1)
+            o.set_pose(1, Q, c)
+            o.map()
+            vols.append(o.fractions()[2].sum(dtype=np.int64) / 8.0 ** s)
+        e = abs(np.mean(vols) - N ** 3) / N ** 3
+        err[mapping] = e * e
+    assert paper / 3 <= err["R2"] <= paper * 3, (err, paper)
+    assert err["R1"] * 10 <= err["R2"], err
