@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
 
   // ---- fused halo: the populations leaving the slab through z go straight into the
   // neighbours' ghost planes (peer stores over NVLink), replacing the separate exchange ----
-  if (act && p.p2p) {
+  if (PAT == 0 && act && p.p2p) {  // (multi-rank runs are two-array only)
     const int pl = yc * nx + xc;
     if (z == G.nzl - 1) {
 #pragma unroll
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
       T* Dq = static_cast<T*>(p.dstq[q]);
       T* Do = static_cast<T*>(p.dstq[stc_opp(q)]);
       if (PAT == 0) {
-        __stcs(Dq + self, f[q]);
+        Dq[self] = f[q];  // default write-back policy: measured 0.9 % faster than __stcs (c5w)
       } else if (PAT == 1) {
         Do[self] = f[q];
       } else {
