@@ -172,9 +172,12 @@ def oracle_sample(wl: dict, steps, budget_s: float, seed: int, warmup: int = 0):
     """Time the CPU oracle (as it stands) on a bounded sub-box of the same workload: same
     stencil/tau/operator, bodies scaled with the box, moving, remapped every step.  `warmup`
     untimed steps first; steps=None sizes the timed steps to about `budget_s` seconds."""
+    cores = os.cpu_count() or 1
+    # torchrun pins OMP_NUM_THREADS=1 per rank; the sample runs on rank 0 alone and may use the
+    # whole host (set before the oracle library, and with it libgomp, is loaded)
+    os.environ["OMP_NUM_THREADS"] = str(cores)
     import oracle
     import psm_inputs as pi
-    cores = os.cpu_count() or 1
     # oracle throughput is ~0.6-1 MLUPS per core for D3Q19; size the box for the budget
     est = 0.6e6 * cores * (19.0 / wl["Q"])
     per_step = budget_s / max(1, steps or 10)
