@@ -70,7 +70,7 @@ def lib():
             "orc_step": (I, [P]),
             "orc_error_cell": (I64, [P]),
             "orc_force_torque": (None, [P, I, P, P, P, P]),
-            "orc_set_dynamics": (None, [P, I, D, P, P, P]),
+            "orc_set_dynamics": (None, [P, I, D, P, P, P, D, P]),
             "orc_set_mapping": (None, [P, I, I]),
             "orc_integrate": (None, [P]),
             "orc_get_body_state": (None, [P, I, P, P, P, P]),
@@ -272,9 +272,12 @@ class Oracle:
                 raise FloatingPointError(
                     f"oracle: invalid state at cell {lib().orc_error_cell(self._h)}")
 
-    def set_dynamics(self, bid, mass, inertia, ext_force=(0, 0, 0), ext_torque=(0, 0, 0)):
-        keep = [_f64(np.ravel(inertia)), _f64(ext_force), _f64(ext_torque)]
-        lib().orc_set_dynamics(self._h, bid, float(mass), *[_p(k) for k in keep])
+    def set_dynamics(self, bid, mass, inertia, ext_force=(0, 0, 0), ext_torque=(0, 0, 0),
+                     added_mass=0.0, added_inertia=None):
+        ai = np.zeros(9) if added_inertia is None else np.ravel(added_inertia)
+        keep = [_f64(np.ravel(inertia)), _f64(ext_force), _f64(ext_torque), _f64(ai)]
+        lib().orc_set_dynamics(self._h, bid, float(mass), _p(keep[0]), _p(keep[1]), _p(keep[2]),
+                               float(added_mass), _p(keep[3]))
 
     def integrate(self):
         """Advance the dynamic bodies with the force/torque of the last step (two-way coupling)."""

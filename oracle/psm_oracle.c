@@ -447,6 +447,8 @@ typedef struct {
   int dynamic;          /* two-way coupled: orc_integrate advances Q, t, v, w */
   int mapping;          /* meshes: 0 = R1 every sub-sample, 1 = R2 centre only (A12) */
   double mass, I[9], fext[3], text[3];
+  double Ma, Ia[9];     /* virtual mass / inertia (A28), 0 = plain semi-implicit Euler */
+  double dv[3], dw[3];  /* last velocity increments, world frame */
   double gorigin[3];
   int64_t gdims[3];
   uint8_t* gbits;
@@ -633,6 +635,8 @@ void orc_set_pose(orc_sim* S, int id, const double Q[9], const double t[3], cons
   memcpy(b->t, t, sizeof(b->t));
   memcpy(b->v, v, sizeof(b->v));
   memcpy(b->w, w, sizeof(b->w));
+  if (b->dynamic)  /* a new initial state of a dynamic body: no previous increments */
+    for (int a = 0; a < 3; ++a) b->dv[a] = b->dw[a] = 0.0;
 }
 
 /* Minimum image on a periodic axis of length L (A7). */
@@ -920,13 +924,17 @@ int64_t orc_error_cell(const orc_sim* S) { return S->err_cell; }
  *   I_w = Q I Q^T;  w <- w + I_w^{-1} (T + T_ext)  (adjugate / determinant);
  *   Q <- Rot(w/|w|, |w|) Q;  columns of Q re-orthonormalised (Gram-Schmidt). */
 void orc_set_dynamics(orc_sim* S, int id, double mass, const double I[9], const double fext[3],
-                      const double text[3]) {
+                      const double text[3], double Ma, const double Ia[9]) {
   orc_body* b = &S->bodies[id];
+  if (!b->dynamic)
+    for (int a = 0; a < 3; ++a) b->dv[a] = b->dw[a] = 0.0;
   b->dynamic = 1;
   b->mass = mass;
   memcpy(b->I, I, sizeof(b->I));
   memcpy(b->fext, fext, sizeof(b->fext));
   memcpy(b->text, text, sizeof(b->text));
+  b->Ma = Ma;
+  memcpy(b->Ia, Ia, sizeof(b->Ia));
 }
 
 void orc_integrate(orc_sim* S) {
@@ -939,25 +947,45 @@ void orc_integrate(orc_sim* S) {
       F[a] = -S->SF[id][a];
       T[a] = -S->ST[id][a];
     }
-    for (int a = 0; a < 3; ++a) b->v[a] = b->v[a] + (F[a] + b->fext[a]) / b->mass;
+    /* virtual-mass form (A28): (m + M_a) dv_new = F + F_e + M_a dv_old; M_a = 0: plain Euler */
+    for (int a = 0; a < 3; ++a) {
+      b->dv[a] = (F[a] + b->fext[a] + b->Ma * b->dv[a]) / (b->mass + b->Ma);
+      b->v[a] = b->v[a] + b->dv[a];
+    }
     for (int a = 0; a < 3; ++a) {
       double x = b->t[a] + b->v[a];
       if (S->bc[a] == 0) x = x - L[a] * floor(x / L[a]);
       b->t[a] = x;
     }
-    double QI[9], Iw[9];
+    /* I_w = Q I Q^T, A_w = Q I_a Q^T (world frame) */
+    double QI[9], Iw[9], QA[9], Aw[9];
     for (int r = 0; r < 3; ++r)
       for (int c = 0; c < 3; ++c) {
-        double acc = 0.0;
-        for (int k = 0; k < 3; ++k) acc += b->Q[3 * r + k] * b->I[3 * k + c];
+        double acc = 0.0, acc2 = 0.0;
+        for (int k = 0; k < 3; ++k) {
+          acc += b->Q[3 * r + k] * b->I[3 * k + c];
+          acc2 += b->Q[3 * r + k] * b->Ia[3 * k + c];
+        }
         QI[3 * r + c] = acc;
+        QA[3 * r + c] = acc2;
       }
     for (int r = 0; r < 3; ++r)
       for (int c = 0; c < 3; ++c) {
-        double acc = 0.0;
-        for (int k = 0; k < 3; ++k) acc += QI[3 * r + k] * b->Q[3 * c + k];
+        double acc = 0.0, acc2 = 0.0;
+        for (int k = 0; k < 3; ++k) {
+          acc += QI[3 * r + k] * b->Q[3 * c + k];
+          acc2 += QA[3 * r + k] * b->Q[3 * c + k];
+        }
         Iw[3 * r + c] = acc;
+        Aw[3 * r + c] = acc2;
       }
+    double Adw[3];
+    for (int r = 0; r < 3; ++r) {
+      double acc = 0.0;
+      for (int k = 0; k < 3; ++k) acc += Aw[3 * r + k] * b->dw[k];
+      Adw[r] = acc;
+    }
+    for (int k = 0; k < 9; ++k) Iw[k] = Iw[k] + Aw[k];
     /* inverse by the adjugate: inv = adj / det */
     double a = Iw[0], bb = Iw[1], c = Iw[2], d = Iw[3], e = Iw[4], f = Iw[5], g = Iw[6],
            h = Iw[7], i = Iw[8];
@@ -965,12 +993,14 @@ void orc_integrate(orc_sim* S) {
                      f * g - d * i, a * i - c * g, c * d - a * f,
                      d * h - e * g, bb * g - a * h, a * e - bb * d};
     double det = a * (e * i - f * h) - bb * (d * i - f * g) + c * (d * h - e * g);
-    double tt[3] = {T[0] + b->text[0], T[1] + b->text[1], T[2] + b->text[2]};
+    double tt[3] = {T[0] + b->text[0] + Adw[0], T[1] + b->text[1] + Adw[1],
+                    T[2] + b->text[2] + Adw[2]};
     for (int r = 0; r < 3; ++r) {
       double acc = 0.0;
       for (int k = 0; k < 3; ++k) acc += adj[3 * r + k] * tt[k];
-      b->w[r] = b->w[r] + acc / det;
+      b->dw[r] = acc / det;
     }
+    for (int r = 0; r < 3; ++r) b->w[r] = b->w[r] + b->dw[r];
     double Qn[9], zero[3] = {0, 0, 0}, one[3] = {1, 1, 1}, tdummy[3];
     int noper[3] = {0, 0, 0};
     orc_pose_advance(b->Q, zero, zero, b->w, 1, one, noper, Qn, tdummy);
