@@ -175,8 +175,14 @@ psm_status psm_remove_body(psm_ctx* ctx, int32_t body_id);
  * PSM force back to the body; its integrator is unstated).
  * With dyn != NULL the body becomes dynamic: after every step the library reduces F, T of
  * Eqs.(10)-(11) on the device (allreduced over ranks), and integrates on the host in fp64:
- *   v += (F + ext_force)/mass;  t += v (wrapped);  I_w = Q I Q^T;  omega += I_w^-1 (T + ext_torque);
+ *   dv = (F + ext_force + M_a dv_prev) / (mass + M_a);  v += dv;  t += v (wrapped);
+ *   I_w = Q I Q^T, A_w = Q I_a Q^T;  dw = (I_w + A_w)^-1 (T + ext_torque + A_w dw_prev);  omega += dw;
  *   Q = Rot(omega/|omega|, |omega|) Q, then Gram-Schmidt on the columns of Q.
+ * (M_a, I_a) is an optional virtual mass (default 0: plain semi-implicit Euler): the fluid's
+ * reaction to the body's acceleration reaches the body one step late, which makes explicit
+ * coupling unstable for density ratios near 1; adding M_a dv on both sides, lagged on the right,
+ * cancels that lag (consistent: at constant acceleration the two terms are equal).  A natural
+ * choice is the displaced fluid, M_a = rho_f V, I_a = (rho_f V / mass) I (A28).
  * The pose and velocities given to psm_set_body are the initial state.  dyn == NULL returns the
  * body to prescribed motion (closed form from its current state).  Errors: PSM_E_ARG (unknown
  * body, mass <= 0, inertia not symmetric positive definite). */
@@ -185,6 +191,8 @@ typedef struct {
   double inertia[9];     /* body-frame inertia tensor about the body origin, row-major        */
   double ext_force[3];   /* constant external force, world frame (e.g. (m - rho_f V) g)       */
   double ext_torque[3];  /* constant external torque, world frame                             */
+  double added_mass;     /* M_a >= 0 (virtual-mass stabilisation, see above; 0 = off)         */
+  double added_inertia[9];  /* I_a, body frame, symmetric positive semi-definite (0 = off)    */
 } psm_dynamics;
 psm_status psm_set_dynamics(psm_ctx* ctx, int32_t body_id, const psm_dynamics* dyn);
 /* Current pose and velocities of a body (the state the next step will map and use for u_s). */

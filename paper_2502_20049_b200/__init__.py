@@ -77,7 +77,8 @@ class psm_velocity(C.Structure):
 
 class psm_dynamics(C.Structure):
     _fields_ = [("mass", C.c_double), ("inertia", C.c_double * 9),
-                ("ext_force", C.c_double * 3), ("ext_torque", C.c_double * 3)]
+                ("ext_force", C.c_double * 3), ("ext_torque", C.c_double * 3),
+                ("added_mass", C.c_double), ("added_inertia", C.c_double * 9)]
 
 
 class PSMError(RuntimeError):
@@ -382,13 +383,16 @@ class Simulation:
         psm_set_body(self.ctx, bid, None, _pose(Q, t), _vel(v, w))
 
     def set_dynamics(self, bid, mass=None, inertia=None, ext_force=(0, 0, 0),
-                     ext_torque=(0, 0, 0)):
-        """Two-way coupled body (mass=None: back to prescribed motion)."""
+                     ext_torque=(0, 0, 0), added_mass=0.0, added_inertia=None):
+        """Two-way coupled body (mass=None: back to prescribed motion); optional virtual mass
+        (added_mass, added_inertia) for density ratios near 1 (psm.h, A28)."""
         if mass is None:
             psm_set_dynamics(self.ctx, bid, None)
             return
+        ai = np.zeros(9) if added_inertia is None else np.ravel(added_inertia)
         d = psm_dynamics(float(mass), (C.c_double * 9)(*np.ravel(inertia)),
-                         (C.c_double * 3)(*ext_force), (C.c_double * 3)(*ext_torque))
+                         (C.c_double * 3)(*ext_force), (C.c_double * 3)(*ext_torque),
+                         float(added_mass), (C.c_double * 9)(*ai))
         psm_set_dynamics(self.ctx, bid, d)
 
     def body_state(self, bid):

@@ -69,6 +69,8 @@ struct Body {
   // two-way coupling: state advanced by the host integrator after every step
   bool dynamic = false;
   double mass = 0, Ib[9] = {0}, fext[3] = {0, 0, 0}, text[3] = {0, 0, 0};
+  double Ma = 0, Ia[9] = {0};                    // virtual mass / inertia (A28)
+  double dv[3] = {0, 0, 0}, dw[3] = {0, 0, 0};   // last velocity increments (world frame)
   double Qd[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, td[3] = {0, 0, 0}, vd[3] = {0, 0, 0},
          wd[3] = {0, 0, 0};
 };
@@ -550,7 +552,10 @@ static void fill_kin(const psm_ctx* c, CollideParams& p, int64_t step) {
 // Semi-implicit Euler step of a dynamic body with the force/torque ON it from the step just
 // completed (the oracle implements the same formulas independently).
 static void integrate_body(const psm_ctx* c, Body& b, const double F[3], const double T[3]) {
-  for (int a = 0; a < 3; ++a) b.vd[a] = b.vd[a] + (F[a] + b.fext[a]) / b.mass;
+  for (int a = 0; a < 3; ++a) {
+    b.dv[a] = (F[a] + b.fext[a] + b.Ma * b.dv[a]) / (b.mass + b.Ma);
+    b.vd[a] = b.vd[a] + b.dv[a];
+  }
   for (int a = 0; a < 3; ++a) {
     double x = b.td[a] + b.vd[a];
     if (c->grid.bc[a] == PSM_PERIODIC) {
@@ -559,33 +564,47 @@ static void integrate_body(const psm_ctx* c, Body& b, const double F[3], const d
     }
     b.td[a] = x;
   }
-  // world-frame inertia I_w = Q I Q^T
-  double M[9], Iw[9];
-  for (int r = 0; r < 3; ++r)
-    for (int cc = 0; cc < 3; ++cc) {
-      double acc = 0.0;
-      for (int l = 0; l < 3; ++l) acc += b.Qd[3 * r + l] * b.Ib[3 * l + cc];
-      M[3 * r + cc] = acc;
-    }
-  for (int r = 0; r < 3; ++r)
-    for (int cc = 0; cc < 3; ++cc) {
-      double acc = 0.0;
-      for (int l = 0; l < 3; ++l) acc += M[3 * r + l] * b.Qd[3 * cc + l];
-      Iw[3 * r + cc] = acc;
-    }
-  // omega += I_w^-1 (T + ext_torque), by the adjugate: d_r = sum_c adj[r][c] tt[c] / det
+  // world-frame inertia I_w = Q I Q^T and virtual inertia A_w = Q I_a Q^T
+  auto to_world = [&](const double* Ib, double* W) {
+    double M[9];
+    for (int r = 0; r < 3; ++r)
+      for (int cc = 0; cc < 3; ++cc) {
+        double acc = 0.0;
+        for (int l = 0; l < 3; ++l) acc += b.Qd[3 * r + l] * Ib[3 * l + cc];
+        M[3 * r + cc] = acc;
+      }
+    for (int r = 0; r < 3; ++r)
+      for (int cc = 0; cc < 3; ++cc) {
+        double acc = 0.0;
+        for (int l = 0; l < 3; ++l) acc += M[3 * r + l] * b.Qd[3 * cc + l];
+        W[3 * r + cc] = acc;
+      }
+  };
+  double Iw[9], Aw[9];
+  to_world(b.Ib, Iw);
+  to_world(b.Ia, Aw);
+  double Aw_dw[3];
+  for (int r = 0; r < 3; ++r) {
+    double acc = 0.0;
+    for (int cc = 0; cc < 3; ++cc) acc += Aw[3 * r + cc] * b.dw[cc];
+    Aw_dw[r] = acc;
+  }
+  for (int k = 0; k < 9; ++k) Iw[k] = Iw[k] + Aw[k];
+  // dw = (I_w + A_w)^-1 (T + ext_torque + A_w dw_prev), by the adjugate
   const double A = Iw[0], B = Iw[1], C = Iw[2], D = Iw[3], E = Iw[4], Fm = Iw[5], G = Iw[6],
                H = Iw[7], I = Iw[8];
   const double adj[9] = {E * I - Fm * H, C * H - B * I, B * Fm - C * E,
                          Fm * G - D * I, A * I - C * G, C * D - A * Fm,
                          D * H - E * G, B * G - A * H, A * E - B * D};
   const double det = A * (E * I - Fm * H) - B * (D * I - Fm * G) + C * (D * H - E * G);
-  const double tt[3] = {T[0] + b.text[0], T[1] + b.text[1], T[2] + b.text[2]};
+  const double tt[3] = {T[0] + b.text[0] + Aw_dw[0], T[1] + b.text[1] + Aw_dw[1],
+                        T[2] + b.text[2] + Aw_dw[2]};
   for (int r = 0; r < 3; ++r) {
     double acc = 0.0;
     for (int cc = 0; cc < 3; ++cc) acc += adj[3 * r + cc] * tt[cc];
-    b.wd[r] = b.wd[r] + acc / det;
+    b.dw[r] = acc / det;
   }
+  for (int r = 0; r < 3; ++r) b.wd[r] = b.wd[r] + b.dw[r];
   double Qn[9];
   rodrigues(b.wd, 1.0, b.Qd, Qn);
   // Gram-Schmidt on the columns
@@ -1427,6 +1446,7 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
   b.step0 = c->step;
   if (b.dynamic) {  // new initial state of a dynamic body
     b.moving = true;
+    for (int a = 0; a < 3; ++a) b.dv[a] = b.dw[a] = 0.0;
     std::memcpy(b.Qd, b.Q0, sizeof(b.Qd));
     std::memcpy(b.td, b.t0, sizeof(b.td));
     std::memcpy(b.vd, b.v, sizeof(b.vd));
@@ -1507,10 +1527,22 @@ psm_status psm_set_dynamics(psm_ctx* c, int32_t id, const psm_dynamics* d) {
     std::memcpy(b.td, t, sizeof(t));
     std::memcpy(b.vd, b.v, sizeof(b.vd));
     std::memcpy(b.wd, b.w, sizeof(b.wd));
+    for (int a = 0; a < 3; ++a) b.dv[a] = b.dw[a] = 0.0;
+  }
+  if (!(d->added_mass >= 0.0) || !std::isfinite(d->added_mass))
+    FAIL(c, PSM_E_ARG, "added mass must be finite and >= 0");
+  for (int r = 0; r < 3; ++r) {
+    if (!(d->added_inertia[4 * r] >= 0.0)) FAIL(c, PSM_E_ARG, "added inertia must be >= 0");
+    for (int cc = 0; cc < 3; ++cc)
+      if (!std::isfinite(d->added_inertia[3 * r + cc]) ||
+          d->added_inertia[3 * r + cc] != d->added_inertia[3 * cc + r])
+        FAIL(c, PSM_E_ARG, "added inertia must be symmetric and finite");
   }
   b.dynamic = true;
   b.moving = true;
   b.mass = d->mass;
+  b.Ma = d->added_mass;
+  std::memcpy(b.Ia, d->added_inertia, sizeof(b.Ia));
   std::memcpy(b.Ib, d->inertia, sizeof(b.Ib));
   std::memcpy(b.fext, d->ext_force, sizeof(b.fext));
   std::memcpy(b.text, d->ext_torque, sizeof(b.text));

@@ -569,3 +569,34 @@ def test_gpu_voxelizer_speed_large_rotor(monkeypatch):
     print(f"set_mesh s=3, {len(tr)} faces: GPU voxeliser {t_gpu:.2f} s, host {t_host:.2f} s")
     assert np.array_equal(cnt_gpu, cnt_host)
     g.close()
+
+
+def test_two_way_coupled_light_body_with_virtual_mass():
+    """A light body (density ratio 1.1) with the virtual-mass stabilisation (psm.h
+    psm_dynamics.added_mass / added_inertia, A28), closed box, SC2: library integrator vs the
+    oracle's, body states <= 1e-11 relative, PDFs <= 1e-12 over 60 coupled steps."""
+    n, r, ratio, gz = (28, 26, 30), 4.0, 1.1, 2e-4
+    o = oracle.Oracle(*n, 19, 0.8, (1, 1, 1), 2, 1)
+    g = _sim(nx=n[0], ny=n[1], nz=n[2], Q=19, tau=0.8, bc=(1, 1, 1), sc=2, bmode=1)
+    rho, u = pi.perturbed_flow(n[::-1], 31, u0=(0.0, 0.0, 0.0))
+    o.init_equilibrium(rho, u)
+    g.init_equilibrium(rho, u)
+    V = 4.0 / 3.0 * np.pi * r ** 3
+    m = ratio * V
+    I = 0.4 * m * r * r * np.eye(3)
+    kw = dict(added_mass=V, added_inertia=I / ratio)
+    o.set_sphere(1, r, 1)
+    o.set_pose(1, np.eye(3), (14.2, 13.1, 17.4), (0, 0, 0), (0, 0, 0.001))
+    o.set_dynamics(1, m, I, (0.0, 0.0, -(m - V) * gz), **kw)
+    g.set_sphere(1, r, 1, np.eye(3), (14.2, 13.1, 17.4), (0, 0, 0), (0, 0, 0.001))
+    g.set_dynamics(1, m, I, (0.0, 0.0, -(m - V) * gz), **kw)
+    for k in range(60):
+        o.map()
+        o.step(1)
+        o.integrate()
+        g.step(1)
+        so, sg = o.body_state(1), g.body_state(1)
+        for a, c in zip(so, sg):
+            assert np.allclose(a, c, rtol=1e-11, atol=1e-14), (k, a, c)
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+    assert g.body_state(1)[2][2] < 0  # sinking

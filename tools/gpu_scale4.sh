@@ -1,8 +1,8 @@
 set -x
-timeout 900 python -m pytest tests/test_multigpu.py -x -q > gpurun_out/gputests_mg.log 2>&1; echo rc=$? >> gpurun_out/gputests_mg.log
-timeout 600 python bench.py --steps 50 --warmup 5 > gpurun_out/scale_n1.json 2> gpurun_out/scale_n1.err
+timeout 1200 python -m pytest tests/test_multigpu.py -x -q > gpurun_out/gputests_mg.log 2>&1; echo rc=$? >> gpurun_out/gputests_mg.log
+timeout 600 python bench.py --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/scale_n1.json 2> gpurun_out/scale_n1.err
 for n in 2 4; do timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2955$n bench.py --gpus $n --steps 50 --warmup 5 > gpurun_out/scale_n$n.json 2> gpurun_out/scale_n$n.err; done
 timeout 600 python bench.py --config c5s --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/strong_n1.json 2> gpurun_out/strong_n1.err
 for n in 2 4; do timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2956$n bench.py --config c5s --gpus $n --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/strong_n$n.json 2> gpurun_out/strong_n$n.err; done
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ref_n1.json 2> gpurun_out/ref_n1.err
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29571 bench.py --impl reference --gpus 4 --steps 3 --warmup 3 > gpurun_out/ref_n4.json 2> gpurun_out/ref_n4.err
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1

@@ -30,8 +30,10 @@ def run(nx=135, nz=216, r=10.125, tau=0.65, ratio=1.164, g=3.8e-4, steps=12000, 
     m = ratio * vol
     z0 = nz - 2.5 * 2 * r
     sim.set_sphere(1, r, s, np.eye(3), (nx / 2, nx / 2, z0))
-    sim.set_dynamics(1, m, 0.4 * m * r * r * np.eye(3),
-                     ext_force=(0.0, 0.0, -(m - vol) * g))
+    I = 0.4 * m * r * r * np.eye(3)
+    # virtual mass of the displaced fluid (psm.h, A28): stable at ratio ~1
+    sim.set_dynamics(1, m, I, ext_force=(0.0, 0.0, -(m - vol) * g), added_mass=vol,
+                     added_inertia=I * (vol / m))
     hist = []
     for k in range(0, steps, every):
         sim.step(every)
@@ -54,15 +56,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    # ten Cate's ratio 1.164 is unstable with our explicit coupling (added-mass effect at
-    # density ratios near 1); 1.5 keeps the set-up otherwise the paper's
-    r, ratio, U = 10.125, 1.5, 0.02
+    # ten Cate's sphere/oil density ratio (1120 / 962); stable with the virtual mass
+    r, ratio, U = 10.125, 1.164, 0.02
     lines = ["# Settling sphere (two-way coupled PSM, B200 path)", "",
              "The paper's set-up (PAPER.md:444-448): 135x135x216 cells, no-slip walls, SRT + SC2, "
-             f"sphere d = {2 * r:g} cells (s = 1), rho_s/rho_f = {ratio} (ten Cate's 1.16 is unstable "
-             "with explicit coupling); D3Q19 fp64. Gravity is chosen so that the Schiller-Naumann terminal velocity of "
+             f"sphere d = {2 * r:g} cells (s = 1), rho_s/rho_f = {ratio} (ten Cate), virtual mass of the "
+             "displaced fluid; D3Q19 fp64. Gravity is chosen so that the Schiller-Naumann terminal velocity of "
              f"an unbounded fluid is U = {U}; the table gives the measured terminal velocity.", ""]
-    for Re in (1.5, 4.1):  # ten Cate E1, E2 (at E3 = 11.6, tau = 0.535, SC2 blows up here)
+    for Re in (1.5, 4.1, 11.6, 31.9):  # ten Cate's E1-E4
         nu = U * 2 * r / Re
         tau = 3 * nu + 0.5
         g = gravity_for(U, r, nu, ratio)
