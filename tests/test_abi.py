@@ -145,3 +145,36 @@ def test_voxelize_rejects_open_mesh():
     with pytest.raises(psm.PSMError) as e:
         psm.psm_voxelize(v, t2, 1)
     assert e.value.code == psm.PSM_E_MESH
+
+
+def test_struct_layouts_match_the_c_compiler(tmp_path):
+    """sizeof and field offsets of every ABI struct as gcc sees include/psm.h == the ctypes
+    binding's (catches a header change the binding did not follow)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    checks = {
+        "psm_grid": ["nx", "bc"], "psm_options": ["body_force", "rank", "cuda_stream",
+                                                  "collision", "trt_magic"],
+        "psm_shape": ["radius", "verts", "tris", "mapping"], "psm_pose": ["t"],
+        "psm_velocity": ["omega"],
+        "psm_dynamics": ["inertia", "ext_torque", "added_mass", "added_inertia"],
+    }
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "psm.h"', "int main(void) {"]
+    for st, fields in checks.items():
+        lines.append(f'  printf("{st} %zu\\n", sizeof({st}));')
+        for f in fields:
+            lines.append(f'  printf("{st}.{f} %zu\\n", offsetof({st}, {f}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    out = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                 check=True).stdout.splitlines())
+    for st, fields in checks.items():
+        cls = getattr(psm, st)
+        assert int(out[st]) == C.sizeof(cls), st
+        for f in fields:
+            assert int(out[f"{st}.{f}"]) == getattr(cls, f).offset, (st, f)
