@@ -884,7 +884,9 @@ static psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
       continue;
     }
     b.ms.cache = false;
-    b.want_cache = !no_cache && !c->dbg;
+    // the cached band pays off while the exact pass is cheap (8 sub-samples per cell); at
+    // s >= 2 the radius-2 band's 64/512 samples per cell cost more than the L0-L2 pipeline
+    b.want_cache = !no_cache && !c->dbg && b.s <= 1;
     remap_region(c, b, Q, t, boxes);
   }
   // an incremental body whose (build) box meets a box remapped now goes the full way
@@ -894,7 +896,7 @@ static psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
       Body& b = c->bodies[incr[k]];
       if (!boxes_overlap(c, b, boxes)) continue;
       b.ms.cache = false;
-      b.want_cache = true;
+      b.want_cache = b.s <= 1;
       remap_region(c, b, b.ms.Qc, b.ms.tc, boxes);
       incr.erase(incr.begin() + (long)k);
       changed = true;
@@ -1789,18 +1791,22 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
   CUDA_TRY(c, cudaMemsetAsync(c->overflow, 0, (kMaxBodies + 1) * kSlotVals * 8, c->st));
   // remap-ahead pipeline: several steps in this call, bodies in prescribed motion only
   bool any_moving = false, any_dynamic = false;
+  int max_s = 0;
   for (int id = 1; id <= kMaxBodies; ++id) {
     const Body& b = c->bodies[id];
     if (!b.present) continue;
     any_moving |= b.moving;
     any_dynamic |= b.dynamic;
+    if (b.moving) max_s = std::max(max_s, b.s);
   }
   if (c->world > 1) {
     st = ensure_p2p(c);
     if (st != PSM_OK) return st;
   }
   static const bool no_ahead = std::getenv("PSM_NO_REMAP_AHEAD") != nullptr;
-  const bool ahead = n > 1 && any_moving && !any_dynamic && !c->dbg && !no_ahead;
+  // (at s = 3 the remap is ALU-heavy enough to slow the collide more than it hides: measured
+  // 12.4k vs 14.8k MLUPS on c5w, so it runs in series there)
+  const bool ahead = n > 1 && any_moving && !any_dynamic && !c->dbg && !no_ahead && max_s <= 2;
   if (ahead) {
     st = ensure_pipeline(c);
     if (st != PSM_OK) return st;
