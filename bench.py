@@ -262,6 +262,20 @@ def workload_config(wl: dict, world: int) -> dict:
             "l2": "inputs larger than L2 (PDF arrays >> 126 MB)"}
 
 
+_MESHES = {}
+
+
+def _rotor_mesh(blades: int, tip: float):
+    """The CROR-like rotor meshes (~0.6 M faces), generated once per process: at N GPUs every
+    rank holds all 2N rotors, which share two shapes."""
+    import psm_inputs as pi
+    key = (blades, tip)
+    if key not in _MESHES:
+        _MESHES[key] = pi.propeller_mesh(n_blades=blades, scale=tip / 110.0, n_st=200, n_pts=128,
+                                         hub_seg=256)
+    return _MESHES[key]
+
+
 def build_workload(psm, wl: dict, rank: int, world: int, nccl_id=None):
     """The bench's simulation: the grid of `wl` (nz per GPU stacked in z), rest fluid, and the
     bodies (a CROR-like rotor pair or one moving sphere per GPU slab; every rank holds every
@@ -286,8 +300,7 @@ def build_workload(psm, wl: dict, rank: int, world: int, nccl_id=None):
         if wl.get("rotors"):
             for k, front in enumerate((True, False)):
                 tip = wl.get("rotor_tip", (200.0, 180.0))[k]
-                v, t = pi.propeller_mesh(n_blades=12 if front else 10, scale=tip / 110.0,
-                                         n_st=200, n_pts=128, hub_seg=256)
+                v, t = _rotor_mesh(12 if front else 10, tip)
                 w = (wl["omega"] if front else -wl["omega"], 0.0, 0.0)
                 tpos = (wl.get("rotor_x", (200.0, 330.0))[k], ny / 2, zc)
                 sim.set_mesh(1 + 2 * r + k, v, t, wl["s"], np.eye(3), tpos, (0, 0, 0), w,
