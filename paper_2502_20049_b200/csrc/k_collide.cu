@@ -12,6 +12,8 @@
 //   PAT 1  AA even step   : f_i(x) = A[i][x];                      write A[ibar][x] = f*_i
 //   PAT 2  AA odd step    : f_i(x) = A[ibar][x - c_i] (wall: A[i][x]);
 //                           write A[i][x + c_i] = f*_i (wall: A[ibar][x])
+#include <type_traits>
+
 #include "psm_device.cuh"
 #include "psm_internal.h"
 
@@ -374,12 +376,13 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
 
   // ---- gather the pre-collision populations f_i(x) ----
   T f[Q];
-  {
+  auto gather = [&](auto with_walls) {
+    constexpr bool W = decltype(with_walls)::value;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int cx = stc_x(q) + 1, cy = stc_y(q) + 1, cz = stc_z(q) + 1;
       const int src = RB[cy][cz] + OX[cx];
-      const bool out = WALLS && (OUTX[cx] || OUTY[cy] || OUTZ[cz]);
+      const bool out = W && (OUTX[cx] || OUTY[cy] || OUTZ[cz]);
       const T* Aq = static_cast<const T*>(p.srcq[q]);
       const T* Ao = static_cast<const T*>(p.srcq[stc_opp(q)]);
       if (PAT == 0) {
@@ -392,6 +395,14 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
         f[q] = *ptr;
       }
     }
+  };
+  if constexpr (WALLS == 2) {
+    // only x is non-periodic: the wall/open-face selects matter in the first and last tile
+    // column alone (block-uniform branch), every other block runs the periodic gather
+    if (blockIdx.x == 0 || blockIdx.x == G.gx - 1) gather(std::true_type{});
+    else gather(std::false_type{});
+  } else {
+    gather(std::integral_constant<bool, (WALLS != 0)>{});
   }
 
   // ---- open x faces (reading A30): the populations entering at x = 0 / nx-1 were gathered
