@@ -1,533 +1,16 @@
-// psm_api.cpp — C ABI of the B200 PSM hot path (include/psm.h).  Host orchestration only:
-// validation, memory layout, closed-form pose advance (host fp64 libm, reading A13),
-// remap-box planning, the per-step launch sequence, NCCL halo exchange and force/torque
-// allreduce.  Every arithmetic step of the method runs in the sm_100a kernels (k_*.cu).
-#include "psm.h"
-
-#include <cuda_runtime.h>
-#include <nccl.h>
-
-#include <algorithm>
-#include <array>
-#include <cmath>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <new>
-#include <string>
-#include <vector>
-
-#include "psm_device.cuh"
-#include "psm_host.h"
-#include "psm_internal.h"
+// psm_api.cpp — C ABI of the B200 PSM hot path (include/psm.h): validation, the extern "C" entry
+// points and the per-step launch sequence.  Host orchestration only; every arithmetic step of the
+// method runs in the sm_100a kernels (k_*.cu).  The rest of the host side is split over
+// host_bodies.cpp, host_memory.cpp, host_remap.cpp and host_halo.cpp (psm_ctx.h).
+#include "psm_ctx.h"
 
 using namespace psm;
 
+namespace psm {
+std::string g_last_error;
+}  // namespace psm
+
 namespace {
-
-constexpr int kFtChunks = 296;           // 2 x 148 SMs, pass-1 blocks of the F/T reduction
-constexpr size_t kStageBudget = 256ull << 20;
-constexpr size_t kGeomCapBytes = 1ull << 30;
-
-struct MapState {
-  double Qc[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, tc[3] = {0, 0, 0};  // pose of the mapping
-  int64_t mapped_step = -1;
-  bool has_box = false;
-  int64_t box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};  // mapped box (global, unwrapped)
-  // cached narrow band (k_remap.cu, margin 1): valid for poses within one cell of (Qrb, trb)
-  int slot = 0;        // which of the body's two band stores belongs to this word buffer
-  bool cache = false;
-  double Qrb[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, trb[3] = {0, 0, 0};
-};
-
-struct Body {
-  bool present = false;
-  int kind = 0, s = 0, mapping = 0;
-  double radius = 0, rbound = 0;
-  double bmin[3] = {0, 0, 0}, bmax[3] = {0, 0, 0};  // body-frame AABB of the shape
-  // mesh geometry field (device)
-  double o[3] = {0, 0, 0};
-  int64_t dims[3] = {0, 0, 0};
-  int words = 1;
-  unsigned long long* d_bits = nullptr;
-  uint8_t* d_mask = nullptr;
-  // prescribed motion: pose at step0, closed-form advance
-  double Q0[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, t0[3] = {0, 0, 0};
-  double v[3] = {0, 0, 0}, w[3] = {0, 0, 0};
-  int64_t step0 = 0;
-  bool moving = false;
-  // mapping state of the active solid-word buffer (ms) and of the spare one (alt, used by the
-  // remap-ahead pipeline of psm_step; swapped together with the buffers)
-  MapState ms, alt;
-  // band stores (device), indexed by MapState::slot; capacity in cells
-  uint32_t* cband[2] = {nullptr, nullptr};
-  int* ccnt[2] = {nullptr, nullptr};
-  int* cn[2] = {nullptr, nullptr};
-  size_t ccap[2] = {0, 0};
-  bool want_cache = false;  // transient: the current remap rebuilds this body's band
-  Body() { alt.slot = 1; }
-  // two-way coupling: state advanced by the host integrator after every step
-  bool dynamic = false;
-  double mass = 0, Ib[9] = {0}, fext[3] = {0, 0, 0}, text[3] = {0, 0, 0};
-  double Ma = 0, Ia[9] = {0};                    // virtual mass / inertia (A28)
-  double dv[3] = {0, 0, 0}, dw[3] = {0, 0, 0};   // last velocity increments (world frame)
-  double Qd[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, td[3] = {0, 0, 0}, vd[3] = {0, 0, 0},
-         wd[3] = {0, 0, 0};
-};
-
-struct Box {
-  int64_t lo[3], hi[3];  // global cells, [lo, hi), already wrapped into the domain
-};
-
-}  // namespace
-
-struct psm_ctx {
-  psm_grid grid{};
-  int Q = 19;
-  double tau = 0.8;
-  psm_options opt{};
-  double u_in[3] = {0.0, 0.0, 0.0};  // A30 open boundaries (bc[0] == PSM_INOUT)
-  double rho_out = 1.0;
-  int rank = 0, world = 1;
-  int64_t z0 = 0, nzl = 0;
-  Geom geom{};
-  int64_t ncell_local = 0, ntiles = 0;
-  size_t S = 8;
-  // device memory
-  void* mem = nullptr;
-  size_t mem_bytes = 0;
-  bool own_mem = false, bound = false;
-  void* A[2] = {nullptr, nullptr};
-  int cur = 0;
-  uint32_t* word = nullptr;          // active solid-word buffer (read by the next collide)
-  uint8_t* tile_flag = nullptr;
-  uint32_t* word_alt = nullptr;      // spare buffer: the remap of step n+1 runs into it while
-  uint8_t* tile_flag_alt = nullptr;  // the collide of step n reads the active one
-  bool alt_valid = false;            // the spare buffer's words match every body's alt state
-  cudaStream_t mst = nullptr;        // stream the remap launches go to (st, or map_st ahead)
-  cudaStream_t map_st = nullptr;     // remap-ahead stream (high priority)
-  cudaEvent_t ev_map = nullptr, ev_coll = nullptr;
-  int ahead_blocks = 148;            // persistent remap blocks when overlapped with the collide
-  int ahead_threads = 256;
-  double* partial = nullptr;
-  double* overflow = nullptr;
-  unsigned long long* err = nullptr;
-  double* ft_scratch = nullptr;
-  double* ft_out = nullptr;
-  int* ft_ids = nullptr;
-  double* stage = nullptr;
-  size_t stage_bytes = 0;
-  // narrow-band remap lists
-  int* r_counters = nullptr;
-  int* r_tiles = nullptr;
-  uint32_t* r_segs = nullptr;
-  float4* r_segq = nullptr;
-  uint32_t* r_band = nullptr;
-  int* r_bandcnt = nullptr;
-  int seg_cap = 0, band_cap = 0;
-  double* pinned = nullptr;  // host staging (ft + err)
-  // test-only dense fields
-  double *dbg_B = nullptr, *dbg_us = nullptr;
-  uint8_t* dbg_id = nullptr;
-  bool dbg = false;
-  Body bodies[kMaxBodies + 1];
-  int64_t step = 0;
-  double ft[kMaxBodies + 1][kSlotVals] = {};
-  bool ft_valid = false;
-  cudaStream_t st = nullptr;
-  ncclComm_t comm = nullptr;
-  cudaStream_t comm_st = nullptr;     // halo stream (overlaps the interior collide)
-  cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
-  // fused peer-store halo (psm_halo_mode 2)
-  bool p2p_checked = false, p2p = false;
-  bool has_up = false, has_dn = false;
-  void* ipc_up = nullptr;            // opened IPC base of the upper / lower neighbour's memory
-  void* ipc_dn = nullptr;
-  char* up_A[2] = {nullptr, nullptr};
-  char* dn_A[2] = {nullptr, nullptr};
-  int64_t up_qs = 0, dn_qs = 0, dn_nzl = 0;
-  unsigned long long* up_flag = nullptr;  // the upper neighbour's "from below" flag word
-  unsigned long long* dn_flag = nullptr;  // the lower neighbour's "from above" flag word
-  unsigned long long* flags = nullptr;    // mine: [0] from below, [1] from above, [2] hs error
-  unsigned long long epoch = 0;
-  unsigned char nccl_id[128] = {};
-  std::string err_msg;
-  int64_t launches = 0;
-  bool prof = false;
-  std::vector<std::array<cudaEvent_t, 2>> ev[PSM_NUM_PHASES];
-  double prof_ms[PSM_NUM_PHASES] = {};
-  int64_t prof_cnt[PSM_NUM_PHASES] = {};
-};
-
-static std::string g_last_error;
-
-#define FAIL(ctx, code, msg)                  \
-  do {                                        \
-    std::string _m = (msg);                   \
-    if (ctx) (ctx)->err_msg = _m;             \
-    g_last_error = _m;                        \
-    return (code);                            \
-  } while (0)
-
-#define CUDA_TRY(ctx, expr)                                                             \
-  do {                                                                                  \
-    cudaError_t _e = (expr);                                                            \
-    if (_e != cudaSuccess)                                                              \
-      FAIL(ctx, PSM_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));        \
-  } while (0)
-
-#define NCCL_TRY(ctx, expr)                                                             \
-  do {                                                                                  \
-    ncclResult_t _r = (expr);                                                           \
-    if (_r != ncclSuccess)                                                              \
-      FAIL(ctx, PSM_E_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));        \
-  } while (0)
-
-// ---------------------------------------------------------------------------- helpers ------
-static void free_bands(Body& b) {  // callers have synchronised the streams
-  for (int k = 0; k < 2; ++k) {
-    if (b.cband[k]) cudaFreeAsync(b.cband[k], 0);
-    if (b.ccnt[k]) cudaFreeAsync(b.ccnt[k], 0);
-    if (b.cn[k]) cudaFreeAsync(b.cn[k], 0);
-    b.cband[k] = nullptr;
-    b.ccnt[k] = nullptr;
-    b.cn[k] = nullptr;
-    b.ccap[k] = 0;
-  }
-}
-
-static void rodrigues(const double w[3], double n, const double Q0[9], double out[9]) {
-  // Q_n = Rot(w/|w|, n|w|) Q_0 (A13: host libm sin/cos)
-  const double wn = std::sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
-  double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-  if (wn > 0.0) {
-    const double k[3] = {w[0] / wn, w[1] / wn, w[2] / wn};
-    const double th = n * wn, s = std::sin(th), c = 1.0 - std::cos(th);
-    const double K[9] = {0, -k[2], k[1], k[2], 0, -k[0], -k[1], k[0], 0};
-    for (int r = 0; r < 3; ++r)
-      for (int cc = 0; cc < 3; ++cc) {
-        double k2 = 0.0;
-        for (int l = 0; l < 3; ++l) k2 += K[3 * r + l] * K[3 * l + cc];
-        R[3 * r + cc] += s * K[3 * r + cc] + c * k2;
-      }
-  }
-  for (int r = 0; r < 3; ++r)
-    for (int cc = 0; cc < 3; ++cc) {
-      double acc = 0.0;
-      for (int l = 0; l < 3; ++l) acc += R[3 * r + l] * Q0[3 * l + cc];
-      out[3 * r + cc] = acc;
-    }
-}
-
-static double extent(const psm_ctx* c, int a) {
-  return (double)(a == 0 ? c->grid.nx : (a == 1 ? c->grid.ny : c->grid.nz));
-}
-
-static void pose_at(const psm_ctx* c, const Body& b, int64_t step, double Q[9], double t[3]) {
-  const double n = (double)(step - b.step0);
-  for (int a = 0; a < 3; ++a) {
-    double x = b.t0[a] + n * b.v[a];
-    if (c->grid.bc[a] == PSM_PERIODIC) {
-      const double L = extent(c, a);
-      x = x - L * std::floor(x / L);
-    }
-    t[a] = x;
-  }
-  rodrigues(b.w, n, b.Q0, Q);
-}
-
-// world box of the cells the body can touch at pose (Q, t): AABB of the rotated body-frame
-// AABB, dilated by one cell (the kernel's per-cell filter uses the same +-1 margin)
-static void body_box(const psm_ctx* c, const Body& b, const double Q[9], const double t[3],
-                     int64_t lo[3], int64_t hi[3]) {
-  (void)c;
-  double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
-  for (int k = 0; k < 8; ++k) {
-    const double p[3] = {(k & 1) ? b.bmax[0] : b.bmin[0], (k & 2) ? b.bmax[1] : b.bmin[1],
-                         (k & 4) ? b.bmax[2] : b.bmin[2]};
-    for (int a = 0; a < 3; ++a) {
-      const double w = Q[3 * a] * p[0] + Q[3 * a + 1] * p[1] + Q[3 * a + 2] * p[2];
-      mn[a] = std::min(mn[a], w);
-      mx[a] = std::max(mx[a], w);
-    }
-  }
-  for (int a = 0; a < 3; ++a) {
-    // +2: one cell for the kernel filter margin, one for rounding of the corner transform
-    lo[a] = (int64_t)std::floor(t[a] + mn[a] - 2.0);
-    hi[a] = (int64_t)std::floor(t[a] + mx[a] + 2.0) + 1;
-  }
-}
-
-// split [lo, hi) on axis a into in-domain pieces
-static int axis_pieces(const psm_ctx* c, int a, int64_t lo, int64_t hi, int64_t out[2][2]) {
-  const int64_t L = (int64_t)extent(c, a);
-  if (c->grid.bc[a] != PSM_PERIODIC) {
-    lo = std::max<int64_t>(lo, 0);
-    hi = std::min<int64_t>(hi, L);
-    if (hi <= lo) return 0;
-    out[0][0] = lo;
-    out[0][1] = hi;
-    return 1;
-  }
-  if (hi - lo >= L) {
-    out[0][0] = 0;
-    out[0][1] = L;
-    return 1;
-  }
-  int64_t l = ((lo % L) + L) % L, len = hi - lo;
-  if (l + len <= L) {
-    out[0][0] = l;
-    out[0][1] = l + len;
-    return 1;
-  }
-  out[0][0] = l;
-  out[0][1] = L;
-  out[1][0] = 0;
-  out[1][1] = l + len - L;
-  return 2;
-}
-
-static void add_box(const psm_ctx* c, const int64_t lo[3], const int64_t hi[3],
-                    std::vector<Box>& boxes) {
-  int64_t px[2][2], py[2][2], pz[2][2];
-  const int nxp = axis_pieces(c, 0, lo[0], hi[0], px);
-  const int nyp = axis_pieces(c, 1, lo[1], hi[1], py);
-  const int nzp = axis_pieces(c, 2, lo[2], hi[2], pz);
-  for (int i = 0; i < nxp; ++i)
-    for (int j = 0; j < nyp; ++j)
-      for (int k = 0; k < nzp; ++k) {
-        Box b;
-        b.lo[0] = px[i][0]; b.hi[0] = px[i][1];
-        b.lo[1] = py[j][0]; b.hi[1] = py[j][1];
-        b.lo[2] = pz[k][0]; b.hi[2] = pz[k][1];
-        boxes.push_back(b);
-      }
-}
-
-// region to remap for body b moving to pose t: hull of the old and new boxes if they overlap
-// (after the periodic shift that brings them closest), both boxes otherwise
-static void remap_region(const psm_ctx* c, Body& b, const double Q[9], const double t[3],
-                         std::vector<Box>& boxes) {
-  int64_t lo[3], hi[3];
-  body_box(c, b, Q, t, lo, hi);
-  if (b.ms.has_box) {
-    bool overlap = true;
-    int64_t slo[3], shi[3];
-    for (int a = 0; a < 3; ++a) {
-      int64_t shift = 0;
-      if (c->grid.bc[a] == PSM_PERIODIC) {
-        const int64_t L = (int64_t)extent(c, a);
-        const double dc = 0.5 * ((lo[a] + hi[a]) - (b.ms.box_lo[a] + b.ms.box_hi[a]));
-        shift = -(int64_t)std::llround(dc / (double)L) * L;
-      }
-      slo[a] = lo[a] + shift;
-      shi[a] = hi[a] + shift;
-      if (slo[a] >= b.ms.box_hi[a] || shi[a] <= b.ms.box_lo[a]) overlap = false;
-    }
-    if (overlap) {
-      int64_t ulo[3], uhi[3];
-      for (int a = 0; a < 3; ++a) {
-        ulo[a] = std::min(slo[a], b.ms.box_lo[a]);
-        uhi[a] = std::max(shi[a], b.ms.box_hi[a]);
-      }
-      add_box(c, ulo, uhi, boxes);
-    } else {
-      add_box(c, b.ms.box_lo, b.ms.box_hi, boxes);
-      add_box(c, lo, hi, boxes);
-    }
-  } else {
-    add_box(c, lo, hi, boxes);
-  }
-  for (int a = 0; a < 3; ++a) {
-    b.ms.box_lo[a] = lo[a];
-    b.ms.box_hi[a] = hi[a];
-  }
-  b.ms.has_box = true;
-}
-
-static cudaError_t record(psm_ctx* c, int phase, int which, cudaStream_t s = nullptr) {
-  if (!c->prof) return cudaSuccess;
-  if (which == 0) {
-    std::array<cudaEvent_t, 2> e{};
-    cudaError_t r = cudaEventCreate(&e[0]);
-    if (r != cudaSuccess) return r;
-    r = cudaEventCreate(&e[1]);
-    if (r != cudaSuccess) return r;
-    c->ev[phase].push_back(e);
-  }
-  return cudaEventRecord(c->ev[phase].back()[which], s ? s : c->st);
-}
-
-// ------------------------------------------------------------------------- memory plan -----
-struct Plan {
-  size_t off_A0, off_A1, off_word, off_flag, off_word_alt, off_flag_alt, off_partial, off_overflow, off_err, off_scratch,
-      off_ftout, off_ids, off_stage, off_flags, stage_bytes, total;
-  size_t off_rcnt, off_rtiles, off_rsegs, off_rsegq, off_rband, off_rbandcnt;
-  int seg_cap, band_cap;
-};
-
-static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
-
-static Plan make_plan(const psm_ctx* c) {
-  Plan p{};
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    size_t o = off;
-    off = align256(off + bytes);
-    return o;
-  };
-  const size_t arr = (size_t)c->Q * (size_t)c->geom.qstride * c->S;
-  p.off_A0 = take(arr);
-  p.off_A1 = (c->opt.pattern == PSM_TWO_ARRAY) ? take(arr) : 0;
-  p.off_word = take((size_t)c->ncell_local * 4);
-  p.off_flag = take((size_t)c->ntiles);
-  p.off_word_alt = take((size_t)c->ncell_local * 4);
-  p.off_flag_alt = take((size_t)c->ntiles);
-  p.off_partial = take((size_t)c->ntiles * 2 * (1 + kSlotVals) * 8);
-  p.off_overflow = take((kMaxBodies + 1) * kSlotVals * 8);
-  p.off_err = take(8);
-  p.off_scratch = take((size_t)kFtChunks * kMaxBodies * kSlotVals * 8);
-  p.off_ftout = take(kMaxBodies * kSlotVals * 8);
-  p.off_ids = take(kMaxBodies * 4);
-  p.off_flags = take(64);
-  // narrow-band remap lists (k_remap.cu); overflow is handled in-kernel (serial fallback)
-  p.seg_cap = (int)std::min<int64_t>(32 * c->ntiles, 1 << 22);
-  p.band_cap = (int)std::min<int64_t>(c->ncell_local, 1 << 23);
-  p.off_rcnt = take(4 * sizeof(int));
-  p.off_rtiles = take((size_t)c->ntiles * 4);
-  p.off_rsegs = take((size_t)p.seg_cap * 4);
-  p.off_rsegq = take((size_t)p.seg_cap * 16);
-  p.off_rband = take((size_t)p.band_cap * 4);
-  p.off_rbandcnt = take((size_t)p.band_cap * 4);
-  const size_t plane = (size_t)c->grid.nx * c->grid.ny * 8;
-  const size_t per = plane * (size_t)c->Q;
-  size_t planes = std::max<size_t>(3, kStageBudget / per);
-  planes = std::min<size_t>(planes, (size_t)c->nzl + 2);
-  p.stage_bytes = planes * per;
-  p.off_stage = take(p.stage_bytes);
-  p.total = off;
-  return p;
-}
-
-static psm_status ensure_pinned(psm_ctx* c);
-
-static psm_status ensure_comm(psm_ctx* c);
-
-static psm_status bind(psm_ctx* c, void* mem, size_t bytes) {
-  psm_status ps = ensure_pinned(c);
-  if (ps != PSM_OK) return ps;
-  ps = ensure_comm(c);
-  if (ps != PSM_OK) return ps;
-  Plan p = make_plan(c);
-  if (bytes < p.total)
-    FAIL(c, PSM_E_OOM, "bound buffer has " + std::to_string(bytes) + " bytes, need " +
-                           std::to_string(p.total));
-  char* m = static_cast<char*>(mem);
-  c->mem = mem;
-  c->mem_bytes = bytes;
-  c->A[0] = m + p.off_A0;
-  c->A[1] = (c->opt.pattern == PSM_TWO_ARRAY) ? (void*)(m + p.off_A1) : nullptr;
-  c->word = reinterpret_cast<uint32_t*>(m + p.off_word);
-  c->tile_flag = reinterpret_cast<uint8_t*>(m + p.off_flag);
-  c->word_alt = reinterpret_cast<uint32_t*>(m + p.off_word_alt);
-  c->tile_flag_alt = reinterpret_cast<uint8_t*>(m + p.off_flag_alt);
-  c->alt_valid = false;
-  c->partial = reinterpret_cast<double*>(m + p.off_partial);
-  c->overflow = reinterpret_cast<double*>(m + p.off_overflow);
-  c->err = reinterpret_cast<unsigned long long*>(m + p.off_err);
-  c->ft_scratch = reinterpret_cast<double*>(m + p.off_scratch);
-  c->ft_out = reinterpret_cast<double*>(m + p.off_ftout);
-  c->ft_ids = reinterpret_cast<int*>(m + p.off_ids);
-  c->flags = reinterpret_cast<unsigned long long*>(m + p.off_flags);
-  c->stage = reinterpret_cast<double*>(m + p.off_stage);
-  c->r_counters = reinterpret_cast<int*>(m + p.off_rcnt);
-  c->r_tiles = reinterpret_cast<int*>(m + p.off_rtiles);
-  c->r_segs = reinterpret_cast<uint32_t*>(m + p.off_rsegs);
-  c->r_segq = reinterpret_cast<float4*>(m + p.off_rsegq);
-  c->r_band = reinterpret_cast<uint32_t*>(m + p.off_rband);
-  c->r_bandcnt = reinterpret_cast<int*>(m + p.off_rbandcnt);
-  c->seg_cap = p.seg_cap;
-  c->band_cap = p.band_cap;
-  c->stage_bytes = p.stage_bytes;
-  CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->st));
-  CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->st));
-  CUDA_TRY(c, cudaMemsetAsync(c->overflow, 0, (kMaxBodies + 1) * kSlotVals * 8, c->st));
-  CUDA_TRY(c, cudaMemsetAsync(c->err, 0xFF, 8, c->st));
-  CUDA_TRY(c, cudaMemsetAsync(c->flags, 0, 64, c->st));
-  c->bound = true;
-  return PSM_OK;
-}
-
-static psm_status ensure_pinned(psm_ctx* c) {
-  if (c->pinned) return PSM_OK;
-  if (cudaMallocHost(&c->pinned, (kMaxBodies + 2) * kSlotVals * 8) != cudaSuccess) {
-    cudaGetLastError();
-    c->pinned = nullptr;
-    FAIL(c, PSM_E_OOM, "cudaMallocHost failed");
-  }
-  return PSM_OK;
-}
-
-static psm_status ensure_comm(psm_ctx* c) {
-  // the communicator is created at the first device call, so psm_create stays host-only
-  if (c->world == 1 || c->comm) return PSM_OK;
-  ncclUniqueId id;
-  static_assert(sizeof(id) == sizeof(c->nccl_id), "ncclUniqueId size");
-  std::memcpy(&id, c->nccl_id, sizeof(id));
-  NCCL_TRY(c, ncclCommInitRank(&c->comm, c->world, id, c->rank));
-  // highest priority: NCCL's blocks are scheduled as soon as interior-collide blocks retire
-  int lo_prio = 0, hi_prio = 0;
-  CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-  CUDA_TRY(c, cudaStreamCreateWithPriority(&c->comm_st, cudaStreamNonBlocking, hi_prio));
-  CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_bnd, cudaEventDisableTiming));
-  CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
-  return PSM_OK;
-}
-
-static psm_status ensure_mem(psm_ctx* c) {
-  psm_status ps = ensure_pinned(c);
-  if (ps != PSM_OK) return ps;
-  ps = ensure_comm(c);
-  if (ps != PSM_OK) return ps;
-  if (c->bound) return PSM_OK;
-  Plan p = make_plan(c);
-  void* m = nullptr;
-  if (cudaMalloc(&m, p.total) != cudaSuccess) {
-    cudaGetLastError();
-    FAIL(c, PSM_E_OOM, "cudaMalloc of " + std::to_string(p.total) + " bytes failed");
-  }
-  c->own_mem = true;
-  return bind(c, m, p.total);
-}
-
-static psm_status halo(psm_ctx* c, void* arr, cudaStream_t hst) {
-  // two-array pull: ship the c_z = +1 populations of the top plane up and the c_z = -1
-  // populations of the bottom plane down, straight from/into the SoA planes (no packing)
-  if (c->world == 1) return PSM_OK;
-  const int P = c->world, r = c->rank;
-  const bool zwall = c->grid.bc[2] == PSM_WALL;
-  const int up = (r + 1) % P, down = (r - 1 + P) % P;
-  const bool has_up = !(zwall && r == P - 1), has_down = !(zwall && r == 0);
-  const size_t plane = (size_t)c->grid.nx * c->grid.ny;
-  const ncclDataType_t dt = (c->opt.prec == PSM_F64) ? ncclFloat64 : ncclFloat32;
-  char* base = static_cast<char*>(arr);
-  auto ptr = [&](int q, int64_t zs) {
-    return base + ((size_t)q * (size_t)c->geom.qstride + (size_t)zs * plane) * c->S;
-  };
-  NCCL_TRY(c, ncclGroupStart());
-  for (int q = 0; q < c->Q; ++q) {
-    const int cz = stc_z(q);
-    if (cz > 0) {
-      if (has_up) NCCL_TRY(c, ncclSend(ptr(q, c->nzl), plane, dt, up, c->comm, hst));
-      if (has_down) NCCL_TRY(c, ncclRecv(ptr(q, 0), plane, dt, down, c->comm, hst));
-    } else if (cz < 0) {
-      if (has_down) NCCL_TRY(c, ncclSend(ptr(q, 1), plane, dt, down, c->comm, hst));
-      if (has_up) NCCL_TRY(c, ncclRecv(ptr(q, c->nzl + 1), plane, dt, up, c->comm, hst));
-    }
-  }
-  NCCL_TRY(c, ncclGroupEnd());
-  return PSM_OK;
-}
 
 static void fill_kin(const psm_ctx* c, CollideParams& p, int64_t step) {
   for (int id = 0; id <= kMaxBodies; ++id) {
@@ -547,546 +30,6 @@ static void fill_kin(const psm_ctx* c, CollideParams& p, int64_t step) {
     k.s = b.s;
     k.present = 1;
   }
-}
-
-// Semi-implicit Euler step of a dynamic body with the force/torque ON it from the step just
-// completed (the oracle implements the same formulas independently).
-static void integrate_body(const psm_ctx* c, Body& b, const double F[3], const double T[3]) {
-  for (int a = 0; a < 3; ++a) {
-    b.dv[a] = (F[a] + b.fext[a] + b.Ma * b.dv[a]) / (b.mass + b.Ma);
-    b.vd[a] = b.vd[a] + b.dv[a];
-  }
-  for (int a = 0; a < 3; ++a) {
-    double x = b.td[a] + b.vd[a];
-    if (c->grid.bc[a] == PSM_PERIODIC) {
-      const double L = extent(c, a);
-      x = x - L * std::floor(x / L);
-    }
-    b.td[a] = x;
-  }
-  // world-frame inertia I_w = Q I Q^T and virtual inertia A_w = Q I_a Q^T
-  auto to_world = [&](const double* Ib, double* W) {
-    double M[9];
-    for (int r = 0; r < 3; ++r)
-      for (int cc = 0; cc < 3; ++cc) {
-        double acc = 0.0;
-        for (int l = 0; l < 3; ++l) acc += b.Qd[3 * r + l] * Ib[3 * l + cc];
-        M[3 * r + cc] = acc;
-      }
-    for (int r = 0; r < 3; ++r)
-      for (int cc = 0; cc < 3; ++cc) {
-        double acc = 0.0;
-        for (int l = 0; l < 3; ++l) acc += M[3 * r + l] * b.Qd[3 * cc + l];
-        W[3 * r + cc] = acc;
-      }
-  };
-  double Iw[9], Aw[9];
-  to_world(b.Ib, Iw);
-  to_world(b.Ia, Aw);
-  double Aw_dw[3];
-  for (int r = 0; r < 3; ++r) {
-    double acc = 0.0;
-    for (int cc = 0; cc < 3; ++cc) acc += Aw[3 * r + cc] * b.dw[cc];
-    Aw_dw[r] = acc;
-  }
-  for (int k = 0; k < 9; ++k) Iw[k] = Iw[k] + Aw[k];
-  // dw = (I_w + A_w)^-1 (T + ext_torque + A_w dw_prev), by the adjugate
-  const double A = Iw[0], B = Iw[1], C = Iw[2], D = Iw[3], E = Iw[4], Fm = Iw[5], G = Iw[6],
-               H = Iw[7], I = Iw[8];
-  const double adj[9] = {E * I - Fm * H, C * H - B * I, B * Fm - C * E,
-                         Fm * G - D * I, A * I - C * G, C * D - A * Fm,
-                         D * H - E * G, B * G - A * H, A * E - B * D};
-  const double det = A * (E * I - Fm * H) - B * (D * I - Fm * G) + C * (D * H - E * G);
-  const double tt[3] = {T[0] + b.text[0] + Aw_dw[0], T[1] + b.text[1] + Aw_dw[1],
-                        T[2] + b.text[2] + Aw_dw[2]};
-  for (int r = 0; r < 3; ++r) {
-    double acc = 0.0;
-    for (int cc = 0; cc < 3; ++cc) acc += adj[3 * r + cc] * tt[cc];
-    b.dw[r] = acc / det;
-  }
-  for (int r = 0; r < 3; ++r) b.wd[r] = b.wd[r] + b.dw[r];
-  double Qn[9];
-  rodrigues(b.wd, 1.0, b.Qd, Qn);
-  // Gram-Schmidt on the columns
-  double c0[3] = {Qn[0], Qn[3], Qn[6]}, c1[3] = {Qn[1], Qn[4], Qn[7]};
-  const double n0 = std::sqrt(c0[0] * c0[0] + c0[1] * c0[1] + c0[2] * c0[2]);
-  for (int a = 0; a < 3; ++a) c0[a] = c0[a] / n0;
-  const double d01 = c0[0] * c1[0] + c0[1] * c1[1] + c0[2] * c1[2];
-  for (int a = 0; a < 3; ++a) c1[a] = c1[a] - d01 * c0[a];
-  const double n1 = std::sqrt(c1[0] * c1[0] + c1[1] * c1[1] + c1[2] * c1[2]);
-  for (int a = 0; a < 3; ++a) c1[a] = c1[a] / n1;
-  const double c2[3] = {c0[1] * c1[2] - c0[2] * c1[1], c0[2] * c1[0] - c0[0] * c1[2],
-                        c0[0] * c1[1] - c0[1] * c1[0]};
-  for (int a = 0; a < 3; ++a) {
-    b.Qd[3 * a + 0] = c0[a];
-    b.Qd[3 * a + 1] = c1[a];
-    b.Qd[3 * a + 2] = c2[a];
-  }
-}
-
-static psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
-  MapParams mp;
-  std::memset(&mp, 0, sizeof(mp));
-  mp.g = c->geom;
-  mp.word = c->word;
-  mp.tile_flag = c->tile_flag;
-  for (int id = 1; id <= kMaxBodies; ++id) {
-    const Body& b = c->bodies[id];
-    BodyGeo& g = mp.bodies[id];
-    if (!b.present) continue;
-    std::memcpy(g.Q, b.ms.Qc, sizeof(g.Q));
-    std::memcpy(g.t, b.ms.tc, sizeof(g.t));
-    for (int a = 0; a < 3; ++a) {
-      g.lo1[a] = b.bmin[a] - 1.0;
-      g.hi1[a] = b.bmax[a] + 1.0;
-    }
-    g.r2 = b.radius * b.radius;
-    for (int a = 0; a < 3; ++a) {
-      g.o[a] = b.o[a];
-      g.dims_b[a] = (int)b.dims[a];
-    }
-    g.kind = b.kind;
-    g.s = b.s;
-    g.words = b.words;
-    g.present = 1;
-    g.mapping = b.mapping;
-    g.bits = b.d_bits;
-    g.mask = b.d_mask;
-  }
-  // boxes -> local tile boxes, launched in batches of kMaxBoxes
-  std::vector<MapBox> tb;
-  for (const Box& b : boxes) {
-    const int64_t zlo = std::max<int64_t>(b.lo[2], c->z0) - c->z0;
-    const int64_t zhi = std::min<int64_t>(b.hi[2], c->z0 + c->nzl) - c->z0;
-    if (zhi <= zlo || b.hi[0] <= b.lo[0] || b.hi[1] <= b.lo[1]) continue;
-    MapBox m;
-    m.t0[0] = (int)(b.lo[0] / kTileX);
-    m.n[0] = (int)((b.hi[0] - 1) / kTileX + 1 - m.t0[0]);
-    m.t0[1] = (int)(b.lo[1] / kTileY);
-    m.n[1] = (int)((b.hi[1] - 1) / kTileY + 1 - m.t0[1]);
-    m.t0[2] = (int)(zlo / kTileZ);
-    m.n[2] = (int)((zhi - 1) / kTileZ + 1 - m.t0[2]);
-    m.first = 0;
-    // bodies whose current box overlaps the TILE-ALIGNED extent of this box (the kernels
-    // rewrite whole tiles, so every body that can own a cell of those tiles must be evaluated)
-    const int64_t tlo[3] = {(int64_t)m.t0[0] * kTileX, (int64_t)m.t0[1] * kTileY,
-                            (int64_t)m.t0[2] * kTileZ + c->z0};
-    const int64_t thi[3] = {tlo[0] + (int64_t)m.n[0] * kTileX, tlo[1] + (int64_t)m.n[1] * kTileY,
-                            tlo[2] + (int64_t)m.n[2] * kTileZ};
-    m.bodymask = 0;
-    for (int id = 1; id <= kMaxBodies; ++id) {
-      const Body& bd = c->bodies[id];
-      if (!bd.present || !bd.ms.has_box) continue;
-      std::vector<Box> pieces;
-      add_box(c, bd.ms.box_lo, bd.ms.box_hi, pieces);
-      for (const Box& pc : pieces) {
-        bool ov = true;
-        for (int a = 0; a < 3; ++a)
-          if (pc.hi[a] <= tlo[a] || pc.lo[a] >= thi[a]) ov = false;
-        if (ov) {
-          m.bodymask |= 1u << id;
-          break;
-        }
-      }
-    }
-    if (!m.bodymask) {
-      // nothing can be inside: still launched so the words/flags of the box are cleared
-    }
-    tb.push_back(m);
-  }
-  static const bool stats_on = std::getenv("PSM_MAP_STATS") != nullptr;
-  unsigned long long* dstats = nullptr;
-  if (stats_on) {
-    CUDA_TRY(c, cudaMalloc(&dstats, 8 * 8));
-    CUDA_TRY(c, cudaMemsetAsync(dstats, 0, 8 * 8, c->mst));
-  }
-  mp.stats = dstats;
-  if (record(c, 0, 0, c->mst) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
-  static const bool force_general = std::getenv("PSM_REMAP_GENERAL") != nullptr;
-  // cached bands: bodies rebuilt in single-body boxes only; capacity = every cell of their boxes
-  size_t need[kMaxBodies + 1] = {};
-  int nsingle[kMaxBodies + 1] = {}, ngeneral[kMaxBodies + 1] = {};
-  for (size_t i = 0; i < tb.size(); ++i) {
-    const int pc = __builtin_popcount(tb[i].bodymask);
-    if (pc == 1 && !force_general) {
-      const int id = __builtin_ctz(tb[i].bodymask);
-      need[id] += (size_t)tb[i].n[0] * tb[i].n[1] * tb[i].n[2] * kTileCells;
-      nsingle[id] += 1;
-    } else {
-      for (int id = 1; id <= kMaxBodies; ++id)
-        if (tb[i].bodymask & (1u << id)) ngeneral[id] += 1;
-    }
-  }
-  for (int id = 1; id <= kMaxBodies; ++id) {
-    Body& bd = c->bodies[id];
-    if (ngeneral[id]) bd.ms.cache = false;  // shares a box with another body: no band cache
-    if (!bd.want_cache || ngeneral[id] || !nsingle[id]) {
-      bd.want_cache = false;
-      continue;
-    }
-    const int sl = bd.ms.slot;
-    if (bd.ccap[sl] < need[id]) {
-      // stream-ordered (no device-wide sync in the middle of a pipelined step), with headroom
-      // so that the slowly changing box of a moving body rarely regrows it
-      const size_t cap = need[id] + need[id] / 4;
-      if (bd.cband[sl]) CUDA_TRY(c, cudaFreeAsync(bd.cband[sl], c->mst));
-      if (bd.ccnt[sl]) CUDA_TRY(c, cudaFreeAsync(bd.ccnt[sl], c->mst));
-      bd.cband[sl] = nullptr;
-      bd.ccnt[sl] = nullptr;
-      bd.ccap[sl] = 0;
-      CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&bd.cband[sl]), cap * 4, c->mst));
-      CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&bd.ccnt[sl]), cap * 4, c->mst));
-      bd.ccap[sl] = cap;
-    }
-    if (!bd.cn[sl]) CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&bd.cn[sl]), sizeof(int), c->mst));
-    CUDA_TRY(c, cudaMemsetAsync(bd.cn[sl], 0, sizeof(int), c->mst));
-  }
-  for (size_t i = 0; i < tb.size(); ++i) {
-    if (__builtin_popcount(tb[i].bodymask) == 1 && !force_general) {
-      // one body in the box: narrow-band pipeline (k_remap.cu)
-      RemapParams r;
-      std::memset(&r, 0, sizeof(r));
-      r.g = c->geom;
-      r.box = tb[i];
-      r.id = __builtin_ctz(tb[i].bodymask);
-      r.body = mp.bodies[r.id];
-      r.word = c->word;
-      r.tile_flag = c->tile_flag;
-      r.counters = c->r_counters;
-      r.tiles = c->r_tiles;
-      r.segs = c->r_segs;
-      r.segq = c->r_segq;
-      r.band = c->r_band;
-      r.bandcnt = c->r_bandcnt;
-      r.bandn = c->r_counters + 2;
-      r.seg_cap = c->seg_cap;
-      r.band_cap = c->band_cap;
-      Body& bd = c->bodies[r.id];
-      if (bd.want_cache) {  // build the body's cached band (decisions with one cell of slack)
-        const int sl = bd.ms.slot;
-        r.margin = 1;
-        r.band = bd.cband[sl];
-        r.bandcnt = bd.ccnt[sl];
-        r.bandn = bd.cn[sl];
-        r.band_cap = (int)std::min<size_t>(bd.ccap[sl], (size_t)INT32_MAX);
-      }
-      CUDA_TRY(c, launch_remap_single(r, c->mst == c->st ? 148 * 8 : c->ahead_blocks, c->mst,
-                                      c->mst == c->st ? 256 : c->ahead_threads));
-      c->launches += 4;
-      continue;
-    }
-    // general box (several bodies may cover its cells): one launch, 3D grid of its tiles
-    mp.box[0] = tb[i];
-    mp.nbox = 1;
-    mp.ntiles = tb[i].n[0] * tb[i].n[1] * tb[i].n[2];
-    CUDA_TRY(c, launch_map(mp, c->mst));
-    c->launches += 1;
-  }
-  for (int id = 1; id <= kMaxBodies; ++id) {
-    Body& bd = c->bodies[id];
-    if (!bd.want_cache) continue;
-    bd.want_cache = false;
-    bd.ms.cache = true;
-    std::memcpy(bd.ms.Qrb, bd.ms.Qc, sizeof(bd.ms.Qrb));
-    std::memcpy(bd.ms.trb, bd.ms.tc, sizeof(bd.ms.trb));
-  }
-  if (record(c, 0, 1, c->mst) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
-  if (dstats) {
-    unsigned long long h[8];
-    CUDA_TRY(c, cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, c->mst));
-    CUDA_TRY(c, cudaStreamSynchronize(c->mst));
-    cudaFree(dstats);
-    std::fprintf(stderr,
-                 "[psm map] boxes %zu  8-cell segments: out %llu in %llu cell %llu | "
-                 "cells: out %llu in %llu band %llu | tiles skipped %llu\n",
-                 tb.size(), h[0], h[1], h[2], h[3], h[4], h[5], h[7]);
-  }
-  return PSM_OK;
-}
-
-// the active and spare solid-word buffers trade places (with every body's mapping state)
-static void swap_buffers(psm_ctx* c) {
-  std::swap(c->word, c->word_alt);
-  std::swap(c->tile_flag, c->tile_flag_alt);
-  for (int id = 1; id <= kMaxBodies; ++id) std::swap(c->bodies[id].ms, c->bodies[id].alt);
-}
-
-static psm_status ensure_pipeline(psm_ctx* c) {
-  if (c->map_st) return PSM_OK;
-  int lo_prio = 0, hi_prio = 0;
-  CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-  CUDA_TRY(c, cudaStreamCreateWithPriority(&c->map_st, cudaStreamNonBlocking, hi_prio));
-  CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_map, cudaEventDisableTiming));
-  CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_coll, cudaEventDisableTiming));
-  return PSM_OK;
-}
-
-// Upper bound on how far any point of body b moves between the band's build pose and (Q, t):
-// |mi(t - t_rb)| + r_bound * |Q - Q_rb|_F / sqrt(2)  (the chord of a rotation by theta is
-// 2 r sin(theta/2) = r |Q - Q_rb|_F / sqrt(2)).
-static double band_displacement(const psm_ctx* c, const Body& b, const double Q[9],
-                                 const double t[3]) {
-  double dt2 = 0.0, dq2 = 0.0;
-  for (int a = 0; a < 3; ++a) {
-    double d = t[a] - b.ms.trb[a];
-    if (c->grid.bc[a] == PSM_PERIODIC) {
-      const double L = extent(c, a);
-      d -= L * std::nearbyint(d / L);
-    }
-    dt2 += d * d;
-  }
-  for (int k = 0; k < 9; ++k) dq2 += (Q[k] - b.ms.Qrb[k]) * (Q[k] - b.ms.Qrb[k]);
-  return std::sqrt(dt2) + b.rbound * std::sqrt(dq2 * 0.5);
-}
-
-static bool boxes_overlap(const psm_ctx* c, const Body& b, const std::vector<Box>& boxes) {
-  std::vector<Box> mine;
-  add_box(c, b.ms.box_lo, b.ms.box_hi, mine);
-  for (const Box& m : mine)
-    for (const Box& o : boxes) {
-      bool ov = true;
-      for (int a = 0; a < 3; ++a)
-        if (m.hi[a] <= o.lo[a] || m.lo[a] >= o.hi[a]) ov = false;
-      if (ov) return true;
-    }
-  return false;
-}
-
-// remap the given bodies at the pose of `step` (or all present bodies if ids empty).  A body with
-// a valid cached band that has moved less than one cell since the band was built (and whose box
-// no other remapped body touches) only re-runs the exact pass over its band.
-static psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
-  static const bool no_cache = [] {
-    const char* e = std::getenv("PSM_BAND_CACHE");
-    return e && std::strcmp(e, "0") == 0;
-  }();
-  std::vector<Box> boxes;
-  std::vector<int> incr;
-  for (int id : ids) {
-    Body& b = c->bodies[id];
-    if (!b.present) continue;
-    double Q[9], t[3];
-    if (b.dynamic) {
-      std::memcpy(Q, b.Qd, sizeof(Q));
-      std::memcpy(t, b.td, sizeof(t));
-    } else if (b.moving) {
-      pose_at(c, b, step, Q, t);
-    } else {
-      std::memcpy(Q, b.Q0, sizeof(Q));
-      std::memcpy(t, b.t0, sizeof(t));
-    }
-    std::memcpy(b.ms.Qc, Q, sizeof(Q));
-    std::memcpy(b.ms.tc, t, sizeof(t));
-    b.ms.mapped_step = step;
-    if (!no_cache && !c->dbg && b.ms.cache && b.ms.has_box &&
-        band_displacement(c, b, Q, t) < 1.0 - 1e-6) {
-      incr.push_back(id);
-      continue;
-    }
-    b.ms.cache = false;
-    // the cached band pays off while the exact pass is cheap (8 sub-samples per cell); at
-    // s >= 2 the radius-2 band's 64/512 samples per cell cost more than the L0-L2 pipeline
-    b.want_cache = !no_cache && !c->dbg && b.s <= 1;
-    remap_region(c, b, Q, t, boxes);
-  }
-  // an incremental body whose (build) box meets a box remapped now goes the full way
-  for (bool changed = true; changed;) {
-    changed = false;
-    for (size_t k = 0; k < incr.size(); ++k) {
-      Body& b = c->bodies[incr[k]];
-      if (!boxes_overlap(c, b, boxes)) continue;
-      b.ms.cache = false;
-      b.want_cache = b.s <= 1;
-      remap_region(c, b, b.ms.Qc, b.ms.tc, boxes);
-      incr.erase(incr.begin() + (long)k);
-      changed = true;
-      break;
-    }
-  }
-  if (c->dbg && !boxes.empty()) {  // leaving the debug field mode: the words are authoritative
-    c->dbg = false;
-    CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->mst));
-    std::vector<Box> all;
-    for (int id = 1; id <= kMaxBodies; ++id)
-      if (c->bodies[id].present && c->bodies[id].ms.has_box)
-        add_box(c, c->bodies[id].ms.box_lo, c->bodies[id].ms.box_hi, all);
-    CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->mst));
-    psm_status s = run_map(c, all);
-    if (s != PSM_OK) return s;
-  }
-  if (!boxes.empty()) {
-    psm_status s = run_map(c, boxes);
-    if (s != PSM_OK) return s;
-  }
-  if (!incr.empty() && record(c, 0, 0, c->mst) != cudaSuccess)
-    FAIL(c, PSM_E_CUDA, "event record failed");
-  for (int id : incr) {
-    Body& b = c->bodies[id];
-    const int sl = b.ms.slot;
-    RemapParams r;
-    std::memset(&r, 0, sizeof(r));
-    r.g = c->geom;
-    r.id = id;
-    BodyGeo& g = r.body;
-    std::memcpy(g.Q, b.ms.Qc, sizeof(g.Q));
-    std::memcpy(g.t, b.ms.tc, sizeof(g.t));
-    for (int a = 0; a < 3; ++a) {
-      g.lo1[a] = b.bmin[a] - 1.0;
-      g.hi1[a] = b.bmax[a] + 1.0;
-      g.o[a] = b.o[a];
-      g.dims_b[a] = (int)b.dims[a];
-    }
-    g.r2 = b.radius * b.radius;
-    g.kind = b.kind;
-    g.s = b.s;
-    g.words = b.words;
-    g.present = 1;
-    g.mapping = b.mapping;
-    g.bits = b.d_bits;
-    g.mask = b.d_mask;
-    r.word = c->word;
-    r.tile_flag = c->tile_flag;
-    r.band = b.cband[sl];
-    r.bandcnt = b.ccnt[sl];
-    r.bandn = b.cn[sl];
-    r.band_cap = (int)std::min<size_t>(b.ccap[sl], (size_t)INT32_MAX);
-    r.margin = 1;
-    CUDA_TRY(c, launch_remap_band(r, c->mst == c->st ? 148 * 8 : c->ahead_blocks, c->mst,
-                                  c->mst == c->st ? 256 : c->ahead_threads));
-    c->launches += (b.s >= 2 && b.mapping == 0) ? 2 : 1;
-  }
-  if (!incr.empty() && record(c, 0, 1, c->mst) != cudaSuccess)
-    FAIL(c, PSM_E_CUDA, "event record failed");
-  return PSM_OK;
-}
-
-static psm_status state_write(psm_ctx* c, const double* host, int mode) {
-  // mode 0: f [Q][N] host; 1: rho/u host (rho or u may be NULL -> defaults); 2: uniform rest
-  psm_status s = ensure_mem(c);
-  if (s != PSM_OK) return s;
-  const size_t plane = (size_t)c->grid.nx * c->grid.ny;
-  const int nvals = mode == 0 ? c->Q : 4;
-  const size_t per = plane * (size_t)nvals * 8;
-  const int64_t cap = (int64_t)(c->stage_bytes / per);  // planes in staging
-  const bool ghost = c->geom.zghost != 0;
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(c->nzl, cap - 2));
-  void* arr = c->A[c->opt.pattern == PSM_TWO_ARRAY ? c->cur : 0];
-  std::vector<double> tmp;
-  for (int64_t za = 0; za < c->nzl; za += chunk) {
-    const int64_t zb = std::min<int64_t>(c->nzl, za + chunk);
-    StateParams p{};
-    p.g = c->geom;
-    p.A = arr;
-    p.stage = c->stage;
-    p.za = (int)za;
-    p.zb = (int)zb;
-    p.pattern = c->opt.pattern == PSM_AA ? 1 : 0;
-    p.mode = mode;
-    p.ghosts = ghost ? 1 : 0;
-    for (int a = 0; a < 3; ++a) p.u_in[a] = c->u_in[a];
-    p.rho_out = c->rho_out;
-    if (mode != 2) {
-      // staging planes cover the readers of slots in [za, zb): local planes [za-1, zb+1)
-      int64_t s0 = za - 1, s1 = zb + 1;
-      if (ghost || c->opt.pattern == PSM_AA) {
-        s0 = std::max<int64_t>(0, s0);
-        s1 = std::min<int64_t>(c->nzl, s1);
-      }
-      if (!ghost && c->opt.pattern != PSM_AA && c->grid.bc[2] == PSM_WALL) {
-        s0 = std::max<int64_t>(0, s0);
-        s1 = std::min<int64_t>(c->nzl, s1);
-      }
-      int64_t ns = s1 - s0;
-      if (ns > c->nzl) {  // small periodic grid: the whole slab once
-        s0 = 0;
-        ns = c->nzl;
-      }
-      p.stage_z0 = (int)s0;
-      p.stage_nz = (int)ns;
-      // gather host planes (wrapped) into a contiguous pinned-free host buffer, then H2D
-      tmp.assign((size_t)(ns * plane * nvals), 0.0);
-      const size_t N = (size_t)c->nzl * plane;
-      if (mode == 0)
-        for (int v = 0; v < nvals; ++v)
-          for (int64_t k = 0; k < ns; ++k) {
-            const int64_t zl = ((s0 + k) % c->nzl + c->nzl) % c->nzl;
-            std::memcpy(&tmp[((size_t)v * ns + k) * plane], host + (size_t)v * N + (size_t)zl * plane,
-                        plane * 8);
-          }
-      if (mode == 1) {
-        // host points to a 2-element array {rho, u} packed by the caller
-        const double* const* ru = reinterpret_cast<const double* const*>(host);
-        for (int64_t k = 0; k < ns; ++k) {
-          const int64_t zl = ((s0 + k) % c->nzl + c->nzl) % c->nzl;
-          for (size_t i = 0; i < plane; ++i) {
-            const size_t src = (size_t)zl * plane + i;
-            tmp[((size_t)0 * ns + k) * plane + i] = ru[0] ? ru[0][src] : 1.0;
-            for (int a = 0; a < 3; ++a)
-              tmp[((size_t)(a + 1) * ns + k) * plane + i] = ru[1] ? ru[1][a * N + src] : 0.0;
-          }
-        }
-      }
-      CUDA_TRY(c, cudaMemcpyAsync(c->stage, tmp.data(), tmp.size() * 8, cudaMemcpyHostToDevice,
-                                  c->st));
-    }
-    CUDA_TRY(c, launch_write_state(c->Q, c->opt.prec == PSM_F64, p, c->st));
-    c->launches += 1;
-    CUDA_TRY(c, cudaStreamSynchronize(c->st));  // tmp is reused by the next chunk
-  }
-  c->step = 0;
-  c->ft_valid = false;
-  return PSM_OK;
-}
-
-static psm_status state_read(psm_ctx* c, double* f, double* rho, double* u, int64_t zbeg = 0,
-                             int64_t zend = -1) {
-  psm_status s = ensure_mem(c);
-  if (s != PSM_OK) return s;
-  if (zend < 0) zend = c->nzl;
-  const size_t plane = (size_t)c->grid.nx * c->grid.ny;
-  const int mode = f ? 0 : 1;
-  const int nvals = mode == 0 ? c->Q : 4;
-  const size_t per = plane * (size_t)nvals * 8;
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(c->nzl,
-                                                              (int64_t)(c->stage_bytes / per)));
-  const void* arr = (c->opt.pattern == PSM_TWO_ARRAY) ? c->A[c->cur] : c->A[0];
-  const size_t N = (size_t)(zend - zbeg) * plane;
-  std::vector<double> tmp;
-  for (int64_t za = zbeg; za < zend; za += chunk) {
-    const int64_t zb = std::min<int64_t>(zend, za + chunk);
-    StateParams p{};
-    p.g = c->geom;
-    p.A = const_cast<void*>(arr);
-    p.stage = c->stage;
-    p.za = (int)za;
-    p.zb = (int)zb;
-    p.stage_z0 = (int)za;
-    p.stage_nz = (int)(zb - za);
-    for (int a = 0; a < 3; ++a) p.u_in[a] = c->u_in[a];
-    p.rho_out = c->rho_out;
-    p.pattern = c->opt.pattern == PSM_AA ? 1 : 0;
-    p.odd = (int)(c->step & 1);
-    p.mode = mode;
-    CUDA_TRY(c, launch_read_state(c->Q, c->opt.prec == PSM_F64, p, c->st));
-    c->launches += 1;
-    const size_t nz = (size_t)(zb - za);
-    tmp.resize(nz * plane * nvals);
-    CUDA_TRY(c, cudaMemcpyAsync(tmp.data(), c->stage, tmp.size() * 8, cudaMemcpyDeviceToHost,
-                                c->st));
-    CUDA_TRY(c, cudaStreamSynchronize(c->st));
-    for (int v = 0; v < nvals; ++v) {
-      const double* src = &tmp[(size_t)v * nz * plane];
-      const size_t o = (size_t)(za - zbeg) * plane;
-      if (mode == 0) {
-        std::memcpy(f + (size_t)v * N + o, src, nz * plane * 8);
-      } else if (v == 0) {
-        if (rho) std::memcpy(rho + o, src, nz * plane * 8);
-      } else if (u) {
-        std::memcpy(u + (size_t)(v - 1) * N + o, src, nz * plane * 8);
-      }
-    }
-  }
-  return PSM_OK;
 }
 
 // ----------------------------------------------------------------------------- ABI --------
@@ -1119,6 +62,8 @@ static void ft_store(psm_ctx* c, const std::vector<int>& ids) {
     std::memcpy(c->ft[ids[i]], c->pinned + i * kSlotVals, kSlotVals * 8);
   c->ft_valid = true;
 }
+
+}  // namespace
 
 extern "C" {
 
@@ -1236,7 +181,7 @@ psm_status psm_destroy(psm_ctx* c) {
 
 psm_status psm_required_bytes(const psm_ctx* c, size_t* bytes) {
   if (!c || !bytes) FAIL((psm_ctx*)nullptr, PSM_E_ARG, "null argument");
-  *bytes = make_plan(c).total;
+  *bytes = plan_total_bytes(c);
   return PSM_OK;
 }
 
@@ -1606,155 +551,6 @@ psm_status psm_map_fractions(psm_ctx* c) {
   for (int id = 1; id <= kMaxBodies; ++id)
     if (c->bodies[id].present) ids.push_back(id);
   return remap(c, ids, c->step);
-}
-
-// Fused halo setup (collective over the ranks, once): exchange CUDA IPC handles of every rank's
-// device memory through NCCL, check peer access to both z neighbours on every rank, open the
-// neighbours' memory.  Any failure anywhere keeps the NCCL send/recv halo on all ranks.
-struct P2PInfo {
-  cudaIpcMemHandle_t h;
-  unsigned long long off_A0, off_A1, off_flags;
-  long long nzl, qstride;
-  int dev, ok;
-};
-
-static psm_status ensure_p2p(psm_ctx* c) {
-  if (c->p2p_checked) return PSM_OK;
-  c->p2p_checked = true;
-  if (c->world == 1 || c->opt.pattern != PSM_TWO_ARRAY) return PSM_OK;
-  const char* env = std::getenv("PSM_HALO");
-  const bool want = !(env && std::strcmp(env, "nccl") == 0);
-  const int P = c->world, r = c->rank;
-  const bool zwall = c->grid.bc[2] == PSM_WALL;
-  const int up = (r + 1) % P, dn = (r - 1 + P) % P;
-  c->has_up = !(zwall && r == P - 1);
-  c->has_dn = !(zwall && r == 0);
-  P2PInfo mine;
-  std::memset(&mine, 0, sizeof(mine));
-  CUDA_TRY(c, cudaGetDevice(&mine.dev));
-  // base of the allocation that holds the context memory (it may be a sub-block of a caller's
-  // allocation, psm_bind_memory): driver cuMemGetAddressRange through the runtime entry point
-  unsigned long long base = 0;
-  size_t size = 0;
-  typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (want && cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) ==
-                  cudaSuccess && fn && q == cudaDriverEntryPointSuccess &&
-      reinterpret_cast<GetRange>(fn)(&base, &size, (unsigned long long)c->mem) == 0 &&
-      cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)) == cudaSuccess) {
-    const unsigned long long m = (unsigned long long)c->mem;
-    mine.off_A0 = (unsigned long long)c->A[0] - base;
-    mine.off_A1 = (unsigned long long)c->A[1] - base;
-    mine.off_flags = (unsigned long long)c->flags - base;
-    (void)m;
-    mine.ok = 1;
-  }
-  cudaGetLastError();
-  mine.nzl = c->nzl;
-  mine.qstride = c->geom.qstride;
-  std::vector<P2PInfo> all(P);
-  char* d = nullptr;
-  CUDA_TRY(c, cudaMalloc(&d, sizeof(P2PInfo) * (P + 1)));
-  CUDA_TRY(c, cudaMemcpyAsync(d, &mine, sizeof(mine), cudaMemcpyHostToDevice, c->st));
-  NCCL_TRY(c, ncclAllGather(d, d + sizeof(P2PInfo), sizeof(P2PInfo), ncclChar, c->comm, c->st));
-  CUDA_TRY(c, cudaMemcpyAsync(all.data(), d + sizeof(P2PInfo), sizeof(P2PInfo) * P,
-                              cudaMemcpyDeviceToHost, c->st));
-  CUDA_TRY(c, cudaStreamSynchronize(c->st));
-  // every rank must be able to reach both its neighbours
-  int ok = 1;
-  for (int k = 0; k < P; ++k) ok &= all[k].ok;
-  if (ok) {
-    for (int nb : {up, dn}) {
-      if (nb == r) continue;
-      int can = 0;
-      if (all[nb].dev == mine.dev) can = 1;  // same device (two ranks on one GPU): IPC works
-      else if (cudaDeviceCanAccessPeer(&can, mine.dev, all[nb].dev) != cudaSuccess) can = 0;
-      ok &= can;
-    }
-  }
-  int* dok = reinterpret_cast<int*>(d);
-  CUDA_TRY(c, cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, c->st));
-  NCCL_TRY(c, ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->comm, c->st));
-  CUDA_TRY(c, cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  CUDA_TRY(c, cudaStreamSynchronize(c->st));
-  cudaFree(d);
-  if (!ok || up == r) return PSM_OK;
-  auto open = [&](int nb, void** out) -> bool {
-    if (cudaIpcOpenMemHandle(out, all[nb].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-      cudaGetLastError();
-      *out = nullptr;
-      return false;
-    }
-    return true;
-  };
-  bool good = true;
-  if (c->has_up) good &= open(up, &c->ipc_up);
-  if (c->has_dn) {
-    if (dn == up && c->has_up) c->ipc_dn = c->ipc_up;
-    else good &= open(dn, &c->ipc_dn);
-  }
-  // all ranks must agree again (an open can fail)
-  int g = good ? 1 : 0;
-  CUDA_TRY(c, cudaMalloc(&dok, sizeof(int)));
-  CUDA_TRY(c, cudaMemcpyAsync(dok, &g, sizeof(int), cudaMemcpyHostToDevice, c->st));
-  NCCL_TRY(c, ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->comm, c->st));
-  CUDA_TRY(c, cudaMemcpyAsync(&g, dok, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  CUDA_TRY(c, cudaStreamSynchronize(c->st));
-  cudaFree(dok);
-  if (!g) return PSM_OK;  // (opened handles are closed in psm_destroy)
-  if (c->has_up) {
-    char* b = static_cast<char*>(c->ipc_up);
-    c->up_A[0] = b + all[up].off_A0;
-    c->up_A[1] = b + all[up].off_A1;
-    c->up_qs = all[up].qstride;
-    c->up_flag = reinterpret_cast<unsigned long long*>(b + all[up].off_flags) + 0;
-  }
-  if (c->has_dn) {
-    char* b = static_cast<char*>(c->ipc_dn);
-    c->dn_A[0] = b + all[dn].off_A0;
-    c->dn_A[1] = b + all[dn].off_A1;
-    c->dn_qs = all[dn].qstride;
-    c->dn_nzl = all[dn].nzl;
-    c->dn_flag = reinterpret_cast<unsigned long long*>(b + all[dn].off_flags) + 1;
-  }
-  c->p2p = true;
-  return PSM_OK;
-}
-
-// Remap-ahead (prescribed motion only): enqueue the remap for step `next` into the spare buffer
-// on map_st, after the collide that last read that buffer (ev_coll); ev_map marks completion.
-// The remap is latency/ALU-bound and the collide HBM-bound, so the two overlap.
-static psm_status remap_ahead(psm_ctx* c, int64_t next) {
-  CUDA_TRY(c, cudaStreamWaitEvent(c->map_st, c->ev_coll, 0));
-  swap_buffers(c);
-  c->mst = c->map_st;
-  std::vector<int> ids;
-  if (!c->alt_valid) {  // start the spare buffer from scratch: every body mapped afresh
-    CUDA_TRY(c, cudaMemsetAsync(c->word, 0, (size_t)c->ncell_local * 4, c->mst));
-    CUDA_TRY(c, cudaMemsetAsync(c->tile_flag, 0, (size_t)c->ntiles, c->mst));
-    for (int id = 1; id <= kMaxBodies; ++id) {
-      const int sl = c->bodies[id].ms.slot;
-      c->bodies[id].ms = MapState();
-      c->bodies[id].ms.slot = sl;
-      if (c->bodies[id].present) ids.push_back(id);
-    }
-    c->alt_valid = true;
-  } else {
-    for (int id = 1; id <= kMaxBodies; ++id) {
-      const Body& b = c->bodies[id];
-      if (b.present && b.ms.mapped_step != next &&
-          (b.moving || b.ms.mapped_step < 0))
-        ids.push_back(id);
-    }
-  }
-  psm_status st = PSM_OK;
-  if (!ids.empty()) st = remap(c, ids, next);
-  c->mst = c->st;
-  swap_buffers(c);
-  if (st != PSM_OK) return st;
-  CUDA_TRY(c, cudaEventRecord(c->ev_map, c->map_st));
-  return PSM_OK;
 }
 
 psm_status psm_step(psm_ctx* c, int64_t n) {
