@@ -92,7 +92,7 @@ typedef struct {
  * collective: every rank must reach it.  Rank r owns global z in [r*nz/world, (r+1)*nz/world).
  * Errors: PSM_E_ARG if tau <= 1/2 or non-finite (Eq.(2): tau is the relaxation time and the
  * viscosity (tau-1/2)/3 must be positive), any extent < 1, nz < world, or an unknown enum;
- * PSM_E_UNSUPPORTED for body_force with PSM_AA or world > 1 with PSM_AA.
+ * PSM_E_UNSUPPORTED for body_force with PSM_AA, or world > 1 with PSM_AA and a non-periodic x axis.
  * Ownership: *out is owned by the caller and released with psm_destroy. */
 psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
                       const psm_options* opt, psm_ctx** out);

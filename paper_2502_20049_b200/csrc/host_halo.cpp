@@ -33,6 +33,60 @@ psm_status halo(psm_ctx* c, void* arr, cudaStream_t hst) {
   return PSM_OK;
 }
 
+// AA pattern across ranks (ghost planes, NCCL): the even step is local; the odd step reads
+// A[ibar][x - c_i] and writes A[i][x + c_i], so it reaches one plane into each neighbour.
+//   after an even step: the boundary planes the neighbours' odd step will read go into their
+//     ghost planes (top plane, c_z = -1 directions, up; bottom plane, c_z = +1, down);
+//   after an odd step: what this rank's odd step wrote into its ghost planes belongs to the
+//     neighbours' boundary planes (ghost below, c_z = -1, down; ghost above, c_z = +1, up).
+// A ghost slot whose source cell would lie beyond a y wall is not written by this rank's odd
+// step (the neighbour bounces that population into its own slot), so the second copy skips that
+// row: planes of directions with c_y = +1 start at row 1, with c_y = -1 end at row ny-2 — still
+// contiguous.  (x walls would need strided copies; psm_create rejects them with AA across ranks.)
+psm_status halo_aa(psm_ctx* c, bool after_odd, cudaStream_t hst) {
+  if (c->world == 1) return PSM_OK;
+  const int P = c->world, r = c->rank;
+  const bool zwall = c->grid.bc[2] == PSM_WALL;
+  const int up = (r + 1) % P, down = (r - 1 + P) % P;
+  const bool has_up = !(zwall && r == P - 1), has_down = !(zwall && r == 0);
+  const size_t plane = (size_t)c->grid.nx * c->grid.ny;
+  const ncclDataType_t dt = (c->opt.prec == PSM_F64) ? ncclFloat64 : ncclFloat32;
+  char* base = static_cast<char*>(c->A[0]);
+  auto ptr = [&](int q, int64_t zs) {
+    return base + ((size_t)q * (size_t)c->geom.qstride + (size_t)zs * plane) * c->S;
+  };
+  const int64_t top = c->nzl, bot = 1, gdn = 0, gup = c->nzl + 1;
+  const bool ywall = c->grid.bc[1] == PSM_WALL;
+  const size_t nx = (size_t)c->grid.nx;
+  NCCL_TRY(c, ncclGroupStart());
+  for (int q = 0; q < c->Q; ++q) {
+    const int cz = stc_z(q), cy = stc_y(q);
+    // rows of the second (after-odd) copy: all, or all but the row beyond the y wall
+    const size_t r0 = (after_odd && ywall && cy > 0) ? nx : 0;
+    const size_t cnt = (after_odd && ywall && cy != 0) ? plane - nx : plane;
+    auto at = [&](int64_t zs) { return ptr(q, zs) + r0 * c->S; };
+    if (cz < 0) {
+      if (!after_odd) {
+        if (has_up) NCCL_TRY(c, ncclSend(ptr(q, top), plane, dt, up, c->comm, hst));
+        if (has_down) NCCL_TRY(c, ncclRecv(ptr(q, gdn), plane, dt, down, c->comm, hst));
+      } else {
+        if (has_down) NCCL_TRY(c, ncclSend(at(gdn), cnt, dt, down, c->comm, hst));
+        if (has_up) NCCL_TRY(c, ncclRecv(at(top), cnt, dt, up, c->comm, hst));
+      }
+    } else if (cz > 0) {
+      if (!after_odd) {
+        if (has_down) NCCL_TRY(c, ncclSend(ptr(q, bot), plane, dt, down, c->comm, hst));
+        if (has_up) NCCL_TRY(c, ncclRecv(ptr(q, gup), plane, dt, up, c->comm, hst));
+      } else {
+        if (has_up) NCCL_TRY(c, ncclSend(at(gup), cnt, dt, up, c->comm, hst));
+        if (has_down) NCCL_TRY(c, ncclRecv(at(bot), cnt, dt, down, c->comm, hst));
+      }
+    }
+  }
+  NCCL_TRY(c, ncclGroupEnd());
+  return PSM_OK;
+}
+
 // Fused halo setup (collective over the ranks, once): exchange CUDA IPC handles of every rank's
 // device memory through NCCL, check peer access to both z neighbours on every rank, open the
 // neighbours' memory.  Any failure anywhere keeps the NCCL send/recv halo on all ranks.

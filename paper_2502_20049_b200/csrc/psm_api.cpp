@@ -99,10 +99,10 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
                      opt->body_force[2] != 0.0;
   if (force && opt->pattern == PSM_AA)
     FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "body force needs PSM_TWO_ARRAY");
-  if (world > 1 && opt->pattern == PSM_AA)
-    FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "multi-rank runs need PSM_TWO_ARRAY");
   if (opt->collision == PSM_CUMULANT && (stencil != PSM_D3Q27 || force))
     FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "the cumulant operator needs D3Q27 and no body force");
+  if (world > 1 && opt->pattern == PSM_AA && grid->bc[0] != PSM_PERIODIC)
+    FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "PSM_AA across ranks needs a periodic x axis");
   if (world > 1 && !opt->nccl_unique_id)
     FAIL((psm_ctx*)nullptr, PSM_E_ARG, "world > 1 needs an ncclUniqueId");
   psm_ctx* c = new (std::nothrow) psm_ctx();
@@ -676,7 +676,7 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
                                     c->has_dn ? c->dn_flag : nullptr, c->epoch, c->st));
       c->launches += (c->epoch > 1) ? 3 : 2;
       c->cur ^= 1;
-    } else if (c->world == 1 || gz < 3) {
+    } else if (c->world == 1 || gz < 3 || c->opt.pattern == PSM_AA) {
       if (record(c, 1, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
       p.tz0 = 0;
       CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, gz, c->st));
@@ -685,7 +685,8 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
       if (c->opt.pattern == PSM_TWO_ARRAY) c->cur ^= 1;
       if (c->world > 1) {
         if (record(c, 3, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
-        st = halo(c, c->A[c->cur], c->st);
+        st = (c->opt.pattern == PSM_AA) ? halo_aa(c, pat == 2, c->st)
+                                        : halo(c, c->A[c->cur], c->st);
         if (st != PSM_OK) return st;
         if (record(c, 3, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
       }

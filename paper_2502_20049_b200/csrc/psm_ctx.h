@@ -218,6 +218,7 @@ psm_status state_read(psm_ctx* c, double* f, double* rho, double* u, int64_t zbe
                       int64_t zend = -1);
 // host_halo.cpp
 psm_status halo(psm_ctx* c, void* arr, cudaStream_t hst);
+psm_status halo_aa(psm_ctx* c, bool after_odd, cudaStream_t hst);
 psm_status ensure_p2p(psm_ctx* c);
 // host_remap.cpp
 psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes);

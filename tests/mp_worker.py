@@ -25,10 +25,13 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     failures = []
-    for (bc, Q, prec, coll) in [((0, 0, 0), 19, "f64", "srt"), ((0, 1, 1), 27, "f64", "srt"),
-                                ((0, 0, 0), 19, "f32", "srt"),
-                                ((2, 1, 0), 19, "f64", "srt"),  # open x faces (A30) + y walls
-                                ((0, 0, 1), 27, "f64", "cumulant"), ((0, 1, 0), 19, "f64", "trt")]:
+    for (bc, Q, prec, coll, pattern) in [
+            ((0, 0, 0), 19, "f64", "srt", "two_array"), ((0, 1, 1), 27, "f64", "srt", "two_array"),
+            ((0, 0, 0), 19, "f32", "srt", "two_array"),
+            ((2, 1, 0), 19, "f64", "srt", "two_array"),  # open x faces (A30) + y walls
+            ((0, 0, 1), 27, "f64", "cumulant", "two_array"),
+            ((0, 1, 0), 19, "f64", "trt", "two_array"),
+            ((0, 0, 0), 19, "f64", "srt", "aa"), ((0, 1, 1), 27, "f32", "srt", "aa")]:
         # an ncclUniqueId serves exactly one communicator: a fresh one per context
         idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
@@ -37,7 +40,7 @@ def main():
         dist.broadcast(idt, 0)
         nid = bytes(idt.cpu().numpy().tobytes())
         nx, ny, nz = 40, 36, 16 * world + 6
-        kw = dict(Q=Q, tau=0.7, bc=bc, prec=prec, sc=1, bmode=1, collision=coll)
+        kw = dict(Q=Q, tau=0.7, bc=bc, prec=prec, sc=1, bmode=1, collision=coll, pattern=pattern)
         dsim = psm.Simulation(nx, ny, nz, rank=rank, world=world, nccl_id=nid, **kw)
         ref = psm.Simulation(nx, ny, nz, **kw)
         if bc[0] == 2:
@@ -64,13 +67,14 @@ def main():
                 Fd, Td, _, _ = dsim.force_torque(b)
                 if not (np.all(np.abs(Fr - Fd) <= 1e-12 * np.maximum(np.abs(Fr), aF)) and
                         np.all(np.abs(Tr - Td) <= 1e-12 * np.maximum(np.abs(Tr), aT))):
-                    failures.append(f"F/T body {b} {bc} Q{Q} {prec}: {Fr} {Fd} {Tr} {Td}")
+                    failures.append(f"F/T body {b} {bc} Q{Q} {prec} {pattern}: {Fr} {Fd} {Tr} {Td}")
         if rank == 0:
-            print(f"halo mode {psm.psm_halo_mode(dsim.ctx)} ({bc} Q{Q} {prec} {coll})", flush=True)
+            print(f"halo mode {psm.psm_halo_mode(dsim.ctx)} ({bc} Q{Q} {prec} {coll} {pattern})",
+                  flush=True)
         fr = ref.pdfs()[:, z0:z0 + nzl]
         fd = dsim.pdfs()
         if not np.array_equal(fr, fd):
-            failures.append(f"pdfs {bc} Q{Q} {prec}: max diff {np.max(np.abs(fr - fd))}")
+            failures.append(f"pdfs {bc} Q{Q} {prec} {pattern}: max diff {np.max(np.abs(fr - fd))}")
         cr = ref.fractions()[2][z0:z0 + nzl]
         if not np.array_equal(cr, dsim.fractions()[2]):
             failures.append(f"fractions {bc} Q{Q} {prec}")
