@@ -73,6 +73,9 @@ def test_create_validation_codes():
         (dict(), _grid(8, 8, 8, (0, 2, 0)), 19, psm.PSM_E_UNSUPPORTED),  # open faces: x only
         (dict(), _grid(2, 8, 8, (2, 0, 0)), 19, psm.PSM_E_UNSUPPORTED),  # nx >= 3
         (dict(pattern=psm.PSM_AA), _grid(8, 8, 8, (2, 0, 0)), 19, psm.PSM_E_UNSUPPORTED),
+        # AA across ranks needs a periodic x axis
+        (dict(pattern=psm.PSM_AA, world=2, rank=0), _grid(8, 8, 8, (1, 0, 0)), 19,
+         psm.PSM_E_UNSUPPORTED),
     ]
     for kw, g, q, code in cases:
         with pytest.raises(psm.PSMError) as e:
