@@ -196,6 +196,8 @@ psm_status ensure_pipeline(psm_ctx* c) {
   if (c->map_st) return PSM_OK;
   int lo_prio = 0, hi_prio = 0;
   CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  // highest priority: measured 40.7k vs 40.0k MLUPS (c5w) against the default priority, which
+  // lets the remap start only as the collide drains
   CUDA_TRY(c, cudaStreamCreateWithPriority(&c->map_st, cudaStreamNonBlocking, hi_prio));
   CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_map, cudaEventDisableTiming));
   CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_coll, cudaEventDisableTiming));
