@@ -46,7 +46,7 @@ def lib():
             "orc_collide_cell": (I, [I, P, D, I, D, P, P, P, P]),
             "orc_collide_cell_trt": (I, [I, P, D, D, I, D, P, P, P, P]),
             "orc_set_collision": (None, [P, I, D]),
-            "orc_collide_cell_cum": (I, [I, P, D, I, D, P, P, P]),
+            "orc_collide_cell_cum": (I, [I, P, D, I, D, P, P, P, P]),
             "orc_pose_advance": (None, [P, P, P, P, I64, P, P, P, P]),
             "orc_geometry_extent": (I64, [P, I64, I, P, P]),
             "orc_voxelize": (None, [P, I64, P, I64, I, P]),
@@ -138,14 +138,16 @@ def collide_cell_trt(Q, f, tau, magic, sc, B, us, g=(0.0, 0.0, 0.0)):
     return out, m, err
 
 
-def collide_cell_cum(Q, f, tau, sc, B, us):
-    """One-cell Eq.(4) collision with the cumulant fluid operator (D3Q27)."""
+def collide_cell_cum(Q, f, tau, sc, B, us, g=(0.0, 0.0, 0.0)):
+    """One-cell Eq.(4) collision with the cumulant fluid operator (D3Q27),
+    optional body force g (reading A31)."""
     f = _f64(f)
     us = _f64(us)
+    g = _f64(g)
     out = np.zeros(Q, np.float64)
     m = np.zeros(3, np.float64)
-    err = lib().orc_collide_cell_cum(Q, _p(f), float(tau), int(sc), float(B), _p(us), _p(out),
-                                     _p(m))
+    err = lib().orc_collide_cell_cum(Q, _p(f), float(tau), int(sc), float(B), _p(us), _p(g),
+                                     _p(out), _p(m))
     return out, m, err
 
 

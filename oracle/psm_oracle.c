@@ -153,8 +153,7 @@ int orc_collide_cell_trt(int Q, const double* f, double tau, double magic, int s
 }
 
 int orc_collide_cell_cum(int Q, const double* f, double tau, int sc, double B, const double us[3],
-                         double* fstar, double m[3]) {
-  const double g[3] = {0.0, 0.0, 0.0};
+                         const double g[3], double* fstar, double m[3]) {
   return collide_cell_impl(Q, f, tau, sc, B, us, g, 2, 0.0, fstar, m);
 }
 
@@ -234,6 +233,12 @@ static int collide_cell_impl(int Q, const double* f, double tau, int sc, double 
     ks[1][1][2] = rho * (Czz * Cxy + 2.0 * Cxz * Cyz);
     ks[2][2][2] = rho * (Cxx * Cyy * Czz + 2.0 * (Cxx * Cyz * Cyz + Cyy * Cxz * Cxz +
                                                   Czz * Cxy * Cxy) + 8.0 * Cxy * Cxz * Cyz);
+    /* forcing (reading A31): about u = (j + g/2)/rho the first-order central moments are -g/2
+     * before the collision and +g/2 after it (sign flip), so the post-collision momentum is
+     * j + g; zero without a force */
+    ks[1][0][0] = 0.5 * g[0];
+    ks[0][1][0] = 0.5 * g[1];
+    ks[0][0][1] = 0.5 * g[2];
     /* solve sum_i (c_ix - ux)^a (c_iy - uy)^b (c_iz - uz)^c fc_i = ks[a][b][c] */
     double M[27][28];
     for (int r = 0; r < 27; ++r) {

@@ -346,3 +346,29 @@ def test_cumulant_shear_wave_viscosity_and_galilean_invariance(U0):
     nu = (tau - 0.5) / 3.0
     k = 2 * np.pi / L
     assert abs(-math.log(amp / U) / steps / (nu * k * k) - 1.0) < 0.01
+
+
+def test_cumulant_forcing_momentum_and_poiseuille():
+    """Reading A31: with a body force the first-order central moments about u = (j + g/2)/rho flip
+    sign in the collision, so every cell gains exactly g of momentum (mass unchanged); a forced
+    channel between resting walls gives the Poiseuille parabola (D3Q27 cumulant)."""
+    Q = 27
+    c, w, _ = oracle.stencil(Q)
+    cf = c.astype(float)
+    g = np.array([2e-4, -1e-4, 5e-5])
+    f = pi.random_pdfs(Q, (1,), 64, w=w, amp=0.2)[:, 0]
+    out, _, err = oracle.collide_cell_cum(Q, f, 0.7, 1, 0.0, [0, 0, 0], g=g)
+    assert err == 0
+    assert abs(out.sum() - f.sum()) < 1e-15 * 4
+    assert np.allclose(out @ cf, f @ cf + g, atol=2e-16 * 8, rtol=0)
+    H, tau, gx = 16, 0.8, 1e-6
+    o = oracle.Oracle(1, H, 1, Q, tau, (0, 1, 0), 1, 1)
+    o.set_collision("cumulant")
+    o.init_equilibrium(None, None)
+    o.set_force([gx, 0, 0])
+    o.step(6000)
+    rho, u = o.velocity()
+    ux = u[0, 0, :, 0] + 0.5 * gx / rho[0, :, 0]
+    yc = np.arange(H) + 0.5
+    ref = gx * yc * (H - yc) / (2 * (tau - 0.5) / 3)
+    assert np.max(np.abs(ux - ref)) / ref.max() < 0.02
