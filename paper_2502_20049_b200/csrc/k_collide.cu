@@ -226,9 +226,9 @@ __device__ __forceinline__ void back1d(T k0, T k1, T k2, T v, T& fm, T& f0, T& f
 // order >= 3 and the bulk rate equal to 1, shear rate omega: normalised second cumulants
 // C = kappa / rho relaxed; post-collision central moments are those of a distribution whose
 // cumulants of order >= 3 vanish (Wick products); three 1-D backward transforms give f*.
-template <typename T>
+template <typename T, bool FORCE = false>
 __device__ __forceinline__ void cumulant_update(T (&f)[27], T rho, T jx, T jy, T jz, T ux, T uy,
-                                                T uz, T om) {
+                                                T uz, T om, const T (&g)[3]) {
   T mxx = T(0), myy = T(0), mzz = T(0), mxy = T(0), mxz = T(0), myz = T(0);
 #pragma unroll
   for (int q = 0; q < 27; ++q) {
@@ -241,12 +241,30 @@ __device__ __forceinline__ void cumulant_update(T (&f)[27], T rho, T jx, T jy, T
     if (cy * cz > 0) myz += f[q]; else if (cy * cz < 0) myz -= f[q];
   }
   const T ir = T(1) / rho;
-  const T Cxx0 = (mxx - ux * jx) * ir, Cyy0 = (myy - uy * jy) * ir, Czz0 = (mzz - uz * jz) * ir;
+  // second central moments about u: m_ab - u_a j_b - u_b j_a + rho u_a u_b, which is
+  // m_ab - u_a j_b for u = j / rho; with a force u = (j + g/2)/rho (reading A31) and j_b is
+  // replaced by j_b - g_b/2 in the first form
+  T Cxx0, Cyy0, Czz0, Kxy, Kxz, Kyz;
+  if constexpr (FORCE) {
+    const T hx = T(0.5) * g[0], hy = T(0.5) * g[1], hz = T(0.5) * g[2];
+    Cxx0 = (mxx - ux * (jx - hx)) * ir;
+    Cyy0 = (myy - uy * (jy - hy)) * ir;
+    Czz0 = (mzz - uz * (jz - hz)) * ir;
+    Kxy = mxy - ux * jy + uy * hx;
+    Kxz = mxz - ux * jz + uz * hx;
+    Kyz = myz - uy * jz + uz * hy;
+  } else {
+    Cxx0 = (mxx - ux * jx) * ir;
+    Cyy0 = (myy - uy * jy) * ir;
+    Czz0 = (mzz - uz * jz) * ir;
+    Kxy = mxy - ux * jy;
+    Kxz = mxz - ux * jz;
+    Kyz = myz - uy * jz;
+  }
   const T w1 = T(1) - om;
   const T Cs = T(1);  // bulk rate 1: trace at its equilibrium 3 c_s^2
   const T D1 = w1 * (Cxx0 - Cyy0), D2 = w1 * (Cxx0 - Czz0);
-  const T Cxy = w1 * (mxy - ux * jy) * ir, Cxz = w1 * (mxz - ux * jz) * ir,
-          Cyz = w1 * (myz - uy * jz) * ir;
+  const T Cxy = w1 * Kxy * ir, Cxz = w1 * Kxz * ir, Cyz = w1 * Kyz * ir;
   const T Cxx = (Cs + D1 + D2) * T(1.0 / 3.0), Cyy = (Cs - T(2) * D1 + D2) * T(1.0 / 3.0),
           Czz = (Cs + D1 - T(2) * D2) * T(1.0 / 3.0);
   // post-collision central moments k[a][b][c] (orders a, b, c in x, y, z)
@@ -273,6 +291,11 @@ __device__ __forceinline__ void cumulant_update(T (&f)[27], T rho, T jx, T jy, T
   k[2][2][2] = rho * (Cxx * Cyy * Czz +
                       T(2) * (Cxx * Cyz * Cyz + Cyy * Cxz * Cxz + Czz * Cxy * Cxy) +
                       T(8) * Cxy * Cxz * Cyz);
+  if constexpr (FORCE) {  // first-order central moments: -g/2 before, +g/2 after (A31)
+    k[1][0][0] = T(0.5) * g[0];
+    k[0][1][0] = T(0.5) * g[1];
+    k[0][0][1] = T(0.5) * g[2];
+  }
   // backward transforms x, then y, then z (the 1-D transforms commute)
 #pragma unroll
   for (int b = 0; b < 3; ++b)
@@ -460,7 +483,8 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
   const T gpref = T(1) - T(0.5) * om, gmref = T(1) - T(0.5) * omm;
 
   if (!solid_tile) {
-    if constexpr (COLL == 2 && Q == 27) cumulant_update<T>(f, rho, jx, jy, jz, ux, uy, uz, om);
+    if constexpr (COLL == 2 && Q == 27)
+      cumulant_update<T, FORCE>(f, rho, jx, jy, jz, ux, uy, uz, om, gl);
     else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
     else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
   } else {
@@ -515,7 +539,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
 #pragma unroll
         for (int q = 0; q < Q; ++q) stash[q * kTileCells + tid] = f[q];
       }
-      cumulant_update<T>(f, rho, jx, jy, jz, ux, uy, uz, om);
+      cumulant_update<T, FORCE>(f, rho, jx, jy, jz, ux, uy, uz, om, gl);
     }
     if (Bd > 0.0) {
       const T B = T(Bd), B1 = T(1) - T(Bd);
@@ -550,7 +574,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
           oFi = om * (ei - fi);
           oFj = om * (ej - fj);
         }
-        if (FORCE) {
+        if (FORCE && COLL != 2) {  // (the cumulant carries its force in fc, reading A31)
           T sp, sm;
           guo_pair<Q, T>(i, ux, uy, uz, gl, sp, sm);
           oFi += gpref * sp + gmref * sm;
@@ -677,16 +701,17 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
   if (p.trt == 2) {
     // cumulant (D3Q27 only; no forcing): periodic fast path and the general variants
     if constexpr (Q == 27) {
-      if (force) return cudaErrorInvalidValue;
       const size_t sm = (size_t)Q * kTileCells * sizeof(T);  // PSM-cell stash
       static bool attr = false;                             // once per instantiation
       if (!attr) {
-        const void* fns[6] = {(const void*)k_collide<Q, T, 0, true, false, true, 2>,
+        const void* fns[8] = {(const void*)k_collide<Q, T, 0, true, false, true, 2>,
                               (const void*)k_collide<Q, T, 0, false, false, false, 2>,
                               (const void*)k_collide<Q, T, 0, true, false, false, 2>,
                               (const void*)k_collide<Q, T, 0, 2, false, false, 2>,
                               (const void*)k_collide<Q, T, 1, false, false, false, 2>,
-                              (const void*)k_collide<Q, T, 2, true, false, false, 2>};
+                              (const void*)k_collide<Q, T, 2, true, false, false, 2>,
+                              (const void*)k_collide<Q, T, 0, true, true, false, 2>,
+                              (const void*)k_collide<Q, T, 0, true, true, true, 2>};
         for (const void* fn : fns) {
           cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)sm);
@@ -694,7 +719,10 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
         }
         attr = true;
       }
-      if (dbg) k_collide<Q, T, 0, true, false, true, 2><<<grid, block, sm, st>>>(p);
+      // body force (reading A31): general two-array variants only, as for SRT/TRT
+      if (force && dbg) k_collide<Q, T, 0, true, true, true, 2><<<grid, block, sm, st>>>(p);
+      else if (force) k_collide<Q, T, 0, true, true, false, 2><<<grid, block, sm, st>>>(p);
+      else if (dbg) k_collide<Q, T, 0, true, false, true, 2><<<grid, block, sm, st>>>(p);
       else if (pat == 0 && !walls) k_collide<Q, T, 0, false, false, false, 2><<<grid, block, sm, st>>>(p);
       else if (pat == 0 && xonly) k_collide<Q, T, 0, 2, false, false, 2><<<grid, block, sm, st>>>(p);
       else if (pat == 0) k_collide<Q, T, 0, true, false, false, 2><<<grid, block, sm, st>>>(p);

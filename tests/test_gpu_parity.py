@@ -600,3 +600,14 @@ def test_two_way_coupled_light_body_with_virtual_mass():
             assert np.allclose(a, c, rtol=1e-11, atol=1e-14), (k, a, c)
     assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
     assert g.body_state(1)[2][2] < 0  # sinking
+
+
+def test_cumulant_with_body_force():
+    """Cumulant operator with a Guo-type body force (reading A31) in a walled channel with a
+    moving sphere: fp64 <= 1e-12 and F/T every step against the oracle."""
+    o, g = _run_pair(36, 20, 18, 27, 0.7, (0, 1, 0), 2, 1, "f64", "two_array",
+                     [dict(id=1, kind="sphere", r=4.5, s=1, v=(0.02, 0.0, 0.0),
+                           pose=lambda k: (np.eye(3), (12.0 + 0.02 * k, 10.3, 9.1)))],
+                     40, 47, u0=(0.02, 0.0, 0.0), force=(2e-5, 0.0, 1e-5),
+                     collision="cumulant")
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
