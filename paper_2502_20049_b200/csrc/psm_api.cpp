@@ -676,7 +676,7 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
                                     c->has_dn ? c->dn_flag : nullptr, c->epoch, c->st));
       c->launches += (c->epoch > 1) ? 3 : 2;
       c->cur ^= 1;
-    } else if (c->world == 1 || gz < 3 || c->opt.pattern == PSM_AA) {
+    } else if (c->world == 1 || gz < 3) {
       if (record(c, 1, 0) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
       p.tz0 = 0;
       CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, gz, c->st));
@@ -699,7 +699,10 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
       CUDA_TRY(c, launch_collide(c->Q, fp64, p, pat, force, c->dbg, 1, c->st));
       CUDA_TRY(c, cudaEventRecord(c->ev_bnd, c->st));
       CUDA_TRY(c, cudaStreamWaitEvent(c->comm_st, c->ev_bnd, 0));
-      st = halo(c, p.dst, c->comm_st);
+      // (AA: the interior layers neither read nor write the boundary or ghost planes the copies
+      // touch, host_halo.cpp)
+      st = (c->opt.pattern == PSM_AA) ? halo_aa(c, pat == 2, c->comm_st)
+                                      : halo(c, p.dst, c->comm_st);
       if (st != PSM_OK) return st;
       CUDA_TRY(c, cudaEventRecord(c->ev_halo, c->comm_st));
       p.tz0 = 1;
@@ -708,7 +711,7 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
       if (record(c, 1, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
       // the next collide (and any readback) reads the ghost planes: join the halo
       CUDA_TRY(c, cudaStreamWaitEvent(c->st, c->ev_halo, 0));
-      c->cur ^= 1;
+      if (c->opt.pattern == PSM_TWO_ARRAY) c->cur ^= 1;
     }
     if (ahead) CUDA_TRY(c, cudaEventRecord(c->ev_coll, c->st));  // this buffer read: done
     c->step += 1;
