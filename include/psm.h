@@ -267,7 +267,9 @@ psm_status psm_profile_read(psm_ctx* ctx, double ms[PSM_NUM_PHASES],
  * 0 = single rank, 1 = NCCL grouped send/recv after the collide, 2 = fused: the collide kernel
  * stores the outgoing populations straight into the neighbours' ghost planes (peer memory over
  * NVLink, CUDA IPC), with a per-step flag handshake.  2 needs peer access between every pair of
- * neighbours and PSM_TWO_ARRAY; the environment variable PSM_HALO=nccl forces 1. */
+ * neighbours and PSM_TWO_ARRAY; the environment variable PSM_HALO=nccl forces 1.  With 2 a step
+ * waits on the device for both neighbours' previous step, bounded by PSM_P2P_TIMEOUT_S seconds
+ * (default 60); a neighbour that never arrives makes psm_step return PSM_E_NCCL. */
 psm_status psm_halo_mode(const psm_ctx* ctx, int32_t* mode);
 
 /* Size of an ncclUniqueId (128) and a fresh one for rank 0 to broadcast (world > 1). */

@@ -761,10 +761,12 @@ __global__ void k_p2p_signal(unsigned long long* up_flag, unsigned long long* dn
 }
 
 // wait: before the next collide reads the ghost planes (and overwrites the neighbours' other
-// array), both neighbours must have signalled step v; bounded spin (2 s) so a lost peer cannot
-// hang the device — then the error word records it and the step fails
+// array), both neighbours must have signalled step v; bounded spin (default 60 s, host work
+// between steps can legitimately skew the ranks) so a lost peer cannot hang the device — then
+// the error word records it and the step fails
 __global__ void k_p2p_wait(const unsigned long long* from_dn, const unsigned long long* from_up,
-                           unsigned long long v, unsigned long long* err) {
+                           unsigned long long v, unsigned long long* err,
+                           unsigned long long timeout_ns) {
   unsigned long long t0, t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {
@@ -773,7 +775,7 @@ __global__ void k_p2p_wait(const unsigned long long* from_dn, const unsigned lon
     if (from_up) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(b) : "l"(from_up) : "memory");
     if (a >= v && b >= v) return;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 2000000000ull) {
+    if (t - t0 > timeout_ns) {
       atomicExch(err, 1ull);  // the host turns this into PSM_E_NCCL
       return;
     }
@@ -788,8 +790,9 @@ cudaError_t launch_p2p_signal(unsigned long long* up_flag, unsigned long long* d
 }
 
 cudaError_t launch_p2p_wait(const unsigned long long* from_dn, const unsigned long long* from_up,
-                            unsigned long long v, unsigned long long* err, cudaStream_t st) {
-  k_p2p_wait<<<1, 1, 0, st>>>(from_dn, from_up, v, err);
+                            unsigned long long v, unsigned long long* err,
+                            unsigned long long timeout_ns, cudaStream_t st) {
+  k_p2p_wait<<<1, 1, 0, st>>>(from_dn, from_up, v, err, timeout_ns);
   return cudaGetLastError();
 }
 

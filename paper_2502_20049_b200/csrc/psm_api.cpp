@@ -119,6 +119,8 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   c->st = static_cast<cudaStream_t>(opt->cuda_stream);
   c->mst = c->st;
   if (const char* e = std::getenv("PSM_AHEAD_BLOCKS")) c->ahead_blocks = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PSM_P2P_TIMEOUT_S"))
+    c->p2p_timeout_ns = (unsigned long long)(std::max(1.0, std::atof(e)) * 1e9);
   if (const char* e = std::getenv("PSM_AHEAD_THREADS"))
     c->ahead_threads = std::min(1024, std::max(32, std::atoi(e)));
   Geom& g = c->geom;
@@ -655,7 +657,7 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
       if (c->epoch > 0)
         CUDA_TRY(c, launch_p2p_wait(c->has_dn ? c->flags + 0 : nullptr,
                                     c->has_up ? c->flags + 1 : nullptr, c->epoch, c->flags + 2,
-                                    c->st));
+                                    c->p2p_timeout_ns, c->st));
       const int d = c->cur ^ 1;
       const size_t plane = (size_t)c->grid.nx * c->grid.ny;
       p.p2p = 1;
@@ -746,7 +748,7 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
   (void)nb;
   ft_store(c, ids);
   if (c->p2p && herr[1] != 0)
-    FAIL(c, PSM_E_NCCL, "fused halo: a neighbour did not signal its step within 2 s");
+    FAIL(c, PSM_E_NCCL, "fused halo: a neighbour did not signal its step in time (PSM_P2P_TIMEOUT_S)");
   if (*herr != ~0ull) {
     const long long ncell = (long long)c->grid.nx * c->grid.ny * c->grid.nz;
     const long long stp = (long long)(*herr / (unsigned long long)ncell);

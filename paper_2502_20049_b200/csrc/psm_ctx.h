@@ -157,6 +157,7 @@ struct psm_ctx {
   unsigned long long* dn_flag = nullptr;  // the lower neighbour's "from above" flag word
   unsigned long long* flags = nullptr;    // mine: [0] from below, [1] from above, [2] hs error
   unsigned long long epoch = 0;
+  unsigned long long p2p_timeout_ns = 60ull * 1000000000ull;  // handshake bound (PSM_P2P_TIMEOUT_S)
   unsigned char nccl_id[128] = {};
   std::string err_msg;
   int64_t launches = 0;

@@ -17,7 +17,8 @@ cudaError_t launch_collide(int Q, bool fp64, const CollideParams& p, int pat, bo
 cudaError_t launch_p2p_signal(unsigned long long* up_flag, unsigned long long* dn_flag,
                               unsigned long long v, cudaStream_t st);
 cudaError_t launch_p2p_wait(const unsigned long long* from_dn, const unsigned long long* from_up,
-                            unsigned long long v, unsigned long long* err, cudaStream_t st);
+                            unsigned long long v, unsigned long long* err,
+                            unsigned long long timeout_ns, cudaStream_t st);
 
 // k_voxelize.cu — GPU voxeliser (reading A15), writes the packed bricks and the brick flags
 struct VoxParams {
