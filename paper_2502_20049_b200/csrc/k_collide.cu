@@ -702,8 +702,13 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
     // cumulant (D3Q27 only; no forcing): periodic fast path and the general variants
     if constexpr (Q == 27) {
       const size_t sm = (size_t)Q * kTileCells * sizeof(T);  // PSM-cell stash
-      static bool attr = false;                             // once per instantiation
-      if (!attr) {
+      // the >48 KB opt-in is a per-device function attribute: set once per instantiation and
+      // device (bit per device ordinal)
+      static unsigned long long attr_devices = 0;
+      int dev = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
+      const unsigned long long bit = 1ull << (dev & 63);
+      if (!(attr_devices & bit)) {
         const void* fns[8] = {(const void*)k_collide<Q, T, 0, true, false, true, 2>,
                               (const void*)k_collide<Q, T, 0, false, false, false, 2>,
                               (const void*)k_collide<Q, T, 0, true, false, false, 2>,
@@ -717,7 +722,7 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
                                                (int)sm);
           if (e != cudaSuccess) return e;
         }
-        attr = true;
+        attr_devices |= bit;
       }
       // body force (reading A31): general two-array variants only, as for SRT/TRT
       if (force && dbg) k_collide<Q, T, 0, true, true, true, 2><<<grid, block, sm, st>>>(p);
