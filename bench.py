@@ -82,6 +82,10 @@ WORKLOADS = {
                   v=(1.0 / 32.0, 0.0, 0.0), pattern="two_array", sc=1, bmode=1,
                   collision="cumulant",
                   desc="c3-shaped, cumulant: D3Q27 PSM fp64 256^3, moving sphere r=48, s=1"),
+    "c5w27": dict(nx=512, ny=512, nz=512, Q=27, prec="f32", tau=0.55, rotors=True, s=1,
+                  omega=0.05 / 220.0, pattern="two_array", sc=1, bmode=1,
+                  desc="c5 weak, D3Q27: D3Q27 PSM fp32 SRT, 512^3 per GPU, CROR-like rotor pair "
+                       "per GPU, s=1, SC1, weighted B"),
     "c5wcum": dict(nx=512, ny=512, nz=512, Q=27, prec="f32", tau=0.55, rotors=True, s=1,
                    omega=0.05 / 220.0, pattern="two_array", sc=1, bmode=1, collision="cumulant",
                    desc="c5 weak, cumulant: D3Q27 PSM fp32, 512^3 per GPU, CROR-like rotor pair "

@@ -7,7 +7,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; 
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
 rm -f gpurun_out/bench_all.jsonl
-for c in c5app c5wr2 c5wcum c4 c4aa c4f64 c4trt c4dyn c3f64 c3cum; do
+for c in c5app c5wr2 c5w27 c5wcum c4 c4aa c4f64 c4trt c4dyn c3f64 c3cum; do
   timeout 300 python bench.py --config $c --steps 40 --warmup 3 --no-cpu-baseline | sed "s/^/$c /" >> gpurun_out/bench_all.jsonl 2>> gpurun_out/bench_all.err
 done
 PSM_NO_REMAP_AHEAD=1 timeout 300 python bench.py --steps 40 --warmup 3 --no-cpu-baseline --no-e2e | sed "s/^/c5w-noahead /" >> gpurun_out/bench_all.jsonl 2>> gpurun_out/bench_all.err
