@@ -228,10 +228,14 @@ psm_status psm_set_open_boundary(psm_ctx* ctx, const double u_in[3], double rho_
 psm_status psm_map_fractions(psm_ctx* ctx);
 
 /* Advance n time steps.  Each step: pose advance of moving bodies (host), fraction remap of moving
- * bodies (GPU), fused PSM stream-collide Eq.(4) with SRT Eq.(2)-(3) and SC1/2/3 Eqs.(7)-(9) (GPU),
- * per-body force/torque partials Eqs.(10)-(11) (GPU), halo exchange (world > 1).  One D2H copy at
- * the end (error word, force/torque).  PSM_E_STATE if any cell had rho <= 0 or a non-finite value
- * (the first offending step/cell is in psm_last_error()); the state is then undefined. */
+ * bodies (GPU), fused PSM stream-collide Eq.(4) with the context's fluid operator (SRT Eq.(2)-(3),
+ * TRT or cumulant) and SC1/2/3 Eqs.(7)-(9) (GPU), per-body force/torque partials Eqs.(10)-(11)
+ * (GPU), halo exchange (world > 1), and for dynamic bodies the coupling integrator (host, one
+ * synchronisation per step).  With n > 1 and bodies in prescribed motion the remap of step k+1
+ * runs on a second stream while step k collides (results identical to n calls with n = 1).  One
+ * D2H copy at the end (error word, force/torque).  PSM_E_STATE if any cell had rho <= 0 or a
+ * non-finite value (the first offending step/cell is in psm_last_error()); the state is then
+ * undefined.  PSM_E_NCCL if a neighbour rank stopped stepping (fused halo, psm_halo_mode). */
 psm_status psm_step(psm_ctx* ctx, int64_t n);
 
 /* Force and torque ON body `body_id` during the most recent step, lattice units (all ranks
