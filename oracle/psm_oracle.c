@@ -14,9 +14,15 @@
  *   Eq.(6)  tau-weighted B
  *   Eq.(7)-(9) SC1/SC2/SC3          PAPER.md:178-189  (SC2 in its literal printed form, A2)
  *   Eq.(10)-(11) force / torque     PAPER.md:196-204  (returned with the sign ON the body, A6)
- *   Sec. III geometry field + super-sampled fraction mapping, PAPER.md:299-321 (reading R1, A12)
+ *   Sec. III geometry field + super-sampled fraction mapping, PAPER.md:299-321 (reading R1, A12;
+ *           the literal centre-only reading R2 selectable per mesh)
+ * and the NEXT rows built on the same hot path:
+ *   TRT fluid operator (listed; reading A27)
+ *   cumulant fluid operator (readings A29, A31 with a body force)
+ *   velocity inflow / pressure outflow on the x faces (reading A30)
+ *   two-way coupling of dynamic bodies (reading A28, optional virtual mass)
  * The readings taken where the paper is silent or garbled are listed in DESIGN.md §3
- * (A1..A26); each use below names its reading.
+ * (A1..A31); each use below names its reading.
  *
  * State convention (A10): f holds the Eq.(4) state, i.e. the PRE-collision populations
  * f_i(x,t).  One step = collide every cell, then push f*_i(x) to x + c_i.
