@@ -17,6 +17,16 @@
 #include "psm_device.cuh"
 #include "psm_internal.h"
 
+// PSM_BOUNDS_CHECK (test builds only: PSM_NVCC_EXTRA=-DPSM_BOUNDS_CHECK): every element offset a
+// kernel forms off a direction-plane base must stay inside that plane set; compute-sanitizer is
+// not available on the GPU pool, so this is the out-of-bounds check of the parity suite
+#if defined(PSM_BOUNDS_CHECK)
+#include <cassert>
+#define PSM_CHECK_OFF(off, n) assert((long long)(off) >= 0 && (long long)(off) < (long long)(n))
+#else
+#define PSM_CHECK_OFF(off, n) ((void)0)
+#endif
+
 namespace psm {
 
 template <int Q, typename T>
@@ -410,11 +420,14 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
       const T* Aq = static_cast<const T*>(p.srcq[q]);
       const T* Ao = static_cast<const T*>(p.srcq[stc_opp(q)]);
       if (PAT == 0) {
+        PSM_CHECK_OFF(out ? self : src, G.qstride);
         const T* ptr = out ? (Ao + self) : (Aq + src);
         f[q] = ld_stream(ptr);
       } else if (PAT == 1) {
+        PSM_CHECK_OFF(self, G.qstride);
         f[q] = Aq[self];
       } else {
+        PSM_CHECK_OFF(out ? self : src, G.qstride);
         const T* ptr = out ? (Aq + self) : (Ao + src);
         f[q] = *ptr;
       }
@@ -625,6 +638,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
   // neighbours' ghost planes (peer stores over NVLink), replacing the separate exchange ----
   if (PAT == 0 && act && p.p2p) {  // (multi-rank runs are two-array only)
     const int pl = yc * nx + xc;
+    PSM_CHECK_OFF(pl, (long long)nx * ny);
     if (z == G.nzl - 1) {
 #pragma unroll
       for (int q = 0; q < Q; ++q)
@@ -644,6 +658,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
       T* Dq = static_cast<T*>(p.dstq[q]);
       T* Do = static_cast<T*>(p.dstq[stc_opp(q)]);
       if (PAT == 0) {
+        PSM_CHECK_OFF(self, G.qstride);
         Dq[self] = f[q];  // default write-back policy: measured 0.9 % faster than __stcs (c5w)
       } else if (PAT == 1) {
         Do[self] = f[q];
@@ -651,6 +666,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
         // destination x + c_q == source position of the opposite direction
         const int cx = 1 - stc_x(q), cy = 1 - stc_y(q), cz = 1 - stc_z(q);
         const bool out = WALLS && (OUTX[cx] || OUTY[cy] || OUTZ[cz]);
+        PSM_CHECK_OFF(out ? self : RB[cy][cz] + OX[cx], G.qstride);
         T* ptr = out ? (Do + self) : (Dq + (RB[cy][cz] + OX[cx]));
         *ptr = f[q];
       }

@@ -15,6 +15,8 @@
 // Every early decision is conservative (it only claims "all sub-samples outside/inside" when the
 // brick flags prove it), so the words equal the brute-force counts bit for bit.  Tile flags ("any word nonzero") are
 // reset for every tile that reaches L1 and set by whichever level writes a nonzero word.
+#include <cassert>
+
 #include "psm_device.cuh"
 #include "psm_internal.h"
 #include "psm_map_common.cuh"
@@ -33,6 +35,10 @@ __device__ __forceinline__ void tile_coords(int t, const Geom& G, int& tx, int& 
 
 __device__ __forceinline__ void put_word(const RemapParams& r, int x, int y, int z, uint32_t w,
                                          int tile) {
+#if defined(PSM_BOUNDS_CHECK)
+  assert(x >= 0 && x < r.g.nx && y >= 0 && y < r.g.ny && z >= 0 && z < r.g.nzl);
+  assert(tile >= 0 && tile < r.g.gx * r.g.gy * r.g.gz);
+#endif
   r.word[((long long)z * r.g.ny + y) * r.g.nx + x] = w;
   if (w) r.tile_flag[tile] = 1;
 }
