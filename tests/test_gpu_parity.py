@@ -611,3 +611,21 @@ def test_cumulant_with_body_force():
                      40, 47, u0=(0.02, 0.0, 0.0), force=(2e-5, 0.0, 1e-5),
                      collision="cumulant")
     assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_degenerate_one_cell_thick_grids(prec):
+    """Edge case: extents of 1 (the periodic neighbour of a cell is itself) and a ragged y/z:
+    a forced 1 x 37 x 1 channel between walls, and a 1 x 1 x 1 periodic box, against the oracle."""
+    tol = F64_TOL if prec == "f64" else F32_TOL
+    for (nx, ny, nz, bc) in [(1, 37, 1, (0, 1, 0)), (1, 1, 1, (0, 0, 0)), (3, 5, 2, (0, 0, 1))]:
+        rho, u = pi.perturbed_flow((nz, ny, nx), 91, u0=(0.01, 0.0, 0.0))
+        o = oracle.Oracle(nx, ny, nz, 19, 0.8, bc, 1, 1)
+        o.set_force((1e-5, 0.0, 0.0))
+        g = _sim(nx=nx, ny=ny, nz=nz, Q=19, tau=0.8, bc=bc, prec=prec, sc=1, bmode=1,
+                 body_force=(1e-5, 0.0, 0.0))
+        o.init_equilibrium(rho, u)
+        g.init_equilibrium(rho, u)
+        o.step(50)
+        g.step(50)
+        assert np.max(np.abs(o.pdfs() - g.pdfs())) <= tol, (nx, ny, nz, bc)
