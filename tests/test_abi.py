@@ -181,3 +181,17 @@ def test_struct_layouts_match_the_c_compiler(tmp_path):
         assert int(out[st]) == C.sizeof(cls), st
         for f in fields:
             assert int(out[f"{st}.{f}"]) == getattr(cls, f).offset, (st, f)
+
+
+def test_size_limits_are_checked_host_side():
+    """Maximum sizes: a local slab beyond 32-bit in-plane indexing (2^31 cells per direction
+    plane set; the limit is per rank) is rejected at psm_create with PSM_E_ARG; the largest
+    bench grid (c5 strong, 1.015e9 cells) fits one rank."""
+    with pytest.raises(psm.PSMError) as e:
+        psm.psm_create(_grid(2048, 2048, 600), 19, 0.6, _opts(prec=psm.PSM_F32))
+    assert e.value.code == psm.PSM_E_ARG
+    ctx = psm.psm_create(_grid(2048, 704, 704), 19, 0.55, _opts(prec=psm.PSM_F32))
+    try:
+        assert psm.psm_required_bytes(ctx) > 150e9  # two fp32 D3Q19 arrays of 1.015e9 cells
+    finally:
+        psm.psm_destroy(ctx)
