@@ -351,11 +351,9 @@ __device__ __forceinline__ T ld_stream(const T* p) {
 template <int Q, typename T, int PAT, int COLL>
 constexpr int collide_min_blocks() {
   // the cumulant keeps a 3x3x3 moment array live (PSM cells stash f in shared memory instead of
-  // registers): two fp64 blocks (a few spilled words), three fp32 blocks (AA odd: two)
-#ifndef PSM_CUM32_BLOCKS
-#define PSM_CUM32_BLOCKS 3
-#endif
-  if (COLL == 2) return sizeof(T) == 8 ? 2 : (PAT == 2 ? 2 : PSM_CUM32_BLOCKS);
+  // registers): two fp64 blocks (a few spilled words), four fp32 blocks (148 B of spills, but
+  // measured 1.4 % faster than three on c5wcum), AA odd two
+  if (COLL == 2) return sizeof(T) == 8 ? 2 : (PAT == 2 ? 2 : 4);
   // the AA odd step keeps the scatter offsets live as well: one block less for fp32
   // (AA odd at 4 fp32 blocks spills 68 B and measured 7 % slower)
   return sizeof(T) == 8 ? 2 : (Q == 19 ? (PAT == 2 ? 3 : 4) : (PAT == 2 ? 2 : 3));
