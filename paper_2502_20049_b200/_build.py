@@ -27,8 +27,18 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
+STAMP = LIB + ".flags"  # the extra nvcc flags the library was built with (PSM_NVCC_EXTRA)
+
+
+def _extra() -> str:
+    return os.environ.get("PSM_NVCC_EXTRA", "").strip()
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
+        return True
+    built = open(STAMP).read().strip() if os.path.exists(STAMP) else ""
+    if built != _extra():  # e.g. a PSM_BOUNDS_CHECK build must not be reused silently
         return True
     t = os.path.getmtime(LIB)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(
@@ -39,22 +49,43 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     nccl = nccl_dir()
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, "-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
-           "-Xcompiler", "-fPIC,-fopenmp,-O2", "-shared", "-Xptxas", "-warn-spills",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-I", os.path.join(nccl, "include"),
-           "-o", LIB + ".tmp"] + sources() + [
-           "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
-           "-Xlinker", "-rpath," + os.path.join(nccl, "lib"), "-lgomp"]
-    extra = os.environ.get("PSM_NVCC_EXTRA")  # tuning experiments only, e.g. -DPSM_CUM32_BLOCKS=4
-    if extra:
-        cmd[1:1] = extra.split()
+    extra = _extra()  # diagnostics only, e.g. -DPSM_BOUNDS_CHECK (device-side bounds asserts)
+    flags = [nvcc, "-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
+             "-Xcompiler", "-fPIC,-fopenmp,-O2", "-Xptxas", "-warn-spills",
+             "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+             "-I", os.path.join(nccl, "include")] + extra.split()
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    objs, cmds = [], []
+    for src in sources():  # one nvcc per translation unit, in parallel
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        cmds.append(flags + ["-c", src, "-o", obj])
+
+    def run(cmd):
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        return subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(run, cmds))
+    for cmd, r in zip(cmds, results):
+        if r.stderr:
+            sys.stderr.write(r.stderr)
+        if r.returncode != 0:
+            raise subprocess.CalledProcessError(r.returncode, cmd, r.stdout, r.stderr)
+    link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp"] + \
+        objs + ["-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
+                "-Xlinker", "-rpath," + os.path.join(nccl, "lib"), "-lgomp"]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True)
     os.replace(LIB + ".tmp", LIB)
+    with open(STAMP, "w") as fh:
+        fh.write(extra + "\n")
     return LIB
 
 

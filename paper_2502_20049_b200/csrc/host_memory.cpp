@@ -52,6 +52,8 @@ static Plan make_plan(const psm_ctx* c) {
   // narrow-band remap lists (k_remap.cu); overflow is handled in-kernel (serial fallback)
   p.seg_cap = (int)std::min<int64_t>(32 * c->ntiles, 1 << 22);
   p.band_cap = (int)std::min<int64_t>(c->ncell_local, 1 << 23);
+  if (c->seg_cap_env > 0) p.seg_cap = (int)std::min<int64_t>(p.seg_cap, c->seg_cap_env);
+  if (c->band_cap_env > 0) p.band_cap = (int)std::min<int64_t>(p.band_cap, c->band_cap_env);
   p.off_rcnt = take(4 * sizeof(int));
   p.off_rtiles = take((size_t)c->ntiles * 4);
   p.off_rsegs = take((size_t)p.seg_cap * 4);

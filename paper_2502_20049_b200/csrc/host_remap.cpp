@@ -83,7 +83,7 @@ psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
   }
   mp.stats = dstats;
   if (record(c, 0, 0, c->mst) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
-  static const bool force_general = std::getenv("PSM_REMAP_GENERAL") != nullptr;
+  const bool force_general = c->force_general;
   // cached bands: bodies rebuilt in single-body boxes only; capacity = every cell of their boxes
   size_t need[kMaxBodies + 1] = {};
   int nsingle[kMaxBodies + 1] = {}, ngeneral[kMaxBodies + 1] = {};
@@ -239,10 +239,7 @@ bool boxes_overlap(const psm_ctx* c, const Body& b, const std::vector<Box>& boxe
 // a valid cached band that has moved less than one cell since the band was built (and whose box
 // no other remapped body touches) only re-runs the exact pass over its band.
 psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
-  static const bool no_cache = [] {
-    const char* e = std::getenv("PSM_BAND_CACHE");
-    return e && std::strcmp(e, "0") == 0;
-  }();
+  const bool no_cache = c->no_cache;
   std::vector<Box> boxes;
   std::vector<int> incr;
   for (int id : ids) {

@@ -50,31 +50,40 @@ __global__ void __launch_bounds__(kTileCells, 6) k_map(const __grid_constant__ M
     const BodyGeo& b = p.bodies[id];
     const int s = b.s;
     // (1) segment decisions: lane k < 4 evaluates segment k of this row
+    // (segments clamped to the grid; sd = 3: the segment straddles a periodic seam, so its
+    // cells transform their own centres)
     int sd = 0;
     float q0 = 0.f, q1 = 0.f, q2 = 0.f;
-    if (lane < kTileX / kSubX && row_ok) {
-      const double ps[3] = {tx * kTileX + lane * kSubX + 0.5 * kSubX, y + 0.5, zg + 0.5};
+    const int sx0 = tx * kTileX + lane * kSubX;
+    if (lane < kTileX / kSubX && row_ok && sx0 < G.nx) {
+      const int sx1 = min(sx0 + kSubX, G.nx);
+      const double ps[3] = {0.5 * (sx0 + sx1), y + 0.5, zg + 0.5};
+      const double half[3] = {0.5 * (sx1 - sx0), 0.5, 0.5};
       double qs[3];
-      sd = tile_decision<kSubReach, 16, 32>(b, ps, L, G.wall, qs);
+      sd = tile_decision<kSubReach, 16, 32>(b, ps, half, L, G.wall, qs);
+      if (p.stats) atomicAdd(p.stats + sd, 1ull);
+      if (sd == 2 && region_straddles(b, ps, half, L, G.wall, 0)) sd = 3;
       q0 = (float)qs[0];
       q1 = (float)qs[1];
       q2 = (float)qs[2];
-      if (p.stats) atomicAdd(p.stats + sd, 1ull);
     }
     const int seg = lane / kSubX;
     const int sdec = __shfl_sync(0xFFFFFFFFu, sd, seg);
     // (2) per-cell fp32 decision from the segment-centre transform
     int cd = sdec;
-    const unsigned need = __ballot_sync(0xFFFFFFFFu, sdec == 2);
+    const unsigned need = __ballot_sync(0xFFFFFFFFu, sdec >= 2);
     if (need) {
       const float qs0 = __shfl_sync(0xFFFFFFFFu, q0, seg);
       const float qs1 = __shfl_sync(0xFFFFFFFFu, q1, seg);
       const float qs2 = __shfl_sync(0xFFFFFFFFu, q2, seg);
       if (sdec == 2) {
-        const float off = (float)(lane % kSubX) + 0.5f - 0.5f * kSubX;
+        const int s0 = tx * kTileX + seg * kSubX;
+        const float off = (float)x + 0.5f - 0.5f * (float)(s0 + min(s0 + kSubX, G.nx));
         const float qc[3] = {qs0 + (float)b.Q[0] * off, qs1 + (float)b.Q[1] * off,
                              qs2 + (float)b.Q[2] * off};
         cd = cell_decision(b, qc);
+      } else if (sdec == 3) {
+        cd = act ? cell_decision_own(b, x, y, zg, L, G.wall) : 0;
       }
     }
     if (!act) cd = 0;

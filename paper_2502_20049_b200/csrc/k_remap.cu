@@ -33,6 +33,20 @@ __device__ __forceinline__ void tile_coords(int t, const Geom& G, int& tx, int& 
   tz = t / (G.gx * G.gy);
 }
 
+// the cells a tile really holds (a ragged last tile is clamped to the grid): centre, half extents
+__device__ __forceinline__ void region_of_tile(const Geom& G, int tx, int ty, int tz, double pc[3],
+                                               double half[3]) {
+  const int lo[3] = {tx * kTileX, ty * kTileY, tz * kTileZ};
+  const int hi[3] = {min(lo[0] + kTileX, G.nx), min(lo[1] + kTileY, G.ny),
+                     min(lo[2] + kTileZ, G.nzl)};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    pc[a] = 0.5 * (lo[a] + hi[a]);
+    half[a] = 0.5 * (hi[a] - lo[a]);
+  }
+  pc[2] += G.z0;
+}
+
 __device__ __forceinline__ void put_word(const RemapParams& r, int x, int y, int z, uint32_t w,
                                          int tile) {
 #if defined(PSM_BOUNDS_CHECK)
@@ -55,10 +69,10 @@ __global__ void k_remap_l0(const __grid_constant__ RemapParams r) {
   const Geom& G = r.g;
   const int tile = (tz * G.gy + ty) * G.gx + tx;
   const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
-  const double pt[3] = {tx * kTileX + 0.5 * kTileX, ty * kTileY + 0.5 * kTileY,
-                        G.z0 + tz * kTileZ + 0.5 * kTileZ};
+  double pt[3], half[3];
+  region_of_tile(G, tx, ty, tz, pt, half);
   double qt[3];
-  const int dec = tile_decision<kTileReach, 4, 8>(r.body, pt, L, G.wall, qt, r.margin);
+  const int dec = tile_decision<kTileReach, 4, 8>(r.body, pt, half, L, G.wall, qt, r.margin);
   if (dec == 0 && r.tile_flag[tile] == 0) return;  // far outside and already all zero
   r.tile_flag[tile] = 0;
   const int k = atomicAdd(r.counters + 0, 1);
@@ -81,23 +95,28 @@ __global__ void k_remap_l1(const __grid_constant__ RemapParams r) {
     const int y = ty * kTileY + row % kTileY, z = tz * kTileZ + row / kTileY;
     if (y >= G.ny || z >= G.nzl) continue;
     const int x0 = tx * kTileX + sx * kSubX;
-    const double ps[3] = {x0 + 0.5 * kSubX, y + 0.5, G.z0 + z + 0.5};
+    if (x0 >= G.nx) continue;
+    const int x1 = min(x0 + kSubX, G.nx);  // ragged last segment: clamped to the grid
+    const double ps[3] = {0.5 * (x0 + x1), y + 0.5, G.z0 + z + 0.5};
+    const double half[3] = {0.5 * (x1 - x0), 0.5, 0.5};
     double qs[3];
-    const int dec = tile_decision<kSubReach, 16, 32>(b, ps, L, G.wall, qs, r.margin);
+    const int dec = tile_decision<kSubReach, 16, 32>(b, ps, half, L, G.wall, qs, r.margin);
     if (dec == 2) {
+      // straddling segments (seam): every cell transforms its own centre in L2 (segq.w = 1)
+      const bool own = region_straddles(b, ps, half, L, G.wall, r.margin);
       const int k = atomicAdd(r.counters + 1, 1);
       if (k < r.seg_cap) {
         r.segs[k] = ((uint32_t)tile << 5) | (uint32_t)sg;
-        r.segq[k] = make_float4((float)qs[0], (float)qs[1], (float)qs[2], 0.f);
+        r.segq[k] = make_float4((float)qs[0], (float)qs[1], (float)qs[2], own ? 1.f : 0.f);
         continue;
       }
       // list full: finish the segment here (exact, serial; a cached band gets its cells)
-      for (int c = 0; c < kSubX; ++c) {
-        if (x0 + c >= G.nx) continue;
-        const float off = (float)c + 0.5f - 0.5f * kSubX;
+      for (int c = 0; c < x1 - x0; ++c) {
+        const float off = (float)(x0 + c) + 0.5f - (float)ps[0];
         const float qc[3] = {(float)qs[0] + (float)b.Q[0] * off, (float)qs[1] + (float)b.Q[1] * off,
                              (float)qs[2] + (float)b.Q[2] * off};
-        const int cd = cell_decision(b, qc, r.margin);
+        const int cd = own ? cell_decision_own(b, x0 + c, y, G.z0 + z, L, G.wall, r.margin)
+                           : cell_decision(b, qc, r.margin);
         if (cd == 2 && r.margin) {  // the cached band holds every cell of the box: no overflow
           const int k = atomicAdd(r.bandn, 1);
           r.band[k] = ((uint32_t)tile << 8) | (uint32_t)(row * kTileX + sx * kSubX + c);
@@ -135,10 +154,12 @@ __global__ void k_remap_l2(const __grid_constant__ RemapParams r) {
     const int x = tx * kTileX + sx * kSubX + c;
     if (x >= G.nx) continue;
     const float4 q = r.segq[si];
-    const float off = (float)c + 0.5f - 0.5f * kSubX;
+    const int x0 = tx * kTileX + sx * kSubX;
+    const float off = (float)x + 0.5f - 0.5f * (float)(x0 + min(x0 + kSubX, G.nx));
     const float qc[3] = {q.x + (float)b.Q[0] * off, q.y + (float)b.Q[1] * off,
                          q.z + (float)b.Q[2] * off};
-    const int cd = cell_decision(b, qc, r.margin);
+    const int cd = q.w != 0.f ? cell_decision_own(b, x, y, G.z0 + z, L, G.wall, r.margin)
+                              : cell_decision(b, qc, r.margin);
     if (cd == 2) {
       const int k = atomicAdd(r.bandn, 1);
       if (k < r.band_cap) {

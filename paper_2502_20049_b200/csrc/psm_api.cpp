@@ -121,6 +121,10 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   if (const char* e = std::getenv("PSM_AHEAD_BLOCKS")) c->ahead_blocks = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PSM_P2P_TIMEOUT_S"))
     c->p2p_timeout_ns = (unsigned long long)(std::max(1.0, std::atof(e)) * 1e9);
+  if (const char* e = std::getenv("PSM_BAND_CACHE")) c->no_cache = std::strcmp(e, "0") == 0;
+  c->force_general = std::getenv("PSM_REMAP_GENERAL") != nullptr;
+  if (const char* e = std::getenv("PSM_SEG_CAP")) c->seg_cap_env = std::max(1ll, std::atoll(e));
+  if (const char* e = std::getenv("PSM_BAND_CAP")) c->band_cap_env = std::max(1ll, std::atoll(e));
   if (const char* e = std::getenv("PSM_AHEAD_THREADS"))
     c->ahead_threads = std::min(1024, std::max(32, std::atoi(e)));
   Geom& g = c->geom;
@@ -151,6 +155,14 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
 
 psm_status psm_destroy(psm_ctx* c) {
   if (!c) return PSM_OK;
+  if (c->p2p && c->comm) {
+    // this rank's memory is mapped by its neighbours (fused halo): a collective barrier before
+    // it is freed, so no rank can still be storing into it (psm_destroy is collective)
+    int one = 1;
+    int* d = reinterpret_cast<int*>(c->flags + 3);
+    cudaMemcpyAsync(d, &one, sizeof(int), cudaMemcpyHostToDevice, c->st);
+    ncclAllReduce(d, d, 1, ncclInt32, ncclSum, c->comm, c->st);
+  }
   cudaStreamSynchronize(c->st);
   if (c->map_st) cudaStreamSynchronize(c->map_st);
   for (int id = 0; id <= kMaxBodies; ++id) {
@@ -450,6 +462,11 @@ psm_status psm_set_dynamics(psm_ctx* c, int32_t id, const psm_dynamics* d) {
       b.moving = false;
       for (int a = 0; a < 3; ++a)
         if (b.v[a] != 0.0 || b.w[a] != 0.0) b.moving = true;
+      // the spare word buffer (and its band) followed the dynamic pose; a body that comes to
+      // rest here is not remapped by psm_step, so map it now at the integrated pose
+      c->alt_valid = false;
+      c->ft_valid = false;
+      if (!b.moving) return remap(c, std::vector<int>{id}, c->step);
     }
     return PSM_OK;
   }
@@ -486,6 +503,10 @@ psm_status psm_set_dynamics(psm_ctx* c, int32_t id, const psm_dynamics* d) {
       if (!std::isfinite(d->added_inertia[3 * r + cc]) ||
           d->added_inertia[3 * r + cc] != d->added_inertia[3 * cc + r])
         FAIL(c, PSM_E_ARG, "added inertia must be symmetric and finite");
+  }
+  if (!b.dynamic) {
+    c->alt_valid = false;
+    c->ft_valid = false;
   }
   b.dynamic = true;
   b.moving = true;
@@ -742,6 +763,15 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
   if (record(c, 2, 1) != cudaSuccess) FAIL(c, PSM_E_CUDA, "event record failed");
   unsigned long long* herr =
       reinterpret_cast<unsigned long long*>(c->pinned + (kMaxBodies + 1) * kSlotVals);
+  if (c->p2p && c->epoch > 0) {
+    // fused halo: the neighbours' last collide stores into this rank's ghost planes; wait for
+    // their signal so that a readback / state write after this call sees (or overwrites) final
+    // values, and no peer store is still in flight when the call returns
+    CUDA_TRY(c, launch_p2p_wait(c->has_dn ? c->flags + 0 : nullptr,
+                                c->has_up ? c->flags + 1 : nullptr, c->epoch, c->flags + 2,
+                                c->p2p_timeout_ns, c->st));
+    c->launches += 1;
+  }
   CUDA_TRY(c, cudaMemcpyAsync(herr, c->err, 8, cudaMemcpyDeviceToHost, c->st));
   if (c->p2p) CUDA_TRY(c, cudaMemcpyAsync(herr + 1, c->flags + 2, 8, cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(c, cudaStreamSynchronize(c->st));

@@ -132,6 +132,11 @@ struct psm_ctx {
   uint32_t* r_band = nullptr;
   int* r_bandcnt = nullptr;
   int seg_cap = 0, band_cap = 0;
+  // remap switches read from the environment at psm_create (diagnostics / tests):
+  // PSM_BAND_CACHE=0, PSM_REMAP_GENERAL, PSM_SEG_CAP / PSM_BAND_CAP (cap the segment / band lists
+  // of the full pipeline so that the in-kernel overflow paths run)
+  bool no_cache = false, force_general = false;
+  int64_t seg_cap_env = 0, band_cap_env = 0;
   double* pinned = nullptr;  // host staging (ft + err)
   // test-only dense fields
   double *dbg_B = nullptr, *dbg_us = nullptr;

@@ -118,30 +118,44 @@ __device__ __forceinline__ int sample_inside(const BodyGeo& b, int x, int y, int
   return mesh_bit(b, q);
 }
 
-// Whole-tile decision (block-uniform): 0 = every sub-sample of the tile is outside, 1 = every
-// sub-sample is inside, 2 = decide per cell.  Every sub-sample lies within 16.16 cells of the
-// tile centre, i.e. within kTileReach - 1 bricks of the centre's brick.  qt = body-frame tile
-// centre (used as the base of the per-cell fp32 decisions).
+// Periodic seam guard.  A region (tile, segment or cell) is the box pc +- half (clamped to the
+// grid, so a ragged last tile is described by the cells it really holds).  On a periodic axis the
+// method maps each sample with its own minimum image (mi(p - t), A14), so a region whose
+// displacement range reaches the cut at +-L/2 holds samples of two different images and its
+// centre transform says nothing about them.  Such a region is never decided as a whole; with
+// margin = 1 (cached band) the range is widened by the one cell the body may still move.
+__device__ __forceinline__ bool region_straddles(const BodyGeo& b, const double pc[3],
+                                                 const double half[3], const double L[3],
+                                                 const int wall[3], int margin) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (wall[a]) continue;
+    const double d = min_image(pc[a] - b.t[a], L[a], true);
+    if (fabs(d) + half[a] + (double)margin >= 0.5 * L[a] - 1e-6) return true;
+  }
+  return false;
+}
+
+// Whole-region decision: 0 = every sub-sample of the region is outside, 1 = every sub-sample is
+// inside, 2 = decide per cell.  pt = centre of the region clamped to the grid, half = its half
+// extents; every sub-sample lies within REACH - 1 bricks of the centre's brick (REACH is sized
+// for the unclamped region, which contains the clamped one).  qt = body-frame region centre
+// (used as the base of the per-cell fp32 decisions).  Regions straddling a periodic seam are
+// always 2 (region_straddles).
 // margin = 1: valid for poses within one cell of this one (the brick reaches keep >= 1.84 cells
 // of slack for meshes; the sphere test widens by the margin).
 template <int REACH, int BIT_OUT, int BIT_IN>
 __device__ __forceinline__ int tile_decision(const BodyGeo& b, const double pt[3],
-                                             const double L[3], const int wall[3],
-                                             double qt[3], int margin = 0) {
+                                             const double half[3], const double L[3],
+                                             const int wall[3], double qt[3], int margin = 0) {
   constexpr int kTileReach = REACH;  // brick reach of the region's sub-samples + 1
   body_frame(b, pt, L, wall, qt);
+  if (region_straddles(b, pt, half, L, wall, margin)) return 2;
   if (b.kind != 1) {
     const double dist = sqrt(qt[0] * qt[0] + qt[1] * qt[1] + qt[2] * qt[2]);
     const double r = sqrt(b.r2);
     if (dist - (double)(kTileReach - 1 + margin) > r) return 0;
-    if (dist + (double)(kTileReach - 1 + margin) < r) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double d = min_image(pt[a] - b.t[a], L[a], !wall[a]);
-        if (!wall[a] && fabs(d) > 0.5 * L[a] - 2.0 * kTileReach) return 2;
-      }
-      return 1;
-    }
+    if (dist + (double)(kTileReach - 1 + margin) < r) return 1;
     return 2;
   }
   int bc[3];
@@ -157,15 +171,7 @@ __device__ __forceinline__ int tile_decision(const BodyGeo& b, const double pt[3
   const uint8_t m =
       __ldg(b.mask + ((long long)bc[2] * b.dims_b[1] + bc[1]) * b.dims_b[0] + bc[0]);
   if (m & BIT_OUT) return 0;
-  if (m & BIT_IN) {
-    // "full" must not straddle a periodic minimum-image cut
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double d = min_image(pt[a] - b.t[a], L[a], !wall[a]);
-      if (!wall[a] && fabs(d) > 0.5 * L[a] - 2.0 * kTileReach) return 2;
-    }
-    return 1;
-  }
+  if (m & BIT_IN) return 1;
   return 2;
 }
 
@@ -205,6 +211,20 @@ __device__ __forceinline__ int cell_decision(const BodyGeo& b, const float qc[3]
   if (m & (margin ? 128 : 2)) return 1;
   if (m & (margin ? 64 : 1)) return 0;
   return 2;
+}
+
+// Per-cell decision of a cell of a region that straddles a periodic seam: the cell's own centre
+// is transformed exactly (its own minimum image); a cell that itself straddles the cut is sampled.
+__device__ __forceinline__ int cell_decision_own(const BodyGeo& b, int x, int y, int zg,
+                                                 const double L[3], const int wall[3],
+                                                 int margin = 0) {
+  const double pc[3] = {x + 0.5, y + 0.5, zg + 0.5};
+  const double half[3] = {0.5, 0.5, 0.5};
+  if (region_straddles(b, pc, half, L, wall, margin)) return 2;
+  double q[3];
+  body_frame(b, pc, L, wall, q);
+  const float qc[3] = {(float)q[0], (float)q[1], (float)q[2]};
+  return cell_decision(b, qc, margin);
 }
 
 // Warp-centric remap of one 32x4x2 tile per block: each warp owns one 32-cell x-row and decides
