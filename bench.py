@@ -40,6 +40,12 @@ WORKLOADS = {
                 desc="c5 weak: D3Q19 PSM fp32, 512^3 per GPU, CROR-like counter-rotating rotor "
                      "pair per GPU (12+10 blades, ~1.1 M faces, s=1, remapped every step), SC1, "
                      "weighted B"),
+    # the same at the paper's precision (fp64): the default bench line
+    "c5w64": dict(nx=512, ny=512, nz=512, Q=19, prec="f64", tau=0.55, rotors=True, s=1,
+                  omega=0.05 / 220.0, pattern="two_array", sc=1, bmode=1,
+                  desc="c5 weak, fp64: D3Q19 PSM fp64 (the paper's precision), 512^3 per GPU, "
+                       "CROR-like counter-rotating rotor pair per GPU (12+10 blades, ~1.1 M "
+                       "faces, s=1, remapped every step), SC1, weighted B"),
     # c5w as an application run: inflow U = 0.05 at x = 0, pressure outflow at
     # x = nx-1 (reading A30), flow starting from rest
     "c5app": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.55, rotors=True, s=1,
@@ -172,16 +178,22 @@ def profiles_traffic(workload: str):
 
 
 # ------------------------------------------------------------------------ CPU oracle leg ---
-def oracle_sample(wl: dict, steps, budget_s: float, seed: int, warmup: int = 0):
+def oracle_sample(wl: dict, steps, budget_s: float, seed: int, warmup: int = 0,
+                  threads: int | None = None):
     """Time the CPU oracle (as it stands) on a bounded sub-box of the same workload: same
     stencil/tau/operator, bodies scaled with the box, moving, remapped every step.  `warmup`
     untimed steps first; steps=None sizes the timed steps to about `budget_s` seconds."""
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     # torchrun pins OMP_NUM_THREADS=1 per rank; the sample runs on rank 0 alone and may use the
     # whole host (set before the oracle library, and with it libgomp, is loaded)
-    os.environ["OMP_NUM_THREADS"] = str(cores)
+    if "oracle" not in sys.modules:
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
+    import ctypes
     import oracle
     import psm_inputs as pi
+    oracle.lib()
+    # the thread count of this sample (libgomp's runtime call; the oracle is unchanged)
+    ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(cores))
     # oracle throughput is ~0.6-1 MLUPS per core for D3Q19; size the box for the budget
     est = 0.6e6 * cores * (19.0 / wl["Q"])
     per_step = budget_s / max(1, steps or 10)
@@ -350,7 +362,12 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c5w", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c5w64", choices=sorted(WORKLOADS))
+    ap.add_argument("--extra", default=None,
+                    help="second workload measured in the same run and reported under its own "
+                         "key (default: c5w, the fp32 line, when --config is c5w64)")
+    ap.add_argument("--reps", type=int, default=5,
+                    help="timed repetitions of exactly K steps; value = their median")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--s", type=int, default=None, help="override the super-sampling exponent")
@@ -383,6 +400,126 @@ def main():
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy().tobytes())
 
+    extra = args.extra if args.extra is not None else ("c5w" if args.config == "c5w64" else "")
+    extra = "" if extra == "none" else extra
+    stream_gbs = stream_copy_gbs(torch) if rank == 0 else None
+    res = measure(psm, torch, dist, wl, args, rank, world, local, nccl_id, e2e=not args.no_e2e,
+                  config_name=args.config)
+    extra_res = None
+    if extra and extra != args.config:
+        nccl_id2 = None
+        if world > 1:
+            idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(psm.psm_nccl_get_unique_id()),
+                                           dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            nccl_id2 = bytes(idt.cpu().numpy().tobytes())
+        extra_res = measure(psm, torch, dist, dict(WORKLOADS[extra]), args, rank, world, local,
+                            nccl_id2, e2e=False, config_name=extra)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(wl, None, 12.0, 7)
+        cpu.pop("ms_per_step", None)
+        one = oracle_sample(wl, None, 8.0, 7, threads=1)
+        cpu["single_thread"] = {"value": one["value"], "unit": UNIT, "cores": 1,
+                                "sample": one["sample"]}
+        cpu["cpu_model"] = cpu_model()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": res["mlups"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong" if wl.get("strong") else "weak",
+            "vs_baseline": None, "dtype": wl["prec"], "data": "synthetic",
+            "config": res["config"],
+            "mlups_per_gpu": res["mlups"] / world,
+            "reps": res["reps"],
+            "roofline_frac_step": res["step_frac"],
+            "roofline": roofline_block(res, stream_gbs),
+            "phases_ms": res["phases_ms"],
+            "gpu_launches": res["launches"],
+            "clocks": res["clocks"],
+            "e2e": res["e2e"],
+            "cpu_baseline": cpu,
+        }
+        if extra_res is not None:
+            line[extra_res["prec"] if extra_res["prec"] != wl["prec"] else extra] = {
+                "config": extra, "workload": extra_res["config"]["workload"],
+                "value": extra_res["mlups"], "unit": UNIT, "ms_per_step": extra_res["ms_per_step"],
+                "reps": extra_res["reps"], "roofline_frac_step": extra_res["step_frac"],
+                "roofline": roofline_block(extra_res, stream_gbs),
+                "phases_ms": extra_res["phases_ms"], "gpu_launches": extra_res["launches"],
+                "clocks": extra_res["clocks"]}
+        emit(line)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+NOMINAL_GBS = 8000.0  # B200 HBM3e nominal (north_star "~8 TB/s")
+
+
+def roofline_block(res, stream_gbs):
+    peak, peak_src = load_peak()
+    a = res["achieved"]
+    out = {"bound": "hbm", "kernel": "k_collide (fused PSM stream-collide)",
+           "achieved": a, "peak": peak, "unit": "GB/s", "frac": (a / peak) if a else None,
+           "traffic": profiles_traffic(res["name"]), "bytes_per_update": res["bpu"],
+           "peak_source": peak_src, "avg_launch_ms": res["avg_launch_ms"],
+           "launches_timed": res["launches_timed"],
+           # the same achieved bandwidth against the other two denominators SURVEY §8(d) names
+           "peaks": {"measured_json": peak, "stream_copy_same_run": stream_gbs,
+                     "nominal": NOMINAL_GBS},
+           "frac_vs_stream_copy_same_run": (a / stream_gbs) if (a and stream_gbs) else None,
+           "frac_vs_nominal": (a / NOMINAL_GBS) if a else None,
+           "step_frac_vs": {"measured_json": res["step_gbs"] / peak,
+                            "stream_copy_same_run": (res["step_gbs"] / stream_gbs)
+                            if stream_gbs else None,
+                            "nominal": res["step_gbs"] / NOMINAL_GBS}}
+    return out
+
+
+def stream_copy_gbs(torch, nbytes=4 << 30, reps=10):
+    """Same-run STREAM-copy bandwidth (the paper's roofline practice): a
+    device-to-device copy of a 4 GiB buffer, read + write bytes over the best of `reps` launches
+    timed with CUDA events on the current stream."""
+    a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    b = torch.empty_like(a)
+    a.fill_(1)
+    best = None
+    for _ in range(reps + 2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        e1.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * nbytes / (best / 1e3) / 1e9
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def measure(psm, torch, dist, wl, args, rank, world, local, nccl_id, e2e=True, config_name=""):
+    """Build the workload, warm up, time `args.reps` repetitions of exactly `args.steps` steps
+    (each bracketed by barrier + synchronize, device time on the library's stream, max over
+    ranks) and, optionally, the end-to-end loop through the public API."""
+    import math
+    import psm_inputs as pi
     sim, body_poses, nbodies, S = build_workload(psm, wl, rank, world, nccl_id)
     nx, ny = wl["nx"], wl["ny"]
     nzg = wl["nz"] if wl.get("strong") else wl["nz"] * world
@@ -394,36 +531,38 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up
     sim.step(max(3, args.warmup))
     barrier()
     l0 = sim.launches
     sim.profile(True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
     with ClockSampler(local) as clk:
-        barrier()
-        e0.record(stream)
-        sim.step(args.steps)
-        e1.record(stream)
-        barrier()
-    ms = e0.elapsed_time(e1)
+        for _ in range(max(1, args.reps)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            e0.record(stream)
+            sim.step(args.steps)
+            e1.record(stream)
+            barrier()
+            ms = e0.elapsed_time(e1)
+            if dist is not None:
+                t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            times.append(ms)
     sim.profile(False)
     prof = sim.profile_read()
-    launches = sim.launches - l0
-    ms_max = ms
-    if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+    reps = max(1, args.reps)
+    launches = (sim.launches - l0) // reps
+    ms_med = float(np.median(times))
     cells_local = nx * ny * nzl
     cells_total = nx * ny * nzg
-    mlups = cells_total * args.steps / (ms_max / 1e3) / 1e6
-    peak, peak_src = load_peak()
+    mlups = cells_total * args.steps / (ms_med / 1e3) / 1e6
     bpu = bytes_per_update(wl["Q"], S)
     coll_ms, coll_n = prof["collide"]
     avg = coll_ms / max(1, coll_n)
     achieved = bpu * cells_local / (avg / 1e3) / 1e9 if coll_n else None
-    step_gbs = bpu * cells_local * args.steps / (ms / 1e3) / 1e9
+    step_gbs = bpu * cells_local * args.steps / (ms_med / 1e3) / 1e9
 
     # end-to-end through the public API with host buffers (the coupled-simulation loop a user
     # runs): every step the host computes each body's pose in closed form and hands it to
@@ -431,9 +570,8 @@ def main():
     # body's force/torque back (D2H, 96 B per body + the 8 B error word).  The one-off field
     # upload (psm_init_equilibrium from pinned host rho/u) and readback (psm_read_velocity) are
     # timed separately and reported as setup_ms / readback_ms.
-    e2e = None
-    if not args.no_e2e:
-        import math
+    e2e_line = None
+    if e2e:
         shape = (nzl, ny, nx)
         rho_h = torch.ones(shape, dtype=torch.float64).pin_memory().numpy()
         u_h = torch.zeros((3,) + shape, dtype=torch.float64).pin_memory().numpy()
@@ -466,53 +604,36 @@ def main():
             t = torch.tensor([dt], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        e2e = {"value": cells_total * args.steps / dt / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": 144 * nbodies, "d2h_bytes_per_step": 96 * nbodies + 8,
-               "ms_per_step": dt / args.steps * 1e3,
-               "setup_ms": (t_b - t_a) * 1e3, "setup_h2d_bytes": int(rho_h.nbytes + u_h.nbytes),
-               "readback_ms": (t_d - t_c) * 1e3,
-               "readback_d2h_bytes": int(rho_o.nbytes + u_o.nbytes),
-               "what": "K x [host closed-form pose -> psm_set_body (each body), psm_step(1), "
-                       "psm_force_torque (each body)], wall clock, max over ranks"}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_sample(wl, None, 12.0, 7)
-        cpu.pop("ms_per_step", None)
-
+        e2e_line = {"value": cells_total * args.steps / dt / 1e6, "unit": UNIT,
+                    "h2d_bytes_per_step": 144 * nbodies, "d2h_bytes_per_step": 96 * nbodies + 8,
+                    "ms_per_step": dt / args.steps * 1e3,
+                    "setup_ms": (t_b - t_a) * 1e3,
+                    "setup_h2d_bytes": int(rho_h.nbytes + u_h.nbytes),
+                    "readback_ms": (t_d - t_c) * 1e3,
+                    "readback_d2h_bytes": int(rho_o.nbytes + u_o.nbytes),
+                    "what": "K x [host closed-form pose -> psm_set_body (each body), "
+                            "psm_step(1), psm_force_torque (each body)], wall clock, max over "
+                            "ranks"}
     halo_cfg = {}
     if world > 1:
         hm = psm.psm_halo_mode(sim.ctx)
         halo_cfg = {"parallelism": f"z-slab x{world} + " + (
             "fused halo (k_collide stores into the neighbours' ghost planes over NVLink)"
             if hm == 2 else "NCCL send/recv halo")}
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": mlups, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong" if wl.get("strong") else "weak",
-            "vs_baseline": None, "dtype": wl["prec"], "data": "synthetic",
-            "config": dict(workload_config(wl, world), **halo_cfg),
-            "mlups_per_gpu": mlups / world,
-            "roofline_frac_step": step_gbs / peak,
-            "roofline": {"bound": "hbm", "kernel": "k_collide (fused PSM stream-collide)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None,
-                         "traffic": profiles_traffic(args.config),
-                         "bytes_per_update": bpu, "peak_source": peak_src,
-                         "avg_launch_ms": avg, "launches_timed": coll_n},
-            "phases_ms": {k: v[0] / max(1, args.steps) for k, v in prof.items()},
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-        }
-        emit(line)
     if dist is not None:
         dist.barrier()
-        sim.close()
-        dist.destroy_process_group()
-    return 0
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
+    return {"name": config_name, "prec": wl["prec"], "mlups": mlups,
+            "ms_per_step": ms_med / args.steps,
+            "reps": {"n": len(times), "ms_per_step": [t / args.steps for t in times],
+                     "value_is": "median"},
+            "step_frac": step_gbs / load_peak()[0], "step_gbs": step_gbs,
+            "achieved": achieved, "bpu": bpu, "avg_launch_ms": avg, "launches_timed": coll_n,
+            "phases_ms": {k: v[0] / (max(1, args.steps) * reps) for k, v in prof.items()},
+            "launches": launches, "clocks": clk.summary(), "e2e": e2e_line,
+            "config": dict(workload_config(wl, world), **halo_cfg)}
 
 
 if __name__ == "__main__":

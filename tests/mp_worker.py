@@ -80,6 +80,39 @@ def main():
             failures.append(f"fractions {bc} Q{Q} {prec}")
         dsim.close()
         ref.close()
+    # body-free (no F/T allreduce syncs the ranks): a readback straight after psm_step and a
+    # state write followed by a step must see the neighbours' final peer stores (fused halo)
+    for prec in ("f64", "f32"):
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(psm.psm_nccl_get_unique_id()),
+                                       dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.cpu().numpy().tobytes())
+        nx, ny, nz = 40, 36, 16 * world + 6
+        kw = dict(Q=19, tau=0.7, bc=(0, 0, 0), prec=prec)
+        dsim = psm.Simulation(nx, ny, nz, rank=rank, world=world, nccl_id=nid, **kw)
+        ref = psm.Simulation(nx, ny, nz, **kw)
+        z0, nzl = dsim.z0, dsim.nzl
+        rho, u = pi.perturbed_flow((nz, ny, nx), 7, u0=(0.02, 0.01, 0.03))
+        ref.init_equilibrium(rho, u)
+        dsim.init_equilibrium(np.ascontiguousarray(rho[z0:z0 + nzl]),
+                              np.ascontiguousarray(u[:, z0:z0 + nzl]))
+        for n in (1, 3, 2):
+            ref.step(n)
+            dsim.step(n)
+            if not np.array_equal(ref.pdfs()[:, z0:z0 + nzl], dsim.pdfs()):
+                failures.append(f"body-free read after step {prec} n={n}")
+        f = ref.pdfs()
+        f = f * (1.0 + 0.001 * pi.uniform_pm1(8, f.size).reshape(f.shape))
+        ref.write_pdfs(f)
+        dsim.write_pdfs(np.ascontiguousarray(f[:, z0:z0 + nzl]))
+        ref.step(3)
+        dsim.step(3)
+        if not np.array_equal(ref.pdfs()[:, z0:z0 + nzl], dsim.pdfs()):
+            failures.append(f"body-free write then step {prec}")
+        dsim.close()
+        ref.close()
     ok = torch.tensor([0 if failures else 1], device="cuda")
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     for f in failures:

@@ -68,3 +68,49 @@ def test_c5w_full_size_sampled_cells_and_invariants():
     for b in (1, 2):
         F, T, aF, aT = sim.force_torque(b)
         assert aF.max() > 0
+
+
+def test_c5w_shaped_256_rotor_pair_full_parity():
+    """The measured configuration's hard paths at a size the oracle can follow: c5w scaled to
+    256^3 (D3Q19 fp32, SRT + SC1, weighted B, tau = 0.55, two-array, rest start), the
+    counter-rotating rotor pair of the c5 recipe at half size (12 + 10 blades, tips 100 / 90,
+    ~57 k faces together, s = 1), advanced by the library itself in ONE psm_step(20) call
+    (closed-form poses, remap-ahead pipeline, cached narrow band) against the oracle fed
+    oracle.pose_advance poses: counts bit-exact after the run, fp32 PDFs within 2e-5 of the
+    fp64 oracle on every cell (PSM cells included), F/T of the last step within fp32 bounds."""
+    import paper_2502_20049_b200 as psm
+    n, steps, tau, om = 256, 20, 0.55, 0.05 / 110.0
+    rot = [(pi.propeller_mesh(n_blades=12, scale=100 / 110, n_st=40, n_pts=32, hub_seg=64),
+            (100.0, 128.0, 128.0), (om, 0.0, 0.0)),
+           (pi.propeller_mesh(n_blades=10, scale=90 / 110, n_st=40, n_pts=32, hub_seg=64),
+            (165.0, 128.0, 128.0), (-om, 0.0, 0.0))]
+    g = psm.Simulation(n, n, n, Q=19, tau=tau, prec="f32", sc=1, bmode=1)
+    o = oracle.Oracle(n, n, n, 19, tau, (0, 0, 0), 1, 1)
+    g.init_equilibrium(None, None)
+    o.init_equilibrium(None, None)
+    for b, ((v, t), pos, w) in enumerate(rot):
+        g.set_mesh(b + 1, v, t, 1, np.eye(3), pos, (0, 0, 0), w)
+        o.set_mesh(b + 1, v, t, 1)
+    for k in range(steps):
+        for b, (_, pos, w) in enumerate(rot):
+            Qk, tk = oracle.pose_advance(np.eye(3), pos, (0, 0, 0), w, k, [n] * 3, [1] * 3)
+            o.set_pose(b + 1, Qk, tk, (0, 0, 0), w)
+        o.map()
+        o.step(1)
+    g.step(steps)
+    _, ido, co, _ = o.fractions()
+    _, idg, cg = g.fractions()
+    assert np.array_equal(co, cg) and np.array_equal(ido, idg)
+    fo = o.pdfs()
+    fg = g.pdfs()
+    d = np.abs(fo - fg).max(axis=0)
+    psm_cells = co > 0
+    assert psm_cells.sum() > 10000
+    assert d[psm_cells].max() <= 2e-5, d[psm_cells].max()
+    assert d.max() <= 2e-5, d.max()
+    for b in (1, 2):
+        Fg, Tg, _, _ = g.force_torque(b)
+        Fo, To, aF, aT = o.force_torque(b)
+        assert np.all(np.abs(Fg - Fo) <= 1e-4 * aF + 1e-12), (b, Fg, Fo, aF)
+        assert np.all(np.abs(Tg - To) <= 1e-4 * aT + 1e-12), (b, Tg, To, aT)
+    g.close()

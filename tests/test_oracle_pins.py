@@ -372,3 +372,112 @@ def test_cumulant_forcing_momentum_and_poiseuille():
     yc = np.arange(H) + 0.5
     ref = gx * yc * (H - yc) / (2 * (tau - 0.5) / 3)
     assert np.max(np.abs(ux - ref)) / ref.max() < 0.02
+
+
+def _set_partitions(items):
+    """All set partitions of a list (Bell(6) = 203 for a sixth-order multi-index)."""
+    if not items:
+        yield []
+        return
+    first, rest = items[0], items[1:]
+    for p in _set_partitions(rest):
+        for i in range(len(p)):
+            yield p[:i] + [[first] + p[i]] + p[i + 1:]
+        yield [[first]] + p
+
+
+def _cumulant(f, c, abc):
+    """Joint cumulant of the velocity distribution f / rho for the multi-index (a, b, c), from
+    its raw moments by the textbook set-partition formula
+    kappa(X_1..X_n) = sum_pi (|pi| - 1)! (-1)^(|pi|-1) prod_B E[prod_{i in B} X_i] — no central
+    moments, no Wick products, nothing shared with the oracle's transform."""
+    rho = f.sum()
+    vs = [0] * abc[0] + [1] * abc[1] + [2] * abc[2]
+
+    def mom(block):
+        pr = np.ones(len(f))
+        for i in block:
+            pr = pr * c[:, vs[i]]
+        return float((f * pr).sum() / rho)
+
+    tot = 0.0
+    for p in _set_partitions(list(range(len(vs)))):
+        k = len(p)
+        tot += (-1) ** (k - 1) * math.factorial(k - 1) * np.prod([mom(B) for B in p])
+    return tot
+
+
+@pytest.mark.parametrize("tau", [0.6, 0.8, 1.7])
+def test_cumulant_relaxes_each_cumulant_as_a29_states(tau):
+    """Reading A29 pinned cumulant by cumulant on a strongly sheared,
+    anisotropic, moving random f: after the collision every cumulant of order >= 3 of f/rho
+    vanishes; the off-diagonal second cumulants and the two deviatoric differences are
+    multiplied by 1 - 1/tau; the trace is its equilibrium 3 c_s^2 = 1; rho and j are kept.
+    The cumulants come from raw moments by the set-partition formula (numpy, independent of the
+    oracle's central-moment/Wick arithmetic), so a wrong coefficient in any Wick product
+    (e.g. kappa_xxyy = rho (C_xx C_yy + 2 C_xy^2)) leaves a nonzero post-collision cumulant."""
+    Q = 27
+    c, w, _ = oracle.stencil(Q)
+    cf = c.astype(float)
+    u = np.array([0.05, -0.03, 0.02])
+    cu = cf @ u
+    f = w * (1 + 3 * cu + 4.5 * cu ** 2 - 1.5 * (u @ u))
+    f += w * 9 * (0.03 * cf[:, 0] * cf[:, 1] + 0.02 * cf[:, 1] * cf[:, 2] +
+                  0.015 * cf[:, 0] * cf[:, 2])
+    f += w * 0.06 * (cf[:, 0] ** 2 - cf[:, 1] ** 2)
+    f *= 1 + 0.1 * pi.uniform_pm1(5, Q)
+    assert f.min() > 0
+    out, _, err = oracle.collide_cell_cum(Q, f, tau, 1, 0.0, [0, 0, 0])
+    assert err == 0
+    idx = [(a, b, k) for a in range(3) for b in range(3) for k in range(3) if a + b + k > 0]
+    pre = {m: _cumulant(f, cf, m) for m in idx}
+    post = {m: _cumulant(out, cf, m) for m in idx}
+    r = 1.0 - 1.0 / tau
+    assert max(abs(pre[m]) for m in idx if sum(m) >= 3) > 1e-3  # far from equilibrium
+    for m in idx:
+        if sum(m) >= 3:
+            assert abs(post[m]) < 1e-15, (m, pre[m], post[m])
+    for m in [(1, 0, 0), (0, 1, 0), (0, 0, 1)]:
+        assert abs(post[m] - pre[m]) < 1e-16, m
+    for m in [(1, 1, 0), (1, 0, 1), (0, 1, 1)]:
+        assert abs(post[m] - r * pre[m]) < 1e-15, (m, pre[m], post[m])
+    assert abs(post[(1, 1, 0)]) > 1e-3 or tau == 1.0  # the sheared state survives the collision
+    for a, b in [((2, 0, 0), (0, 2, 0)), ((2, 0, 0), (0, 0, 2))]:
+        assert abs((post[a] - post[b]) - r * (pre[a] - pre[b])) < 1e-15
+    assert abs(post[(2, 0, 0)] + post[(0, 2, 0)] + post[(0, 0, 2)] - 1.0) < 1e-15
+    assert abs(out.sum() - f.sum()) < 1e-15
+
+
+def test_integrator_world_inertia_is_q_i_qt():
+    """Two-way coupling integrator (reading A28) with an anisotropic,
+    non-diagonal body-frame inertia and a rotated initial pose: a body at rest in fluid at rest
+    feels no fluid force (rest state invariant, P5), so one step gives exactly
+    dv = F_e / m, t1 = t0 + dv (semi-implicit), dw = (Q0 I Q0^T)^-1 T_e (numpy.linalg.solve, not
+    the oracle's adjugate) and Q1 = exp([dw]x) Q0 (scipy rotation vector, not Rodrigues as
+    coded).  Q0^T I Q0 (the other convention) differs by ~2x here."""
+    from scipy.spatial.transform import Rotation
+    n = 12
+    o = oracle.Oracle(n, n, n, 19, 0.8, (0, 0, 0), 1, 1)
+    o.init_equilibrium(None, None)
+    o.set_sphere(1, 3.0, 1)
+    Q0 = pi.rotation_about([1, 2, 3], 0.8)
+    t0 = np.array([6.2, 5.9, 6.4])
+    o.set_pose(1, Q0, t0, (0, 0, 0), (0, 0, 0))
+    inertia = np.array([[300.0, 20.0, -15.0], [20.0, 450.0, 35.0], [-15.0, 35.0, 700.0]])
+    Fe = np.array([1e-3, -2e-3, 5e-4])
+    Te = np.array([2e-3, -1e-3, 3e-3])
+    m = 500.0
+    o.set_dynamics(1, m, inertia, Fe, Te)
+    o.map()
+    o.step(1)
+    F, T, _, _ = o.force_torque(1)
+    assert np.all(F == 0) and np.all(T == 0)
+    o.integrate()
+    Q, t, v, w = o.body_state(1)
+    w_ref = np.linalg.solve(Q0 @ inertia @ Q0.T, Te)
+    assert np.allclose(w, w_ref, rtol=1e-13, atol=0)
+    assert not np.allclose(w, np.linalg.solve(Q0.T @ inertia @ Q0, Te), rtol=0.1, atol=0)
+    assert np.allclose(v, Fe / m, rtol=1e-15, atol=0)
+    assert np.allclose(t, t0 + Fe / m, rtol=0, atol=1e-15)
+    Q_ref = Rotation.from_rotvec(w_ref).as_matrix() @ Q0
+    assert np.abs(Q - Q_ref).max() < 1e-14
