@@ -63,8 +63,9 @@ typedef enum { PSM_SPHERE = 0, PSM_MESH = 1 } psm_shape_kind;
 /* Fluid collision operator: SRT (Eq.(2)), TRT (two relaxation times, one of the
  * operators the paper lists; symmetric rate 1/tau, antisymmetric 1/tau_- with
  * tau_- = 1/2 + Lambda/(tau - 1/2)), or the cumulant operator of the paper's performance runs
- * (D3Q27 only; shear rate 1/tau, bulk and higher-order rates 1; a body force flips
- * the first-order central moments about the force-shifted velocity, reading A31). */
+ * (D3Q27, reading A29, or D3Q19 — the paper's performance stencil — on the 19
+ * moments that stencil carries, reading A32; shear rate 1/tau, bulk and higher-order rates 1; a
+ * body force flips the first-order central moments about the force-shifted velocity, A31). */
 typedef enum { PSM_SRT = 0, PSM_TRT = 1, PSM_CUMULANT = 2 } psm_collision;
 
 typedef struct {

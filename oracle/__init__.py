@@ -139,8 +139,8 @@ def collide_cell_trt(Q, f, tau, magic, sc, B, us, g=(0.0, 0.0, 0.0)):
 
 
 def collide_cell_cum(Q, f, tau, sc, B, us, g=(0.0, 0.0, 0.0)):
-    """One-cell Eq.(4) collision with the cumulant fluid operator (D3Q27),
-    optional body force g (reading A31)."""
+    """One-cell Eq.(4) collision with the cumulant fluid operator (D3Q27 reading A29, D3Q19
+    reading A32), optional body force g (reading A31)."""
     f = _f64(f)
     us = _f64(us)
     g = _f64(g)

@@ -197,7 +197,8 @@ static int collide_cell_impl(int Q, const double* f, double tau, int sc, double 
   const int forced = (g[0] != 0.0 || g[1] != 0.0 || g[2] != 0.0);
   if (coll == 2) {
     /* Cumulant collision (the operator of the paper's performance runs),
-     * D3Q27, with every relaxation rate of order >= 3 equal to 1 (those cumulants are set to their
+     * D3Q27 (reading A29), or D3Q19 — the paper's performance stencil, PAPER.md:494 — on the 19
+     * moments it carries (reading A32), with every relaxation rate of order >= 3 equal to 1 (those cumulants are set to their
      * equilibrium 0), the bulk rate 1 and the shear rate 1/tau.  Plain form: second central
      * moments by brute force; normalised cumulants C = kappa/rho relaxed; post-collision central
      * moments of a distribution whose cumulants of order >= 3 vanish (Wick products of the C's);
@@ -245,34 +246,40 @@ static int collide_cell_impl(int Q, const double* f, double tau, int sc, double 
     ks[1][0][0] = 0.5 * g[0];
     ks[0][1][0] = 0.5 * g[1];
     ks[0][0][1] = 0.5 * g[2];
-    /* solve sum_i (c_ix - ux)^a (c_iy - uy)^b (c_iz - uz)^c fc_i = ks[a][b][c] */
+    /* solve sum_i (c_ix - ux)^a (c_iy - uy)^b (c_iz - uz)^c fc_i = ks[a][b][c] over the
+     * moments the velocity set carries: D3Q27 all 27 orders a, b, c <= 2; D3Q19 (reading A32)
+     * the 19 with at least one zero order (it has no (+-1,+-1,+-1) velocities, so xyz, x^2yz,
+     * ... are not independent moments of it) */
     double M[27][28];
+    int nr = 0;
     for (int r = 0; r < 27; ++r) {
       int a = r % 3, b = (r / 3) % 3, cc = r / 9;
-      for (int i = 0; i < 27; ++i) {
+      if (Q == 19 && a > 0 && b > 0 && cc > 0) continue;
+      for (int i = 0; i < Q; ++i) {
         int c[3];
         stencil_c(Q, i, c);
-        M[r][i] = pow(c[0] - u[0], a) * pow(c[1] - u[1], b) * pow(c[2] - u[2], cc);
+        M[nr][i] = pow(c[0] - u[0], a) * pow(c[1] - u[1], b) * pow(c[2] - u[2], cc);
       }
-      M[r][27] = ks[a][b][cc];
+      M[nr][Q] = ks[a][b][cc];
+      ++nr;
     }
-    for (int col = 0; col < 27; ++col) { /* Gaussian elimination, partial pivoting */
+    for (int col = 0; col < Q; ++col) { /* Gaussian elimination, partial pivoting */
       int piv = col;
-      for (int r = col + 1; r < 27; ++r)
+      for (int r = col + 1; r < Q; ++r)
         if (fabs(M[r][col]) > fabs(M[piv][col])) piv = r;
       if (piv != col)
-        for (int k = 0; k < 28; ++k) {
+        for (int k = 0; k <= Q; ++k) {
           double t = M[col][k];
           M[col][k] = M[piv][k];
           M[piv][k] = t;
         }
-      for (int r = 0; r < 27; ++r) {
+      for (int r = 0; r < Q; ++r) {
         if (r == col) continue;
         double fac = M[r][col] / M[col][col];
-        for (int k = col; k < 28; ++k) M[r][k] -= fac * M[col][k];
+        for (int k = col; k <= Q; ++k) M[r][k] -= fac * M[col][k];
       }
     }
-    for (int i = 0; i < 27; ++i) omF[i] = M[i][27] / M[i][i] - f[i];
+    for (int i = 0; i < Q; ++i) omF[i] = M[i][Q] / M[i][i] - f[i];
   } else if (coll == 0) {
     /* Eq.(2): Omega^F_i = -(1/tau)(f_i - f_i^eq) */
     for (int i = 0; i < Q; ++i) {

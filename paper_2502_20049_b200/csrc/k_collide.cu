@@ -339,6 +339,102 @@ __device__ __forceinline__ void cumulant_update(T (&f)[27], T rho, T jx, T jy, T
     }
 }
 
+// D3Q19 cumulant (reading A32; D3Q19 is the stencil of the paper's performance runs,
+// PAPER.md:494): the 19 moments x^a y^b z^c (a, b, c <= 2, at least one order zero) that the
+// D3Q19 velocity set carries.  Second cumulants as in the D3Q27 operator; the six third-order and
+// three fourth-order cumulants of the set are set to 0, so the post-collision central moments
+// are k_xxy = 0, k_xxyy = rho (C_xx C_yy + 2 C_xy^2).  Post-collision raw moments by the binomial
+// shift about u (third central moments zero, first central moments +g/2 with a force, A31), then
+// the populations by the closed-form inverse of the D3Q19 raw-moment map: an edge population of
+// the (a, b) plane is (M_aabb + s_b M_aab + s_a M_abb + s_a s_b M_ab)/4, a face population
+// ((M_aa - M_aabb - M_aacc) +- (M_a - M_abb - M_acc))/2, the rest population
+// rho - sum M_aa + sum M_aabb.
+template <typename T>
+__device__ __forceinline__ void plane_raw(T u, T v, T ku, T kv, T kuv, T kuuvv, T hu, T hv, T rho,
+                                          T& Muv, T& Muuv, T& Muvv, T& Muuvv) {
+  const T uu = u * u, vv = v * v, uv = u * v;
+  Muv = kuv + u * hv + v * hu + rho * uv;
+  Muuv = v * ku + T(2) * u * kuv + T(2) * uv * hu + uu * hv + rho * uu * v;
+  Muvv = u * kv + T(2) * v * kuv + T(2) * uv * hv + vv * hu + rho * u * vv;
+  Muuvv = kuuvv + vv * ku + T(4) * uv * kuv + uu * kv + T(2) * u * vv * hu + T(2) * uu * v * hv +
+          rho * uu * vv;
+}
+
+template <typename T, bool FORCE = false>
+__device__ __forceinline__ void cumulant_update(T (&f)[19], T rho, T jx, T jy, T jz, T ux, T uy,
+                                                T uz, T om, const T (&g)[3]) {
+  T mxx = T(0), myy = T(0), mzz = T(0), mxy = T(0), mxz = T(0), myz = T(0);
+#pragma unroll
+  for (int q = 0; q < 19; ++q) {
+    const int cx = stc_x(q), cy = stc_y(q), cz = stc_z(q);
+    if (cx) mxx += f[q];
+    if (cy) myy += f[q];
+    if (cz) mzz += f[q];
+    if (cx * cy > 0) mxy += f[q]; else if (cx * cy < 0) mxy -= f[q];
+    if (cx * cz > 0) mxz += f[q]; else if (cx * cz < 0) mxz -= f[q];
+    if (cy * cz > 0) myz += f[q]; else if (cy * cz < 0) myz -= f[q];
+  }
+  const T ir = T(1) / rho;
+  T Cxx0, Cyy0, Czz0, Kxy, Kxz, Kyz, hx = T(0), hy = T(0), hz = T(0);
+  if constexpr (FORCE) {
+    hx = T(0.5) * g[0];
+    hy = T(0.5) * g[1];
+    hz = T(0.5) * g[2];
+    Cxx0 = (mxx - ux * (jx - hx)) * ir;
+    Cyy0 = (myy - uy * (jy - hy)) * ir;
+    Czz0 = (mzz - uz * (jz - hz)) * ir;
+    Kxy = mxy - ux * jy + uy * hx;
+    Kxz = mxz - ux * jz + uz * hx;
+    Kyz = myz - uy * jz + uz * hy;
+  } else {
+    Cxx0 = (mxx - ux * jx) * ir;
+    Cyy0 = (myy - uy * jy) * ir;
+    Czz0 = (mzz - uz * jz) * ir;
+    Kxy = mxy - ux * jy;
+    Kxz = mxz - ux * jz;
+    Kyz = myz - uy * jz;
+  }
+  const T w1 = T(1) - om;
+  const T D1 = w1 * (Cxx0 - Cyy0), D2 = w1 * (Cxx0 - Czz0);
+  const T Cxy = w1 * Kxy * ir, Cxz = w1 * Kxz * ir, Cyz = w1 * Kyz * ir;
+  const T Cxx = (T(1) + D1 + D2) * T(1.0 / 3.0), Cyy = (T(1) - T(2) * D1 + D2) * T(1.0 / 3.0),
+          Czz = (T(1) + D1 - T(2) * D2) * T(1.0 / 3.0);
+  const T kxx = rho * Cxx, kyy = rho * Cyy, kzz = rho * Czz;
+  const T kxy = rho * Cxy, kxz = rho * Cxz, kyz = rho * Cyz;
+  const T kxxyy = rho * (Cxx * Cyy + T(2) * Cxy * Cxy);
+  const T kxxzz = rho * (Cxx * Czz + T(2) * Cxz * Cxz);
+  const T kyyzz = rho * (Cyy * Czz + T(2) * Cyz * Cyz);
+  // post-collision raw moments
+  const T Mx = rho * ux + hx, My = rho * uy + hy, Mz = rho * uz + hz;
+  const T Mxx = kxx + T(2) * ux * hx + rho * ux * ux;
+  const T Myy = kyy + T(2) * uy * hy + rho * uy * uy;
+  const T Mzz = kzz + T(2) * uz * hz + rho * uz * uz;
+  T Mxy, Mxxy, Mxyy, Mxxyy, Mxz, Mxxz, Mxzz, Mxxzz, Myz, Myyz, Myzz, Myyzz;
+  plane_raw(ux, uy, kxx, kyy, kxy, kxxyy, hx, hy, rho, Mxy, Mxxy, Mxyy, Mxxyy);
+  plane_raw(ux, uz, kxx, kzz, kxz, kxxzz, hx, hz, rho, Mxz, Mxxz, Mxzz, Mxxzz);
+  plane_raw(uy, uz, kyy, kzz, kyz, kyyzz, hy, hz, rho, Myz, Myyz, Myzz, Myyzz);
+  const T q4 = T(0.25);
+#pragma unroll
+  for (int sa = -1; sa <= 1; sa += 2)
+#pragma unroll
+    for (int sb = -1; sb <= 1; sb += 2) {
+      const T A = T(sa), Bs = T(sb);
+      f[idx27(sa, sb, 0)] = q4 * (Mxxyy + Bs * Mxxy + A * Mxyy + A * Bs * Mxy);
+      f[idx27(sa, 0, sb)] = q4 * (Mxxzz + Bs * Mxxz + A * Mxzz + A * Bs * Mxz);
+      f[idx27(0, sa, sb)] = q4 * (Myyzz + Bs * Myyz + A * Myzz + A * Bs * Myz);
+    }
+  const T Ax = Mxx - Mxxyy - Mxxzz, Bx = Mx - Mxyy - Mxzz;
+  const T Ay = Myy - Mxxyy - Myyzz, By = My - Mxxy - Myzz;
+  const T Az = Mzz - Mxxzz - Myyzz, Bz = Mz - Mxxz - Myyz;
+  f[idx27(1, 0, 0)] = T(0.5) * (Ax + Bx);
+  f[idx27(-1, 0, 0)] = T(0.5) * (Ax - Bx);
+  f[idx27(0, 1, 0)] = T(0.5) * (Ay + By);
+  f[idx27(0, -1, 0)] = T(0.5) * (Ay - By);
+  f[idx27(0, 0, 1)] = T(0.5) * (Az + Bz);
+  f[idx27(0, 0, -1)] = T(0.5) * (Az - Bz);
+  f[0] = rho - (Mxx + Myy + Mzz) + (Mxxyy + Mxxzz + Myyzz);
+}
+
 template <typename T>
 __device__ __forceinline__ T ld_stream(const T* p) {
   // read-only path with normal L2 allocation: the x-shifted rows of neighbouring tiles share
@@ -494,7 +590,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
   const T gpref = T(1) - T(0.5) * om, gmref = T(1) - T(0.5) * omm;
 
   if (!solid_tile) {
-    if constexpr (COLL == 2 && Q == 27)
+    if constexpr (COLL == 2)
       cumulant_update<T, FORCE>(f, rho, jx, jy, jz, ux, uy, uz, om, gl);
     else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
     else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
@@ -542,7 +638,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
     // occupancy of every tile)
     T* stash = nullptr;
     int tid = 0;
-    if constexpr (COLL == 2 && Q == 27) {
+    if constexpr (COLL == 2) {
       extern __shared__ __align__(16) unsigned char smem_raw[];
       stash = reinterpret_cast<T*>(smem_raw);
       tid = threadIdx.x + kTileX * (threadIdx.y + kTileY * threadIdx.z);
@@ -563,7 +659,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
         if (j < i) continue;  // each (i, ibar) pair once
         T fi = f[i], fj = f[j];
         T fci = fi, fcj = fj;  // fluid post-collision state (cumulant only)
-        if constexpr (COLL == 2 && Q == 27) {
+        if constexpr (COLL == 2) {
           fi = stash[i * kTileCells + tid];
           fj = stash[j * kTileCells + tid];
         }
@@ -573,7 +669,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
         const T sj = feq_q<Q, T>(j, rho, sux, suy, suz, susq15);
         // fluid operator on the pair: SRT, or TRT on the symmetric/antisymmetric parts
         T oFi, oFj;
-        if constexpr (COLL == 2 && Q == 27) {
+        if constexpr (COLL == 2) {
           oFi = fci - fi;
           oFj = fcj - fj;
         } else if (COLL == 1) {
@@ -615,7 +711,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
       m[1] = Bd * (double)msy;
       m[2] = Bd * (double)msz;
     } else {
-      if constexpr (COLL == 2 && Q == 27) {
+      if constexpr (COLL == 2) {
         // done above
       } else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
       else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
@@ -713,8 +809,9 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
     return cudaGetLastError();
   }
   if (p.trt == 2) {
-    // cumulant (D3Q27 only; no forcing): periodic fast path and the general variants
-    if constexpr (Q == 27) {
+    // cumulant (D3Q27, reading A29; D3Q19, reading A32): periodic fast path and the general
+    // variants
+    {
       const size_t sm = (size_t)Q * kTileCells * sizeof(T);  // PSM-cell stash
       // the >48 KB opt-in is a per-device function attribute: set once per instantiation and
       // device (bit per device ordinal)
@@ -748,8 +845,6 @@ static cudaError_t launch_variant(const CollideParams& p, int pat, bool force, b
       else if (pat == 1) k_collide<Q, T, 1, false, false, false, 2><<<grid, block, sm, st>>>(p);
       else k_collide<Q, T, 2, true, false, false, 2><<<grid, block, sm, st>>>(p);
       return cudaGetLastError();
-    } else {
-      return cudaErrorInvalidValue;
     }
   }
   if (dbg || force) {

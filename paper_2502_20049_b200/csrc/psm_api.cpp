@@ -99,8 +99,6 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
                      opt->body_force[2] != 0.0;
   if (force && opt->pattern == PSM_AA)
     FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "body force needs PSM_TWO_ARRAY");
-  if (opt->collision == PSM_CUMULANT && stencil != PSM_D3Q27)
-    FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "the cumulant operator needs D3Q27");
   if (world > 1 && opt->pattern == PSM_AA && grid->bc[0] != PSM_PERIODIC)
     FAIL((psm_ctx*)nullptr, PSM_E_UNSUPPORTED, "PSM_AA across ranks needs a periodic x axis");
   if (world > 1 && !opt->nccl_unique_id)

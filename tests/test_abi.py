@@ -68,7 +68,6 @@ def test_create_validation_codes():
         (dict(world=2, rank=2), _grid(), 19, psm.PSM_E_ARG),
         (dict(), _grid(8, 8, 8, (0, 3, 0)), 19, psm.PSM_E_ARG),
         (dict(coll=3), _grid(), 27, psm.PSM_E_ARG),
-        (dict(coll=2), _grid(), 19, psm.PSM_E_UNSUPPORTED),  # cumulant needs D3Q27
         (dict(coll=1, magic=0.0), _grid(), 19, psm.PSM_E_ARG),
         (dict(), _grid(8, 8, 8, (0, 2, 0)), 19, psm.PSM_E_UNSUPPORTED),  # open faces: x only
         (dict(), _grid(2, 8, 8, (2, 0, 0)), 19, psm.PSM_E_UNSUPPORTED),  # nx >= 3
