@@ -46,6 +46,13 @@ WORKLOADS = {
                   desc="c5 weak, fp64: D3Q19 PSM fp64 (the paper's precision), 512^3 per GPU, "
                        "CROR-like counter-rotating rotor pair per GPU (12+10 blades, ~1.1 M "
                        "faces, s=1, remapped every step), SC1, weighted B"),
+    # the paper's own performance configuration: D3Q19, cumulant (reading A32), AA
+    # in-place streaming, SC1, fp64, prescribed rotation — on the c5w rotor pair
+    "c5wpap": dict(nx=512, ny=512, nz=512, Q=19, prec="f64", tau=0.55, rotors=True, s=1,
+                   omega=0.05 / 220.0, pattern="aa", sc=1, bmode=1, collision="cumulant",
+                   desc="c5 weak, the paper's operator: D3Q19 cumulant AA fp64 PSM, 512^3 per "
+                        "GPU, CROR-like counter-rotating rotor pair per GPU (s=1, remapped every "
+                        "step), SC1, weighted B"),
     # c5w as an application run: inflow U = 0.05 at x = 0, pressure outflow at
     # x = nx-1 (reading A30), flow starting from rest
     "c5app": dict(nx=512, ny=512, nz=512, Q=19, prec="f32", tau=0.55, rotors=True, s=1,

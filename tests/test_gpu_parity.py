@@ -402,12 +402,17 @@ def test_r2_centre_only_mapping_rotating_mesh(s):
     assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
 
 
+@pytest.mark.parametrize("Q", [19, 27])
 @pytest.mark.parametrize("pattern,bc,prec", [("two_array", (0, 0, 0), "f64"),
                                              ("aa", (0, 1, 1), "f64"),
-                                             ("two_array", (0, 1, 0), "f32")])
-def test_cumulant_psm_rotating_mesh(pattern, bc, prec):
-    """Cumulant fluid operator (the paper's performance operator, D3Q27) inside the PSM update:
-    kernel factorised back-transform vs the oracle's 27x27 moment solve."""
+                                             ("aa", (0, 0, 0), "f64"),
+                                             ("two_array", (0, 1, 0), "f32"),
+                                             ("aa", (0, 0, 1), "f32")])
+def test_cumulant_psm_rotating_mesh(pattern, bc, prec, Q):
+    """Cumulant fluid operator (the paper's performance operator) inside the PSM
+    update: D3Q27 (A29, kernel factorised back-transform) and D3Q19 (A32, kernel closed-form
+    raw-moment inverse) against the oracle's moment solve (27x27 / 19x19).  D3Q19 + AA +
+    periodic + fp64 + SC1 + rotation is the paper's own performance configuration."""
     v, tr = pi.propeller_mesh(n_blades=3, scale=0.07, n_st=8, n_pts=16, hub_seg=16)
     w = np.array([0.025, 0.0, 0.0])
 
@@ -415,7 +420,7 @@ def test_cumulant_psm_rotating_mesh(pattern, bc, prec):
         return oracle.pose_advance(np.eye(3), [20.0, 11.0, 9.5], [0, 0, 0], w, k, [40, 22, 19],
                                    [1, 1, 1])
 
-    o, g = _run_pair(40, 22, 19, 27, 0.62, bc, 1, 1, prec, pattern,
+    o, g = _run_pair(40, 22, 19, Q, 0.62, bc, 1, 1, prec, pattern,
                      [dict(id=1, kind="mesh", verts=v, tris=tr, s=1, pose=pose, w=w)], 30, 19,
                      u0=(0.03, 0.0, 0.01), collision="cumulant", ft_every=(prec == "f64"),
                      ft_rel=FT_REL if prec == "f64" else 1e-4)  # fp32: ~30 steps of 1e-7 drift
@@ -438,7 +443,8 @@ def test_open_channel_moving_sphere_fp64(sc):
     assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
 
 
-@pytest.mark.parametrize("collision,Q", [("trt", 19), ("cumulant", 27), ("srt", 27)])
+@pytest.mark.parametrize("collision,Q", [("trt", 19), ("cumulant", 27), ("srt", 27),
+                                         ("cumulant", 19)])
 def test_open_channel_rotating_mesh_operators(collision, Q):
     v, tr = pi.propeller_mesh(n_blades=3, scale=0.07, n_st=8, n_pts=16, hub_seg=16)
     w = np.array([0.025, 0.0, 0.0])
@@ -602,10 +608,11 @@ def test_two_way_coupled_light_body_with_virtual_mass():
     assert g.body_state(1)[2][2] < 0  # sinking
 
 
-def test_cumulant_with_body_force():
+@pytest.mark.parametrize("Q", [19, 27])
+def test_cumulant_with_body_force(Q):
     """Cumulant operator with a Guo-type body force (reading A31) in a walled channel with a
     moving sphere: fp64 <= 1e-12 and F/T every step against the oracle."""
-    o, g = _run_pair(36, 20, 18, 27, 0.7, (0, 1, 0), 2, 1, "f64", "two_array",
+    o, g = _run_pair(36, 20, 18, Q, 0.7, (0, 1, 0), 2, 1, "f64", "two_array",
                      [dict(id=1, kind="sphere", r=4.5, s=1, v=(0.02, 0.0, 0.0),
                            pose=lambda k: (np.eye(3), (12.0 + 0.02 * k, 10.3, 9.1)))],
                      40, 47, u0=(0.02, 0.0, 0.0), force=(2e-5, 0.0, 1e-5),
@@ -629,3 +636,39 @@ def test_degenerate_one_cell_thick_grids(prec):
         o.step(50)
         g.step(50)
         assert np.max(np.abs(o.pdfs() - g.pdfs())) <= tol, (nx, ny, nz, bc)
+
+
+@pytest.mark.parametrize("sc", [1, 2, 3])
+def test_paper_configuration_d3q19_cumulant_aa_rotating_100_steps(sc):
+    """The paper's performance configuration: D3Q19, cumulant (A32), AA
+    in-place streaming, fp64, prescribed rotation of a triangle-mesh propeller, 100 steps,
+    fully periodic, with the library advancing the pose itself (psm_step(n) in chunks, so the
+    remap-ahead pipeline and the cached band run too) against the oracle fed
+    oracle.pose_advance poses: PDFs <= 1e-12, counts bit-exact, F/T of the last step."""
+    import paper_2502_20049_b200 as psm
+    nx, ny, nz = 44, 38, 36
+    v, tr = pi.propeller_mesh(n_blades=4, scale=0.13, n_st=10, n_pts=16, hub_seg=16)
+    w = np.array([0.02, 0.0, 0.0])
+    t0 = [21.3, 19.1, 17.7]
+    rho, u = pi.perturbed_flow((nz, ny, nx), 53, u0=(0.03, 0.0, 0.0))
+    o = oracle.Oracle(nx, ny, nz, 19, 0.55, (0, 0, 0), sc, 1)
+    o.set_collision("cumulant")
+    g = psm.Simulation(nx, ny, nz, Q=19, tau=0.55, prec="f64", pattern="aa", sc=sc, bmode=1,
+                       collision="cumulant")
+    o.init_equilibrium(rho, u)
+    g.init_equilibrium(rho, u)
+    o.set_mesh(1, v, tr, 1)
+    g.set_mesh(1, v, tr, 1, np.eye(3), t0, (0, 0, 0), w)
+    for k in range(100):
+        Qk, tk = oracle.pose_advance(np.eye(3), t0, (0, 0, 0), w, k, [nx, ny, nz], [1, 1, 1])
+        o.set_pose(1, Qk, tk, (0, 0, 0), w)
+        o.map()
+        o.step(1)
+    for n in (1, 7, 25, 33, 34):  # odd and even AA step counts, pipelined calls
+        g.step(n)
+    assert g.step_count == 100
+    assert np.array_equal(o.fractions()[2], g.fractions()[2])
+    d = np.max(np.abs(o.pdfs() - g.pdfs()))
+    assert d <= F64_TOL, d
+    ok, info = _ft_close(g.force_torque(1), o.force_torque(1))
+    assert ok, info
