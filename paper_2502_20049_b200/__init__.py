@@ -96,11 +96,15 @@ def load(build_if_missing: bool = True):
     if _lib is not None:
         return _lib
     from . import _build
-    if build_if_missing and _build.needs_build():
-        _build.build()
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build()")
-    L = C.CDLL(LIB_PATH)
+    alt = os.environ.get("PSM_LIB")  # kernel-tuning experiments: an in-tree variant build
+    if alt:
+        L = C.CDLL(os.path.abspath(alt))
+    else:
+        if build_if_missing and _build.needs_build():
+            _build.build()
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
     P, I32, I64, D, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_size_t
     sig = {
         "psm_create": [P, I32, D, P, P], "psm_destroy": [P], "psm_required_bytes": [P, P],

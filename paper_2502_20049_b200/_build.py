@@ -46,18 +46,30 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          extra_flags: str | None = None) -> str:
+    """Compile libpsm.so in-tree.  out / extra_flags: a variant library for kernel-tuning
+    experiments (loaded with PSM_LIB=<path>), never the default one."""
+    if out is not None:
+        return _build_to(out, extra_flags or "", verbose)
     if not force and not needs_build():
         return LIB
+    _build_to(LIB, _extra(), verbose)
+    with open(STAMP, "w") as fh:
+        fh.write(_extra() + "\n")
+    return LIB
+
+
+def _build_to(lib: str, extra: str, verbose: bool) -> str:
     from concurrent.futures import ThreadPoolExecutor
     nccl = nccl_dir()
     nvcc = os.environ.get("NVCC", "nvcc")
-    extra = _extra()  # diagnostics only, e.g. -DPSM_BOUNDS_CHECK (device-side bounds asserts)
+    # extra: diagnostics only, e.g. -DPSM_BOUNDS_CHECK (device-side bounds asserts)
     flags = [nvcc, "-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
              "-Xcompiler", "-fPIC,-fopenmp,-O2", "-Xptxas", "-warn-spills",
              "-I", os.path.join(ROOT, "include"), "-I", CSRC,
              "-I", os.path.join(nccl, "include")] + extra.split()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build", os.path.basename(lib))
     os.makedirs(objdir, exist_ok=True)
     objs, cmds = [], []
     for src in sources():  # one nvcc per translation unit, in parallel
@@ -77,16 +89,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stderr)
         if r.returncode != 0:
             raise subprocess.CalledProcessError(r.returncode, cmd, r.stdout, r.stderr)
-    link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp"] + \
+    link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib + ".tmp"] + \
         objs + ["-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
                 "-Xlinker", "-rpath," + os.path.join(nccl, "lib"), "-lgomp"]
     if verbose:
         print(" ".join(link), file=sys.stderr)
     subprocess.run(link, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    with open(STAMP, "w") as fh:
-        fh.write(extra + "\n")
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
