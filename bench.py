@@ -446,6 +446,7 @@ def main():
             "roofline_frac_step": res["step_frac"],
             "roofline": roofline_block(res, stream_gbs),
             "phases_ms": res["phases_ms"],
+            "nvlink_rank0": res["nvlink"],
             "gpu_launches": res["launches"],
             "clocks": res["clocks"],
             "e2e": res["e2e"],
@@ -510,6 +511,25 @@ def stream_copy_gbs(torch, nbytes=4 << 30, reps=10):
     return 2 * nbytes / (best / 1e3) / 1e9
 
 
+def nvlink_bytes(index: int):
+    """(tx, rx) NVLink data bytes of GPU `index` since the driver started, from NVML's
+    throughput counters (KiB; aggregate over links), or None where unsupported."""
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(index)
+        fids = [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX]
+        tot = [0, 0]
+        for link in range(18):
+            vals = nv.nvmlDeviceGetFieldValues(h, [(f, link) for f in fids])
+            for k, v in enumerate(vals):
+                if v.nvmlReturn == 0:
+                    tot[k] += int(v.value.ullVal)
+        return tot[0] * 1024, tot[1] * 1024
+    except Exception:
+        return None
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as fh:
@@ -543,6 +563,7 @@ def measure(psm, torch, dist, wl, args, rank, world, local, nccl_id, e2e=True, c
     l0 = sim.launches
     sim.profile(True)
     times = []
+    nvl0 = nvlink_bytes(local) if world > 1 else None
     with ClockSampler(local) as clk:
         for _ in range(max(1, args.reps)):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -557,9 +578,21 @@ def measure(psm, torch, dist, wl, args, rank, world, local, nccl_id, e2e=True, c
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
             times.append(ms)
+    nvl1 = nvlink_bytes(local) if world > 1 else None
     sim.profile(False)
     prof = sim.profile_read()
     reps = max(1, args.reps)
+    nvlink = None
+    if nvl0 and nvl1:
+        nsteps = reps * args.steps
+        # halo volume per rank and step: the c_z = +-1 populations of one nx*ny plane to each
+        # of the two z neighbours (5 of 19 / 9 of 27 directions)
+        qz = 5 if wl["Q"] == 19 else 9
+        nvlink = {"tx_bytes_per_step": (nvl1[0] - nvl0[0]) / nsteps,
+                  "rx_bytes_per_step": (nvl1[1] - nvl0[1]) / nsteps,
+                  "halo_bytes_per_step_expected": 2 * qz * nx * ny * S,
+                  "source": "NVML NVLink data throughput counters of this rank's GPU "
+                            "around the timed repetitions"}
     launches = (sim.launches - l0) // reps
     ms_med = float(np.median(times))
     cells_local = nx * ny * nzl
@@ -639,7 +672,7 @@ def measure(psm, torch, dist, wl, args, rank, world, local, nccl_id, e2e=True, c
             "step_frac": step_gbs / load_peak()[0], "step_gbs": step_gbs,
             "achieved": achieved, "bpu": bpu, "avg_launch_ms": avg, "launches_timed": coll_n,
             "phases_ms": {k: v[0] / (max(1, args.steps) * reps) for k, v in prof.items()},
-            "launches": launches, "clocks": clk.summary(), "e2e": e2e_line,
+            "launches": launches, "clocks": clk.summary(), "e2e": e2e_line, "nvlink": nvlink,
             "config": dict(workload_config(wl, world), **halo_cfg)}
 
 

@@ -78,12 +78,18 @@ __device__ __forceinline__ void tile_partial_reduce(int myid, const double* v, d
       if (tid == 0) out[s * (1 + kSlotVals)] = 0.0;
       continue;
     }
+    // warps (x rows) without a contributing cell skip the butterflies (sums of zeros); the
+    // order of the additions of the others is unchanged, so the result is too
+    if (__any_sync(0xFFFFFFFFu, (unsigned)myid == ids[s])) {
 #pragma unroll
-    for (int k = 0; k < kSlotVals; ++k) {
-      double a = ((unsigned)myid == ids[s]) ? v[k] : 0.0;
+      for (int k = 0; k < kSlotVals; ++k) {
+        double a = ((unsigned)myid == ids[s]) ? v[k] : 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
-      if (lane == 0) s_red[warp][k] = a;
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+        if (lane == 0) s_red[warp][k] = a;
+      }
+    } else if (lane < kSlotVals) {
+      s_red[warp][lane] = 0.0;
     }
     __syncthreads();
     if (tid < kSlotVals) {
