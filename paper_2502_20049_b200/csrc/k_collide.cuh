@@ -858,8 +858,10 @@ cudaError_t launch_variant(const CollideParams& p, int pat, bool force, bool dbg
       else k_collide<Q, T, 0, true, false, false, 1><<<grid, block, 0, st>>>(p);
     } else if (pat == 1) {
       k_collide<Q, T, 1, false, false, false, 1><<<grid, block, 0, st>>>(p);
-    } else {
+    } else if (walls) {
       k_collide<Q, T, 2, true, false, false, 1><<<grid, block, 0, st>>>(p);
+    } else {
+      k_collide<Q, T, 2, false, false, false, 1><<<grid, block, 0, st>>>(p);
     }
     return cudaGetLastError();
   }
