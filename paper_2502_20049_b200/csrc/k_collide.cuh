@@ -470,10 +470,13 @@ template <int Q, typename T, int PAT, int COLL, int WALLS>
 constexpr int collide_min_blocks() {
   // fp64: two blocks (the populations alone are 2*Q registers)
   if (sizeof(T) == 8) return 2;
+  // D3Q27 AA odd step, periodic (destinations recomputed after the collision): three fp32
+  // blocks at 80 registers (measured 88.2 -> 96.9 % SRT, 82.1 -> 90.6 % cumulant vs two)
+  if (Q == 27 && PAT == 2 && !WALLS) return 3;
   // the D3Q27 cumulant keeps a 3x3x3 moment array live (PSM cells stash f in shared memory
-  // instead of registers): four fp32 blocks (148 B of spills, but measured 1.4 % faster than
-  // three on c5wcum), AA odd two
-  if (COLL == 2 && Q == 27) return PAT == 2 ? 2 : 4;
+  // instead of registers): three fp32 blocks, no spills (four spill 148 B; measured on one box
+  // 88.1 % at four vs 93.8 % at three, fluid-only 384^3), AA odd with walls two
+  if (COLL == 2 && Q == 27) return PAT == 2 ? 2 : 3;
   // D3Q19 (SRT, TRT, D3Q19 cumulant): four fp32 blocks; the AA odd step with walls keeps the
   // bounce-back selects live as well (three)
   if (Q == 19) return (PAT == 2 && WALLS) ? 3 : 4;
