@@ -630,12 +630,76 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
   const T om = T(p.omega), omm = T(p.omega_m);
   const T gpref = T(1) - T(0.5) * om, gmref = T(1) - T(0.5) * omm;
 
-  if (!solid_tile) {
+  // ---- fused halo + scatter (called once, from the fluid-tile or the PSM-tile path) ----
+  auto store_all = [&]() {
+    // ---- fused halo: the populations leaving the slab through z go straight into the
+    // neighbours' ghost planes (peer stores over NVLink), replacing the separate exchange ----
+    if (PAT == 0 && act && p.p2p) {  // (multi-rank runs are two-array only)
+      const int pl = yc * nx + xc;
+      PSM_CHECK_OFF(pl, (long long)nx * ny);
+      if (z == G.nzl - 1) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (stc_z(q) > 0 && p.gup[q]) static_cast<T*>(p.gup[q])[pl] = f[q];
+      }
+      if (z == 0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (stc_z(q) < 0 && p.gdn[q]) static_cast<T*>(p.gdn[q])[pl] = f[q];
+      }
+    }
+
+    // ---- scatter ----
+    if constexpr (PAT == 2) {
+      // AA odd step: the destination offsets are recomputed here instead of keeping the gather's
+      // offsets live through the collision — register pressure sets this kernel's occupancy
+      // (measured: fp64 SRT 92.3 -> 95.8 %, fp64 cumulant 88.4 -> 94.5 % of HBM; the fp32
+      // kernels then fit four blocks per SM)
+      int xr = xc, yr = yc, zr = zc;
+      asm volatile("" : "+r"(xr), "+r"(yr), "+r"(zr));
+      const int selfr = (zr + G.zghost) * plane + yr * nx + xr;
+      int OXr[3], OYr[3], OZr[3];
+      bool OUTXr[3], OUTYr[3], OUTZr[3];
+      stencil_offsets<WALLS>(G, xr, yr, zr, OXr, OYr, OZr, OUTXr, OUTYr, OUTZr);
+      if (act) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          // destination x + c_q == source position of the opposite direction
+          const int cx = 1 - stc_x(q), cy = 1 - stc_y(q), cz = 1 - stc_z(q);
+          const bool out = WALLS && (OUTXr[cx] || OUTYr[cy] || OUTZr[cz]);
+          const int off = out ? selfr : selfr + OYr[cy] + OZr[cz] + OXr[cx];
+          PSM_CHECK_OFF(off, G.qstride);
+          static_cast<T*>(p.dstq[out ? stc_opp(q) : q])[off] = f[q];
+        }
+      }
+    } else if (act) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        T* Dq = static_cast<T*>(p.dstq[q]);
+        T* Do = static_cast<T*>(p.dstq[stc_opp(q)]);
+        if (PAT == 0) {
+          PSM_CHECK_OFF(self, G.qstride);
+          Dq[self] = f[q];  // default write-back policy: measured 0.9 % faster than __stcs (c5w)
+        } else {
+          Do[self] = f[q];
+        }
+      }
+    }
+  };
+
+  if (!solid_tile) {  // fluid tile: plain fluid operator, store, done
     if constexpr (COLL == 2)
       cumulant_update<T, FORCE>(f, rho, jx, jy, jz, ux, uy, uz, om, gl);
     else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
     else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
-  } else {
+    store_all();
+    return;
+  }
+  // Eq.(10) summand m = B sum_i Omega^S_i c_i of this cell and its body (0: none); reduced per
+  // tile after the scatter, so the block barriers of the reduction never hold back the stores
+  double m[3] = {0.0, 0.0, 0.0};
+  int myid = 0;
+  {
     // ---- PSM cell: B, u_s from the solid word (or the test-only dense fields) ----
     int id = 0;
     double Bd = 0.0;
@@ -672,7 +736,6 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
         }
       }
     }
-    double m[3] = {0.0, 0.0, 0.0};
     // cumulant: every cell of the tile takes the fluid operator once, in place; a solid-covered
     // cell first puts its pre-collision f into a shared-memory stash ([q][thread], conflict-free)
     // so the PSM pair loop never holds both 27-vectors in registers (that peak would halve the
@@ -757,72 +820,28 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
       } else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
       else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
     }
-    // ---- per-body F/T partial of this tile (deterministic block reduction) ----
+    myid = (Bd > 0.0) ? id : 0;
+  }
+
+  store_all();
+  // ---- per-body F/T partial of this tile (deterministic block reduction, Eqs.(10)-(11)) ----
+  {
     double v[kSlotVals];
+    double r[3] = {0.0, 0.0, 0.0};
+    if (myid) {  // lever arm x_c - R, minimum image (reading A7)
+      const BodyKin& b = p.bodies[myid];
+      const double L[3] = {(double)nx, (double)ny, (double)G.nz_global};
+      const double xcen[3] = {x + 0.5, y + 0.5, (double)(G.z0 + z) + 0.5};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) r[a] = min_image(xcen[a] - b.t[a], L[a], !G.wall[a]);
+    }
     v[0] = m[0]; v[1] = m[1]; v[2] = m[2];
     v[3] = r[1] * m[2] - r[2] * m[1];
     v[4] = r[2] * m[0] - r[0] * m[2];
     v[5] = r[0] * m[1] - r[1] * m[0];
 #pragma unroll
     for (int a = 0; a < 6; ++a) v[6 + a] = fabs(v[a]);
-    const int myid = (Bd > 0.0) ? id : 0;
     tile_partial_reduce(myid, v, p.partial + (size_t)tile * 2 * (1 + kSlotVals), p.overflow);
-  }
-
-  // ---- fused halo: the populations leaving the slab through z go straight into the
-  // neighbours' ghost planes (peer stores over NVLink), replacing the separate exchange ----
-  if (PAT == 0 && act && p.p2p) {  // (multi-rank runs are two-array only)
-    const int pl = yc * nx + xc;
-    PSM_CHECK_OFF(pl, (long long)nx * ny);
-    if (z == G.nzl - 1) {
-#pragma unroll
-      for (int q = 0; q < Q; ++q)
-        if (stc_z(q) > 0 && p.gup[q]) static_cast<T*>(p.gup[q])[pl] = f[q];
-    }
-    if (z == 0) {
-#pragma unroll
-      for (int q = 0; q < Q; ++q)
-        if (stc_z(q) < 0 && p.gdn[q]) static_cast<T*>(p.gdn[q])[pl] = f[q];
-    }
-  }
-
-  // ---- scatter ----
-  if constexpr (PAT == 2) {
-    // AA odd step: the destination offsets are recomputed here instead of keeping the gather's
-    // offsets live through the collision — register pressure sets this kernel's occupancy
-    // (measured: fp64 SRT 92.3 -> 95.8 %, fp64 cumulant 88.4 -> 94.5 % of HBM; the fp32
-    // kernels then fit four blocks per SM)
-    int xr = xc, yr = yc, zr = zc;
-    asm volatile("" : "+r"(xr), "+r"(yr), "+r"(zr));
-    const int selfr = (zr + G.zghost) * plane + yr * nx + xr;
-    int OXr[3], OYr[3], OZr[3];
-    bool OUTXr[3], OUTYr[3], OUTZr[3];
-    stencil_offsets<WALLS>(G, xr, yr, zr, OXr, OYr, OZr, OUTXr, OUTYr, OUTZr);
-    if (act) {
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        // destination x + c_q == source position of the opposite direction
-        const int cx = 1 - stc_x(q), cy = 1 - stc_y(q), cz = 1 - stc_z(q);
-        const bool out = WALLS && (OUTXr[cx] || OUTYr[cy] || OUTZr[cz]);
-        const int off = out ? selfr : selfr + OYr[cy] + OZr[cz] + OXr[cx];
-        PSM_CHECK_OFF(off, G.qstride);
-        static_cast<T*>(p.dstq[out ? stc_opp(q) : q])[off] = f[q];
-      }
-    }
-    return;
-  }
-  if (act) {
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      T* Dq = static_cast<T*>(p.dstq[q]);
-      T* Do = static_cast<T*>(p.dstq[stc_opp(q)]);
-      if (PAT == 0) {
-        PSM_CHECK_OFF(self, G.qstride);
-        Dq[self] = f[q];  // default write-back policy: measured 0.9 % faster than __stcs (c5w)
-      } else {
-        Do[self] = f[q];
-      }
-    }
   }
 }
 

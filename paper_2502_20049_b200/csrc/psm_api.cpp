@@ -136,6 +136,8 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   for (int a = 0; a < 3; ++a) g.wall[a] = grid->bc[a] != PSM_PERIODIC;
   g.open_x = grid->bc[0] == PSM_INOUT;
   g.qstride = (long long)(c->nzl + 2 * g.zghost) * grid->ny * grid->nx;
+  if (const char* e = std::getenv("PSM_PLANE_PAD"))  // tuning: elements between direction planes
+    g.qstride += (std::max(0ll, std::atoll(e)) + 31) / 32 * 32;
   g.gx = (int)((grid->nx + kTileX - 1) / kTileX);
   g.gy = (int)((grid->ny + kTileY - 1) / kTileY);
   g.gz = (int)((c->nzl + kTileZ - 1) / kTileZ);

@@ -101,13 +101,15 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default=None)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--scen", default="A,B")
+    ap.add_argument("--vars", default="V0,V1,V2,V3,V4")
     a = ap.parse_args()
     import bench
     peak, _ = bench.load_peak()
     rows = []
     for op in a.ops.split(","):
-        for scen in ("A", "B"):
-            for var in ("V0", "V1", "V2", "V3", "V4"):
+        for scen in a.scen.split(","):
+            for var in a.vars.split(","):
                 t0 = time.time()
                 r = run(op, scen, var, a.steps, a.warmup, a.reps)
                 r["frac"] = r["mlups"] * 1e6 * 2 * OPS[op][0] * 8 / (peak * 1e9)
@@ -122,8 +124,8 @@ def main():
              "| operator | scen. | variant | MLUPS | % of HBM | vs V0 | faces | solid cells |",
              "|---|---|---|---|---|---|---|---|"]
     for r in rows:
-        v0 = next(x for x in rows if x["op"] == r["op"] and x["scen"] == r["scen"] and
-                  x["var"] == "V0")
+        v0 = next((x for x in rows if x["op"] == r["op"] and x["scen"] == r["scen"] and
+                   x["var"] == "V0"), r)
         ov = r["mlups"] / v0["mlups"] - 1.0
         lines.append(f"| {r['op']} | {r['scen']} | {r['var']} | {r['mlups']:.0f} | "
                      f"{100 * r['frac']:.1f} | {100 * ov:+.1f} % | {r['faces']} | "

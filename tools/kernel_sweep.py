@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--n", type=int, default=384)
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--pads", default="", help="comma list of PSM_PLANE_PAD values to cycle")
     ap.add_argument("--only", default="srt19f64,srt19f64aa,cum19f64,cum19f64aa,srt19f32aa,"
                                       "cum27f32,cum27f64,cum19f32aa")
     a = ap.parse_args()
@@ -38,13 +39,18 @@ def main():
     import paper_2502_20049_b200 as psm
     peak, _ = bench.load_peak()
     n = a.n
-    for name in a.only.split(","):
+    pads = a.pads.split(",") if a.pads else [None]
+    for name, pad in [(nm, pd) for nm in a.only.split(",") for pd in pads]:
         Q, prec, pat, coll = VARIANTS[name]
+        if pad is not None:
+            os.environ["PSM_PLANE_PAD"] = pad
         sim = psm.Simulation(n, n, n, Q=Q, tau=0.6, prec=prec, pattern=pat, collision=coll)
         sim.init_equilibrium(None, None)
         sim.step(4)
         st = torch.cuda.current_stream()
         times = []
+        clk = bench.ClockSampler(torch.cuda.current_device())
+        clk.__enter__()
         for _ in range(a.reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
@@ -53,14 +59,16 @@ def main():
             e1.record(st)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / a.steps)
+        clk.__exit__()
         sim.close()
         del sim
         torch.cuda.empty_cache()
         ms = float(np.median(times))
         mlups = n ** 3 / (ms / 1e3) / 1e6
         S = 8 if prec == "f64" else 4
-        print(json.dumps({"variant": name, "n": n, "ms_per_step": ms, "mlups": mlups,
-                          "frac": mlups * 1e6 * 2 * Q * S / (peak * 1e9)}), flush=True)
+        print(json.dumps({"variant": name, "n": n, "pad": pad, "ms_per_step": ms, "mlups": mlups,
+                          "frac": mlups * 1e6 * 2 * Q * S / (peak * 1e9),
+                          "clocks": clk.summary()}), flush=True)
 
 
 if __name__ == "__main__":
