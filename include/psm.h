@@ -98,6 +98,9 @@ typedef struct {
  * Ownership: *out is owned by the caller and released with psm_destroy. */
 psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
                       const psm_options* opt, psm_ctx** out);
+/* Release the context and everything it allocated.  Collective when world > 1 and the fused
+ * peer-store halo is active (psm_halo_mode 2): the neighbours map this rank's memory, so every
+ * rank calls psm_destroy (an NCCL barrier precedes the release). */
 psm_status psm_destroy(psm_ctx* ctx);
 
 /* Device bytes the big per-rank fields need (PDF storage, solid words, tile flags, partials,
