@@ -23,3 +23,7 @@ for link in range(2):
     except Exception as e:
         print("state exc", e)
 PY
+# counters around a 2-rank fused-halo run of the default workload (fp64 c5w64, 40 steps)
+nvidia-smi nvlink -gt d > gpurun_out/nvlink_before.txt 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29591 bench.py --gpus 2 --steps 40 --warmup 3 --reps 1 --extra none --no-e2e > gpurun_out/nvlink_bench.json 2> gpurun_out/nvlink_bench.err
+nvidia-smi nvlink -gt d > gpurun_out/nvlink_after.txt 2>&1
