@@ -239,24 +239,90 @@ __device__ __forceinline__ void back1d(T k0, T k1, T k2, T v, T& fm, T& f0, T& f
   fm = T(0.5) * (m2 - m1);
 }
 
+// population of velocity (cx, cy, cz), zero for the D3Q27 corners a D3Q19 array does not hold
+template <int Q, typename T>
+__device__ __forceinline__ T fpop(const T (&f)[Q], int cx, int cy, int cz) {
+  const int q = idx27(cx, cy, cz);
+  return q < Q ? f[q < Q ? q : 0] : T(0);
+}
+
+// 1-D forward transform along one axis: (f-, f0, f+) -> raw moments of orders 0, 1, 2
+template <typename T>
+__device__ __forceinline__ void fwd1d(T fm, T f0, T fp, T& k0, T& k1, T& k2) {
+  k2 = fp + fm;
+  k0 = k2 + f0;
+  k1 = fp - fm;
+}
+
+// Raw moments of orders <= 2 (rho, j, the six second moments) by factorised 1-D sums along z,
+// y, then x — the forward transform restricted to what the cumulant operators use (the compiler
+// drops the unused branches): ~66 additions for D3Q27 instead of ~170 with one sum per moment;
+// the D3Q19 corners fold away.  mm = {rho, jx, jy, jz, mxx, myy, mzz, mxy, mxz, myz}.
+template <int Q, typename T>
+__device__ __forceinline__ void raw_moments2(const T (&f)[Q], T (&mm)[10]) {
+  T zm[3][3][3], ym[3][3][3], xm[3][3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      fwd1d(fpop<Q, T>(f, a - 1, b - 1, -1), fpop<Q, T>(f, a - 1, b - 1, 0),
+            fpop<Q, T>(f, a - 1, b - 1, 1), zm[a][b][0], zm[a][b][1], zm[a][b][2]);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      fwd1d(zm[a][0][c], zm[a][1][c], zm[a][2][c], ym[a][0][c], ym[a][1][c], ym[a][2][c]);
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      fwd1d(ym[0][b][c], ym[1][b][c], ym[2][b][c], xm[0][b][c], xm[1][b][c], xm[2][b][c]);
+  mm[0] = xm[0][0][0];
+  mm[1] = xm[1][0][0];
+  mm[2] = xm[0][1][0];
+  mm[3] = xm[0][0][1];
+  mm[4] = xm[2][0][0];
+  mm[5] = xm[0][2][0];
+  mm[6] = xm[0][0][2];
+  mm[7] = xm[1][1][0];
+  mm[8] = xm[1][0][1];
+  mm[9] = xm[0][1][1];
+}
+
+// second raw moments: precomputed (PRE, raw_moments2 in the kernel prologue) or one sum each
+template <int Q, typename T, bool PRE>
+__device__ __forceinline__ void second_moments(const T (&f)[Q], const T (&pre)[6], T (&m2)[6]) {
+  if constexpr (PRE) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) m2[k] = pre[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) m2[k] = T(0);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int cx = stc_x(q), cy = stc_y(q), cz = stc_z(q);
+      if (cx) m2[0] += f[q];
+      if (cy) m2[1] += f[q];
+      if (cz) m2[2] += f[q];
+      if (cx * cy > 0) m2[3] += f[q]; else if (cx * cy < 0) m2[3] -= f[q];
+      if (cx * cz > 0) m2[4] += f[q]; else if (cx * cz < 0) m2[4] -= f[q];
+      if (cy * cz > 0) m2[5] += f[q]; else if (cy * cz < 0) m2[5] -= f[q];
+    }
+  }
+}
+
 // Cumulant collision (the paper's performance operator), D3Q27, every rate of
 // order >= 3 and the bulk rate equal to 1, shear rate omega: normalised second cumulants
 // C = kappa / rho relaxed; post-collision central moments are those of a distribution whose
 // cumulants of order >= 3 vanish (Wick products); three 1-D backward transforms give f*.
-template <typename T, bool FORCE = false>
-__device__ __forceinline__ void cumulant_update(T (&f)[27], T rho, T jx, T jy, T jz, T ux, T uy,
-                                                T uz, T om, const T (&g)[3]) {
-  T mxx = T(0), myy = T(0), mzz = T(0), mxy = T(0), mxz = T(0), myz = T(0);
-#pragma unroll
-  for (int q = 0; q < 27; ++q) {
-    const int cx = stc_x(q), cy = stc_y(q), cz = stc_z(q);
-    if (cx) mxx += f[q];
-    if (cy) myy += f[q];
-    if (cz) mzz += f[q];
-    if (cx * cy > 0) mxy += f[q]; else if (cx * cy < 0) mxy -= f[q];
-    if (cx * cz > 0) mxz += f[q]; else if (cx * cz < 0) mxz -= f[q];
-    if (cy * cz > 0) myz += f[q]; else if (cy * cz < 0) myz -= f[q];
-  }
+// (second raw moments m_ab from raw_moments2)
+template <typename T, bool FORCE = false, bool PRE = true>
+__device__ __forceinline__ void cumulant_update(T (&f)[27], T rho, T jx, T jy, T jz,
+                                                const T (&m2pre)[6], T ux, T uy, T uz, T om,
+                                                const T (&g)[3]) {
+  T m2[6];
+  second_moments<27, T, PRE>(f, m2pre, m2);
+  const T mxx = m2[0], myy = m2[1], mzz = m2[2], mxy = m2[3], mxz = m2[4], myz = m2[5];
   const T ir = T(1) / rho;
   // second central moments about u: m_ab - u_a j_b - u_b j_a + rho u_a u_b, which is
   // m_ab - u_a j_b for u = j / rho; with a force u = (j + g/2)/rho (reading A31) and j_b is
@@ -367,20 +433,13 @@ __device__ __forceinline__ void plane_raw(T u, T v, T ku, T kv, T kuv, T kuuvv, 
           rho * uu * vv;
 }
 
-template <typename T, bool FORCE = false>
-__device__ __forceinline__ void cumulant_update(T (&f)[19], T rho, T jx, T jy, T jz, T ux, T uy,
-                                                T uz, T om, const T (&g)[3]) {
-  T mxx = T(0), myy = T(0), mzz = T(0), mxy = T(0), mxz = T(0), myz = T(0);
-#pragma unroll
-  for (int q = 0; q < 19; ++q) {
-    const int cx = stc_x(q), cy = stc_y(q), cz = stc_z(q);
-    if (cx) mxx += f[q];
-    if (cy) myy += f[q];
-    if (cz) mzz += f[q];
-    if (cx * cy > 0) mxy += f[q]; else if (cx * cy < 0) mxy -= f[q];
-    if (cx * cz > 0) mxz += f[q]; else if (cx * cz < 0) mxz -= f[q];
-    if (cy * cz > 0) myz += f[q]; else if (cy * cz < 0) myz -= f[q];
-  }
+template <typename T, bool FORCE = false, bool PRE = true>
+__device__ __forceinline__ void cumulant_update(T (&f)[19], T rho, T jx, T jy, T jz,
+                                                const T (&m2pre)[6], T ux, T uy, T uz, T om,
+                                                const T (&g)[3]) {
+  T m2[6];
+  second_moments<19, T, PRE>(f, m2pre, m2);
+  const T mxx = m2[0], myy = m2[1], mzz = m2[2], mxy = m2[3], mxz = m2[4], myz = m2[5];
   const T ir = T(1) / rho;
   T Cxx0, Cyy0, Czz0, Kxy, Kxz, Kyz, hx = T(0), hy = T(0), hz = T(0);
   if constexpr (FORCE) {
@@ -607,13 +666,30 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
   }
 
   // ---- moments ----
-  T rho = f[0], jx = T(0), jy = T(0), jz = T(0);
+  T rho, jx, jy, jz;
+  T m2[6];  // second raw moments (cumulant only)
+  // (D3Q19 AA: the second moments are summed inside the operator, as in the plain loop, which
+  // measured 1-3 % faster there than the factorised sums in the prologue)
+  constexpr bool kFactMoments = COLL == 2 && !(Q == 19 && PAT != 0);
+  if constexpr (kFactMoments) {
+    T mm[10];
+    raw_moments2<Q, T>(f, mm);
+    rho = mm[0];
+    jx = mm[1];
+    jy = mm[2];
+    jz = mm[3];
 #pragma unroll
-  for (int q = 1; q < Q; ++q) {
-    rho += f[q];
-    if (stc_x(q) > 0) jx += f[q]; else if (stc_x(q) < 0) jx -= f[q];
-    if (stc_y(q) > 0) jy += f[q]; else if (stc_y(q) < 0) jy -= f[q];
-    if (stc_z(q) > 0) jz += f[q]; else if (stc_z(q) < 0) jz -= f[q];
+    for (int k = 0; k < 6; ++k) m2[k] = mm[4 + k];
+  } else {
+    rho = f[0];
+    jx = jy = jz = T(0);
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+      rho += f[q];
+      if (stc_x(q) > 0) jx += f[q]; else if (stc_x(q) < 0) jx -= f[q];
+      if (stc_y(q) > 0) jy += f[q]; else if (stc_y(q) < 0) jy -= f[q];
+      if (stc_z(q) > 0) jz += f[q]; else if (stc_z(q) < 0) jz -= f[q];
+    }
   }
   if (act && !(rho > T(0) && rho < T(INFINITY))) {
     const long long cell = ((long long)(G.z0 + z) * G.ny + y) * (long long)G.nx + x;
@@ -689,7 +765,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
 
   if (!solid_tile) {  // fluid tile: plain fluid operator, store, done
     if constexpr (COLL == 2)
-      cumulant_update<T, FORCE>(f, rho, jx, jy, jz, ux, uy, uz, om, gl);
+      cumulant_update<T, FORCE, kFactMoments>(f, rho, jx, jy, jz, m2, ux, uy, uz, om, gl);
     else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
     else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
     store_all();
@@ -750,7 +826,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
 #pragma unroll
         for (int q = 0; q < Q; ++q) stash[q * kTileCells + tid] = f[q];
       }
-      cumulant_update<T, FORCE>(f, rho, jx, jy, jz, ux, uy, uz, om, gl);
+      cumulant_update<T, FORCE, kFactMoments>(f, rho, jx, jy, jz, m2, ux, uy, uz, om, gl);
     }
     if (Bd > 0.0) {
       const T B = T(Bd), B1 = T(1) - T(Bd);
