@@ -30,13 +30,6 @@
 
 namespace psm {
 
-template <int Q, typename T>
-__device__ __forceinline__ T feq_q(int q, T rho, T ux, T uy, T uz, T usq15) {
-  // w rho [1 + 3 c.u + 4.5 (c.u)^2 - 1.5 u.u]  (Eq.(3) with c_s^2 = 1/3, "-" sign: reading A1)
-  const T cu = T(stc_x(q)) * ux + T(stc_y(q)) * uy + T(stc_z(q)) * uz;
-  return T(stc_w<Q>(q)) * rho * (T(1) - usq15 + cu * (T(3) + T(4.5) * cu));
-}
-
 __device__ __forceinline__ double weight_fraction(double e, double tau, int mode) {
   // Eq.(6) in fp64, fixed operation order (bit-exact with the method definition, A14)
   if (mode == 0) return e;
@@ -44,65 +37,76 @@ __device__ __forceinline__ double weight_fraction(double e, double tau, int mode
   return __ddiv_rn(__dmul_rn(e, a), __dadd_rn(__dsub_rn(1.0, e), a));
 }
 
-// Deterministic per-tile reduction of the Eq.(10)-(11) summands: the (at most) two smallest
-// body ids present in the tile get a slot each (fixed warp-butterfly + fixed warp order), a third
-// or later body in the same tile falls back to fp64 atomics in `overflow` (never happens unless
-// bodies overlap one tile).  Slot layout: [id, v[0..11]].  Called by every thread of the block.
+// Deterministic per-tile reduction of the Eq.(10)-(11) summands without block barriers: each warp
+// reduces its (at most) two smallest body ids with butterflies and parks the partials in shared
+// memory; the warp that arrives last (shared counter, zeroed before the collision) combines them
+// for the tile's two smallest ids in fixed warp order and writes the tile's slots.  A third or
+// later body in one tile falls back to fp64 atomics in `overflow` (never happens unless bodies
+// overlap one tile).  Slot layout in `out`: [id, v[0..11]] x 2.  Called by every thread of the
+// block; no warp waits for another.
+struct TileRed {
+  unsigned cnt;
+  double part[kTileCells / 32][2][1 + kSlotVals];  // per warp: [slot][id, values]
+};
+
 __device__ __forceinline__ void tile_partial_reduce(int myid, const double* v, double* out,
-                                                    double* overflow) {
-  __shared__ unsigned s_min[kTileCells / 32];
-  __shared__ unsigned s_ids[2];
-  __shared__ double s_red[kTileCells / 32][kSlotVals];
+                                                    double* overflow, TileRed& sh) {
+  constexpr unsigned FULL = 0xFFFFFFFFu, NONE = 0xFFFFFFFFu;
+  constexpr int NW = kTileCells / 32;
   const int tid = threadIdx.x + kTileX * (threadIdx.y + kTileY * threadIdx.z);
   const int lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = kTileCells / 32;
-  unsigned ids[2];
+  const unsigned me = myid ? (unsigned)myid : NONE;
+  const unsigned k0 = __reduce_min_sync(FULL, me);
+  const unsigned k1 = __reduce_min_sync(FULL, (me != k0) ? me : NONE);
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
-    const unsigned key = (myid && (s == 0 || (unsigned)myid != ids[0])) ? (unsigned)myid
-                                                                         : 0xFFFFFFFFu;
-    const unsigned k = __reduce_min_sync(0xFFFFFFFFu, key);
-    if (lane == 0) s_min[warp] = k;
-    __syncthreads();
-    if (tid == 0) {
-      unsigned mm = s_min[0];
-      for (int w = 1; w < NW; ++w) mm = min(mm, s_min[w]);
-      s_ids[s] = mm;
-    }
-    __syncthreads();
-    ids[s] = s_ids[s];
-  }
-#pragma unroll 1
-  for (int s = 0; s < 2; ++s) {
-    if (ids[s] == 0xFFFFFFFFu) {
-      if (tid == 0) out[s * (1 + kSlotVals)] = 0.0;
-      continue;
-    }
-    // warps (x rows) without a contributing cell skip the butterflies (sums of zeros); the
-    // order of the additions of the others is unchanged, so the result is too
-    if (__any_sync(0xFFFFFFFFu, (unsigned)myid == ids[s])) {
+    const unsigned id = s == 0 ? k0 : k1;
+    if (id != NONE) {
 #pragma unroll
       for (int k = 0; k < kSlotVals; ++k) {
-        double a = ((unsigned)myid == ids[s]) ? v[k] : 0.0;
+        double a = (me == id) ? v[k] : 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
-        if (lane == 0) s_red[warp][k] = a;
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(FULL, a, o);
+        if (lane == 0) sh.part[warp][s][1 + k] = a;
       }
-    } else if (lane < kSlotVals) {
-      s_red[warp][lane] = 0.0;
     }
-    __syncthreads();
-    if (tid < kSlotVals) {
-      double acc = s_red[0][tid];
-      for (int w = 1; w < NW; ++w) acc += s_red[w][tid];
-      out[s * (1 + kSlotVals) + 1 + tid] = acc;
-    }
-    if (tid == 0) out[s * (1 + kSlotVals)] = (double)ids[s];
-    __syncthreads();
+    if (lane == 0) sh.part[warp][s][0] = (id == NONE) ? -1.0 : (double)id;
   }
-  if (myid && (unsigned)myid != ids[0] && (unsigned)myid != ids[1]) {
+  if (me != NONE && me != k0 && me != k1)  // third+ body in this warp
     for (int k = 0; k < kSlotVals; ++k) atomicAdd(overflow + myid * kSlotVals + k, v[k]);
+  __syncwarp();
+  unsigned prev = 0;
+  __threadfence_block();
+  if (lane == 0) prev = atomicAdd(&sh.cnt, 1u);
+  prev = __shfl_sync(FULL, prev, 0);
+  if (prev != NW - 1) return;  // not the last warp of the tile
+  __threadfence_block();
+  // the tile's two smallest ids over every warp slot
+  const double idl = lane < 2 * NW ? sh.part[lane >> 1][lane & 1][0] : -1.0;
+  const unsigned key = idl >= 0.0 ? (unsigned)idl : NONE;
+  const unsigned t0 = __reduce_min_sync(FULL, key);
+  const unsigned t1 = __reduce_min_sync(FULL, (key != t0) ? key : NONE);
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const unsigned id = s == 0 ? t0 : t1;
+    double* o = out + s * (1 + kSlotVals);
+    if (id == NONE) {
+      if (lane == 0) o[0] = 0.0;
+      continue;
+    }
+    if (lane < kSlotVals) {
+      double acc = 0.0;
+      for (int w = 0; w < NW; ++w)
+        for (int t = 0; t < 2; ++t)
+          if (sh.part[w][t][0] == (double)id) acc += sh.part[w][t][1 + lane];
+      o[1 + lane] = acc;
+    }
+    if (lane == 0) o[0] = (double)id;
   }
+  // a warp slot whose id is not one of the tile's two: its partial goes to the atomics
+  if (lane < 2 * NW && key != NONE && key != t0 && key != t1)
+    for (int k = 0; k < kSlotVals; ++k)
+      atomicAdd(overflow + key * kSlotVals + k, sh.part[lane >> 1][lane & 1][1 + k]);
 }
 
 // explicitly rounded arithmetic: the fluid update must give the same bits wherever it runs
@@ -582,6 +586,12 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
   const bool act = (x < G.nx) && (y < G.ny) && (z < G.nzl);
   const int tile = (tzl * G.gy + blockIdx.y) * G.gx + blockIdx.x;
   const bool solid_tile = DBG ? true : (p.tile_flag[tile] != 0);
+  // PSM tiles, fp64: the cell's solid word is loaded now, with the populations, so its latency
+  // is not exposed after the moments (measured: D3Q19 fp64 AA 95.7 -> 100.7 % fluid-only,
+  // c5wpap 90.4 -> 96.5 %); the fp32 kernels lose occupancy with it and load it late
+  constexpr bool kWordEarly = sizeof(T) == 8;
+  const uint32_t wpre = (kWordEarly && !DBG && solid_tile && act)
+                            ? __ldg(p.word + (((long long)z * G.ny + y) * G.nx + x)) : 0u;
 
   const int nx = G.nx, ny = G.ny;
   const int plane = nx * ny;
@@ -634,6 +644,14 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
     else gather(std::false_type{});
   } else {
     gather(std::integral_constant<bool, (WALLS != 0)>{});
+  }
+
+  // PSM tiles: zero the arrival counter of the barrier-free F/T reduction (the one block barrier
+  // of the kernel, while the gathered loads are still in flight)
+  __shared__ TileRed s_tred;
+  if (solid_tile) {
+    if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) s_tred.cnt = 0u;
+    __syncthreads();
   }
 
   // ---- open x faces (reading A30): the populations entering at x = 0 / nx-1 were gathered
@@ -791,7 +809,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
         usd[1] = p.dbg_us[N + c];
         usd[2] = p.dbg_us[2 * N + c];
       } else {
-        const uint32_t w = p.word[((long long)z * ny + y) * nx + x];
+        const uint32_t w = kWordEarly ? wpre : p.word[((long long)z * ny + y) * nx + x];
         id = (int)(w >> 16);
         if (id) {
           const int cnt = (int)(w & 0xFFFFu);
@@ -843,10 +861,30 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
           fi = stash[i * kTileCells + tid];
           fj = stash[j * kTileCells + tid];
         }
-        const T ei = feq_q<Q, T>(i, rho, ux, uy, uz, usq15);
-        const T ej = feq_q<Q, T>(j, rho, ux, uy, uz, usq15);
-        const T si = feq_q<Q, T>(i, rho, sux, suy, suz, susq15);
-        const T sj = feq_q<Q, T>(j, rho, sux, suy, suz, susq15);
+        // equilibria of the pair: f^eq_i = a + b, f^eq_ibar = a - b with a = w rho (1 - 1.5 u.u
+        // + 4.5 (c.u)^2), b = 3 w rho c.u (Eq.(3)), for the fluid u and for u_s
+        // (per-direction form for D3Q27 fp32 SRT/TRT: measured 97.6 vs 92.3 % on the AA step;
+        // the pair form for every other variant, up to +16 % on the fp32 cumulant AA steps)
+        T ei, ej, si, sj;
+        if constexpr (COLL != 2 && Q == 27 && sizeof(T) == 4) {
+          auto feq = [&](int q, T ux_, T uy_, T uz_, T u15) {
+            const T c = T(stc_x(q)) * ux_ + T(stc_y(q)) * uy_ + T(stc_z(q)) * uz_;
+            return T(stc_w<Q>(q)) * rho * (T(1) - u15 + c * (T(3) + T(4.5) * c));
+          };
+          ei = feq(i, ux, uy, uz, usq15);
+          ej = feq(j, ux, uy, uz, usq15);
+          si = feq(i, sux, suy, suz, susq15);
+          sj = feq(j, sux, suy, suz, susq15);
+        } else {
+          const T wr = T(stc_w<Q>(i)) * rho;
+          const T cu = cdot<T>(i, ux, uy, uz), cs = cdot<T>(i, sux, suy, suz);
+          const T ae = wr * (T(1) - usq15 + T(4.5) * cu * cu), be = wr * (T(3) * cu);
+          const T as = wr * (T(1) - susq15 + T(4.5) * cs * cs), bs = wr * (T(3) * cs);
+          ei = ae + be;
+          ej = ae - be;
+          si = as + bs;
+          sj = as - bs;
+        }
         // fluid operator on the pair: SRT, or TRT on the symmetric/antisymmetric parts
         T oFi, oFj;
         if constexpr (COLL == 2) {
@@ -917,7 +955,8 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
     v[5] = r[0] * m[1] - r[1] * m[0];
 #pragma unroll
     for (int a = 0; a < 6; ++a) v[6 + a] = fabs(v[a]);
-    tile_partial_reduce(myid, v, p.partial + (size_t)tile * 2 * (1 + kSlotVals), p.overflow);
+    tile_partial_reduce(myid, v, p.partial + (size_t)tile * 2 * (1 + kSlotVals), p.overflow,
+                        s_tred);
   }
 }
 

@@ -35,6 +35,10 @@ OPS = {  # name -> (Q, collision, pattern)
     "srt27": (27, "srt", "two_array"),
     "cum27": (27, "cumulant", "two_array"),
     "cum19aa": (19, "cumulant", "aa"),  # the paper's own performance operator
+    "cum19": (19, "cumulant", "two_array"),
+    "srt19aa": (19, "srt", "aa"),
+    "srt19": (19, "srt", "two_array"),
+    "srt27aa": (27, "srt", "aa"),
 }
 N = 256
 _MESH = {}
