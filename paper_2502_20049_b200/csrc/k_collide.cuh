@@ -62,13 +62,27 @@ __device__ __forceinline__ void tile_partial_reduce(int myid, const double* v, d
   for (int s = 0; s < 2; ++s) {
     const unsigned id = s == 0 ? k0 : k1;
     if (id != NONE) {
+      // transpose butterfly: at each stage a lane keeps half of its values and receives the
+      // partner's copy of that half, so the 12 (padded 16) sums take 16 shuffles instead of
+      // 5 x 12; fixed order, so the result is deterministic.  Afterwards lane L (L even) holds
+      // the sum of value ((L>>4)&1)*8 + ((L>>3)&1)*4 + ((L>>2)&1)*2 + ((L>>1)&1).
+      double a[16];
 #pragma unroll
-      for (int k = 0; k < kSlotVals; ++k) {
-        double a = (me == id) ? v[k] : 0.0;
+      for (int k = 0; k < 16; ++k) a[k] = (k < kSlotVals && me == id) ? v[k < kSlotVals ? k : 0] : 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(FULL, a, o);
-        if (lane == 0) sh.part[warp][s][1 + k] = a;
+      for (int o = 16, n = 16; o > 1; o >>= 1, n >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < n / 2; ++k) {
+          const double send = up ? a[k] : a[k + n / 2];
+          const double keep = up ? a[k + n / 2] : a[k];
+          a[k] = keep + __shfl_xor_sync(FULL, send, o);
+        }
       }
+      a[0] += __shfl_xor_sync(FULL, a[0], 1);
+      const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                      ((lane >> 1) & 1);
+      if (!(lane & 1) && idx < kSlotVals) sh.part[warp][s][1 + idx] = a[0];
     }
     if (lane == 0) sh.part[warp][s][0] = (id == NONE) ? -1.0 : (double)id;
   }
@@ -590,6 +604,14 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
   // is not exposed after the moments (measured: D3Q19 fp64 AA 95.7 -> 100.7 % fluid-only,
   // c5wpap 90.4 -> 96.5 %); the fp32 kernels lose occupancy with it and load it late
   constexpr bool kWordEarly = sizeof(T) == 8;
+  // PSM tiles: every cell takes the fluid operator (uniform across the warp) and the solid-covered
+  // cells keep their pre-collision f in a shared-memory stash for the Eq.(4) blend, instead of a
+  // separate fluid path for the B = 0 lanes of a warp that also holds solid cells
+#if defined(PSM_STASH_ALL)
+  constexpr bool kStashAll = true;
+#else
+  constexpr bool kStashAll = COLL == 2;
+#endif
   const uint32_t wpre = (kWordEarly && !DBG && solid_tile && act)
                             ? __ldg(p.word + (((long long)z * G.ny + y) * G.nx + x)) : 0u;
 
@@ -836,7 +858,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
     // occupancy of every tile)
     T* stash = nullptr;
     int tid = 0;
-    if constexpr (COLL == 2) {
+    if constexpr (kStashAll) {
       extern __shared__ __align__(16) unsigned char smem_raw[];
       stash = reinterpret_cast<T*>(smem_raw);
       tid = threadIdx.x + kTileX * (threadIdx.y + kTileY * threadIdx.z);
@@ -844,7 +866,10 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
 #pragma unroll
         for (int q = 0; q < Q; ++q) stash[q * kTileCells + tid] = f[q];
       }
-      cumulant_update<T, FORCE, kFactMoments>(f, rho, jx, jy, jz, m2, ux, uy, uz, om, gl);
+      if constexpr (COLL == 2)
+        cumulant_update<T, FORCE, kFactMoments>(f, rho, jx, jy, jz, m2, ux, uy, uz, om, gl);
+      else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
+      else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
     }
     if (Bd > 0.0) {
       const T B = T(Bd), B1 = T(1) - T(Bd);
@@ -856,8 +881,8 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
         const int j = stc_opp(i);
         if (j < i) continue;  // each (i, ibar) pair once
         T fi = f[i], fj = f[j];
-        T fci = fi, fcj = fj;  // fluid post-collision state (cumulant only)
-        if constexpr (COLL == 2) {
+        T fci = fi, fcj = fj;  // fluid post-collision state (stash mode)
+        if constexpr (kStashAll) {
           fi = stash[i * kTileCells + tid];
           fj = stash[j * kTileCells + tid];
         }
@@ -887,7 +912,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
         }
         // fluid operator on the pair: SRT, or TRT on the symmetric/antisymmetric parts
         T oFi, oFj;
-        if constexpr (COLL == 2) {
+        if constexpr (kStashAll) {  // Omega^F from the fluid update every cell of the tile took
           oFi = fci - fi;
           oFj = fcj - fj;
         } else if (COLL == 1) {
@@ -899,7 +924,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
           oFi = om * (ei - fi);
           oFj = om * (ej - fj);
         }
-        if (FORCE && COLL != 2) {  // (the cumulant carries its force in fc, reading A31)
+        if (FORCE && !kStashAll) {  // (with the stash the force is in fc; cumulant: A31)
           T sp, sm;
           guo_pair<Q, T>(i, ux, uy, uz, gl, sp, sm);
           oFi += gpref * sp + gmref * sm;
@@ -929,7 +954,7 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
       m[1] = Bd * (double)msy;
       m[2] = Bd * (double)msz;
     } else {
-      if constexpr (COLL == 2) {
+      if constexpr (kStashAll) {
         // done above
       } else if (COLL == 1) fluid_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, omm, gl);
       else srt_update<Q, T, FORCE>(f, rho, ux, uy, uz, om, gl);
@@ -978,86 +1003,59 @@ cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool dbg, int 
   return launch_variant<Q, T>(pq, pat, force, dbg, grid, block, st);
 }
 
-template <int Q, typename T>
-cudaError_t launch_variant(const CollideParams& p, int pat, bool force, bool dbg,
-                                  dim3 grid, dim3 block, cudaStream_t st) {
+// One kernel instantiation: dynamic shared memory for the PSM-cell stash (when the variant uses
+// it), with the > 48 KB opt-in set once per instantiation and device (bit per device ordinal).
+template <int Q, typename T, int PAT, int WALLS, bool FORCE, bool DBG, int COLL>
+cudaError_t launch_k(const CollideParams& p, dim3 grid, dim3 block, cudaStream_t st) {
+#if defined(PSM_STASH_ALL)
+  constexpr bool stash = true;
+#else
+  constexpr bool stash = COLL == 2;
+#endif
+  constexpr size_t sm = stash ? (size_t)Q * kTileCells * sizeof(T) : 0;
+  if constexpr (sm > 48 * 1024) {
+    static unsigned long long attr_devices = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_devices & bit)) {
+      e = cudaFuncSetAttribute(k_collide<Q, T, PAT, WALLS, FORCE, DBG, COLL>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      attr_devices |= bit;
+    }
+  }
+  k_collide<Q, T, PAT, WALLS, FORCE, DBG, COLL><<<grid, block, sm, st>>>(p);
+  return cudaGetLastError();
+}
+
+// the variant for the context's operator, pattern, boundaries and test switches
+template <int Q, typename T, int COLL>
+cudaError_t launch_coll(const CollideParams& p, int pat, bool force, bool dbg, dim3 grid,
+                        dim3 block, cudaStream_t st) {
   const bool walls = p.g.wall[0] || p.g.wall[1] || p.g.wall[2];
   const bool xonly = p.g.wall[0] && !p.g.wall[1] && !p.g.wall[2];  // e.g. open x faces
-  if (p.trt == 1) {
-    // TRT: periodic and x-only fast paths for the pull pattern, general variants otherwise
-    if (dbg || force) {
-      if (dbg && force) k_collide<Q, T, 0, true, true, true, 1><<<grid, block, 0, st>>>(p);
-      else if (dbg) k_collide<Q, T, 0, true, false, true, 1><<<grid, block, 0, st>>>(p);
-      else k_collide<Q, T, 0, true, true, false, 1><<<grid, block, 0, st>>>(p);
-    } else if (pat == 0) {
-      if (!walls) k_collide<Q, T, 0, false, false, false, 1><<<grid, block, 0, st>>>(p);
-      else if (xonly) k_collide<Q, T, 0, 2, false, false, 1><<<grid, block, 0, st>>>(p);
-      else k_collide<Q, T, 0, true, false, false, 1><<<grid, block, 0, st>>>(p);
-    } else if (pat == 1) {
-      k_collide<Q, T, 1, false, false, false, 1><<<grid, block, 0, st>>>(p);
-    } else if (walls) {
-      k_collide<Q, T, 2, true, false, false, 1><<<grid, block, 0, st>>>(p);
-    } else {
-      k_collide<Q, T, 2, false, false, false, 1><<<grid, block, 0, st>>>(p);
-    }
-    return cudaGetLastError();
+  // body force / debug fields: general two-array variants only
+  if (dbg && force) return launch_k<Q, T, 0, 1, true, true, COLL>(p, grid, block, st);
+  if (dbg) return launch_k<Q, T, 0, 1, false, true, COLL>(p, grid, block, st);
+  if (force) return launch_k<Q, T, 0, 1, true, false, COLL>(p, grid, block, st);
+  if (pat == 0) {
+    if (!walls) return launch_k<Q, T, 0, 0, false, false, COLL>(p, grid, block, st);
+    if (xonly) return launch_k<Q, T, 0, 2, false, false, COLL>(p, grid, block, st);
+    return launch_k<Q, T, 0, 1, false, false, COLL>(p, grid, block, st);
   }
-  if (p.trt == 2) {
-    // cumulant (D3Q27, reading A29; D3Q19, reading A32): periodic fast path and the general
-    // variants
-    {
-      const size_t sm = (size_t)Q * kTileCells * sizeof(T);  // PSM-cell stash
-      // the >48 KB opt-in is a per-device function attribute: set once per instantiation and
-      // device (bit per device ordinal)
-      static unsigned long long attr_devices = 0;
-      int dev = 0;
-      if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
-      const unsigned long long bit = 1ull << (dev & 63);
-      if (!(attr_devices & bit)) {
-        const void* fns[9] = {(const void*)k_collide<Q, T, 2, false, false, false, 2>,
-                              (const void*)k_collide<Q, T, 0, true, false, true, 2>,
-                              (const void*)k_collide<Q, T, 0, false, false, false, 2>,
-                              (const void*)k_collide<Q, T, 0, true, false, false, 2>,
-                              (const void*)k_collide<Q, T, 0, 2, false, false, 2>,
-                              (const void*)k_collide<Q, T, 1, false, false, false, 2>,
-                              (const void*)k_collide<Q, T, 2, true, false, false, 2>,
-                              (const void*)k_collide<Q, T, 0, true, true, false, 2>,
-                              (const void*)k_collide<Q, T, 0, true, true, true, 2>};
-        for (const void* fn : fns) {
-          cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)sm);
-          if (e != cudaSuccess) return e;
-        }
-        attr_devices |= bit;
-      }
-      // body force (reading A31): general two-array variants only, as for SRT/TRT
-      if (force && dbg) k_collide<Q, T, 0, true, true, true, 2><<<grid, block, sm, st>>>(p);
-      else if (force) k_collide<Q, T, 0, true, true, false, 2><<<grid, block, sm, st>>>(p);
-      else if (dbg) k_collide<Q, T, 0, true, false, true, 2><<<grid, block, sm, st>>>(p);
-      else if (pat == 0 && !walls) k_collide<Q, T, 0, false, false, false, 2><<<grid, block, sm, st>>>(p);
-      else if (pat == 0 && xonly) k_collide<Q, T, 0, 2, false, false, 2><<<grid, block, sm, st>>>(p);
-      else if (pat == 0) k_collide<Q, T, 0, true, false, false, 2><<<grid, block, sm, st>>>(p);
-      else if (pat == 1) k_collide<Q, T, 1, false, false, false, 2><<<grid, block, sm, st>>>(p);
-      else if (walls) k_collide<Q, T, 2, true, false, false, 2><<<grid, block, sm, st>>>(p);
-      else k_collide<Q, T, 2, false, false, false, 2><<<grid, block, sm, st>>>(p);
-      return cudaGetLastError();
-    }
-  }
-  if (dbg || force) {
-    if (dbg && force) k_collide<Q, T, 0, true, true, true, 0><<<grid, block, 0, st>>>(p);
-    else if (dbg) k_collide<Q, T, 0, true, false, true, 0><<<grid, block, 0, st>>>(p);
-    else k_collide<Q, T, 0, true, true, false, 0><<<grid, block, 0, st>>>(p);
-  } else if (pat == 0) {
-    if (xonly) k_collide<Q, T, 0, 2, false, false, 0><<<grid, block, 0, st>>>(p);
-    else if (walls) k_collide<Q, T, 0, true, false, false, 0><<<grid, block, 0, st>>>(p);
-    else k_collide<Q, T, 0, false, false, false, 0><<<grid, block, 0, st>>>(p);
-  } else if (pat == 1) {
-    k_collide<Q, T, 1, false, false, false, 0><<<grid, block, 0, st>>>(p);
-  } else {
-    if (walls) k_collide<Q, T, 2, true, false, false, 0><<<grid, block, 0, st>>>(p);
-    else k_collide<Q, T, 2, false, false, false, 0><<<grid, block, 0, st>>>(p);
-  }
-  return cudaGetLastError();
+  if (pat == 1) return launch_k<Q, T, 1, 0, false, false, COLL>(p, grid, block, st);
+  if (walls) return launch_k<Q, T, 2, 1, false, false, COLL>(p, grid, block, st);
+  return launch_k<Q, T, 2, 0, false, false, COLL>(p, grid, block, st);
+}
+
+template <int Q, typename T>
+cudaError_t launch_variant(const CollideParams& p, int pat, bool force, bool dbg, dim3 grid,
+                           dim3 block, cudaStream_t st) {
+  if (p.trt == 1) return launch_coll<Q, T, 1>(p, pat, force, dbg, grid, block, st);
+  if (p.trt == 2) return launch_coll<Q, T, 2>(p, pat, force, dbg, grid, block, st);
+  return launch_coll<Q, T, 0>(p, pat, force, dbg, grid, block, st);
 }
 
 // one translation unit per (Q, T) instantiates the kernel variants (parallel build)
