@@ -5,6 +5,15 @@
 
 namespace psm {
 
+// Persistent remap blocks when the remap overlaps the collide (remap-ahead): one per SM, two at
+// s >= 2 where the 64-register chunked sample kernel fits twice into the registers one collide
+// block frees (measured: c3 scenario A at s = 2, 9963 -> 10183 MLUPS; one per SM is better for
+// the s = 1 band of c5w).  PSM_AHEAD_BLOCKS overrides.
+static int ahead_blocks(const psm_ctx* c, int s) {
+  if (c->ahead_blocks_env > 0) return c->ahead_blocks_env;
+  return s >= 2 ? 2 * 148 : 148;
+}
+
 psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
   MapParams mp;
   std::memset(&mp, 0, sizeof(mp));
@@ -151,7 +160,7 @@ psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
         r.bandn = bd.cn[sl];
         r.band_cap = (int)std::min<size_t>(bd.ccap[sl], (size_t)INT32_MAX);
       }
-      CUDA_TRY(c, launch_remap_single(r, c->mst == c->st ? 148 * 8 : c->ahead_blocks, c->mst,
+      CUDA_TRY(c, launch_remap_single(r, c->mst == c->st ? 148 * 8 : ahead_blocks(c, r.body.s), c->mst,
                                       c->mst == c->st ? 256 : c->ahead_threads));
       c->launches += 4;
       continue;
@@ -331,7 +340,7 @@ psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
     r.bandn = b.cn[sl];
     r.band_cap = (int)std::min<size_t>(b.ccap[sl], (size_t)INT32_MAX);
     r.margin = 1;
-    CUDA_TRY(c, launch_remap_band(r, c->mst == c->st ? 148 * 8 : c->ahead_blocks, c->mst,
+    CUDA_TRY(c, launch_remap_band(r, c->mst == c->st ? 148 * 8 : ahead_blocks(c, b.s), c->mst,
                                   c->mst == c->st ? 256 : c->ahead_threads));
     c->launches += (b.s >= 2 && b.mapping == 0) ? 2 : 1;
   }

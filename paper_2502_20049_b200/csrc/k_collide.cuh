@@ -546,6 +546,9 @@ __device__ __forceinline__ T aa_load(const T* p) {
 template <int Q, typename T, int PAT, int COLL, int WALLS>
 constexpr int collide_min_blocks() {
   // fp64: two blocks (the populations alone are 2*Q registers)
+#if defined(PSM_F64_Q19_BLOCKS)
+  if (sizeof(T) == 8 && Q == 19) return PSM_F64_Q19_BLOCKS;
+#endif
   if (sizeof(T) == 8) return 2;
   // D3Q27 AA odd step, periodic (destinations recomputed after the collision): three fp32
   // blocks at 80 registers (measured 88.2 -> 96.9 % SRT, 82.1 -> 90.6 % cumulant vs two)

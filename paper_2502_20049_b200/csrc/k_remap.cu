@@ -188,7 +188,12 @@ __device__ __forceinline__ void band_cell(const RemapParams& r, uint32_t e, int&
 
 // L3: one thread per narrow-band cell: all its sub-samples with the exact fp64 test (A14),
 // geometry-bit loads issued 8 at a time, and the word written directly.
-__global__ void k_remap_l3(const __grid_constant__ RemapParams r) {
+// the exact sample kernels at four blocks per SM (64 registers, one sample load in flight per
+// thread, more threads): measured faster than the 118-register batched-load form
+#ifndef PSM_REMAP_MINB
+#define PSM_REMAP_MINB 4
+#endif
+__global__ void __launch_bounds__(256, PSM_REMAP_MINB) k_remap_l3(const __grid_constant__ RemapParams r) {
   const Geom& G = r.g;
   const BodyGeo& b = r.body;
   const int n = min(*r.bandn, r.band_cap);
@@ -210,23 +215,16 @@ __global__ void k_remap_l3(const __grid_constant__ RemapParams r) {
         for (int j = 0; j < m; ++j) cnt += sample_inside(b, x, y, zg, s0 + j, L, G.wall);
         continue;
       }
-      long long wi[8];
-      int bit[8];
       if (m == 8) {
-        mesh_word_index8(b, x, y, zg, s0, L, G.wall, wi, bit);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          wi[j] = -1;
-          bit[j] = 0;
-          if (j < m) mesh_word_index(b, x, y, zg, s0 + j, L, G.wall, wi[j], bit[j]);
+        cnt += mesh_count8(b, x, y, zg, s0, L, G.wall);
+      } else {  // s = 0: the single sample
+        for (int j = 0; j < m; ++j) {
+          long long wi;
+          int bit;
+          mesh_word_index(b, x, y, zg, s0 + j, L, G.wall, wi, bit);
+          if (wi >= 0) cnt += (int)((__ldg(b.bits + wi) >> bit) & 1ull);
         }
       }
-      unsigned long long w[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) w[j] = (wi[j] >= 0) ? __ldg(b.bits + wi[j]) : 0ull;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) cnt += (int)((w[j] >> bit[j]) & 1ull);
     }
     put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
   }
@@ -235,7 +233,7 @@ __global__ void k_remap_l3(const __grid_constant__ RemapParams r) {
 // L3 for s >= 2 (64 or 512 sub-samples per cell): one thread per (band cell, 8-sample chunk),
 // batched geometry-bit loads, integer atomics into the cell's count (order-independent); L4
 // writes the words.
-__global__ void k_remap_l3_chunks(const __grid_constant__ RemapParams r) {
+__global__ void __launch_bounds__(256, PSM_REMAP_MINB) k_remap_l3_chunks(const __grid_constant__ RemapParams r) {
   const Geom& G = r.g;
   const BodyGeo& b = r.body;
   const int n = min(*r.bandn, r.band_cap);
@@ -252,14 +250,7 @@ __global__ void k_remap_l3_chunks(const __grid_constant__ RemapParams r) {
     if (b.kind == 0) {
       for (int j = 0; j < 8; ++j) cnt += sample_inside(b, x, y, zg, ch * 8 + j, L, G.wall);
     } else {
-      long long wi[8];
-      int bit[8];
-      mesh_word_index8(b, x, y, zg, ch * 8, L, G.wall, wi, bit);
-      unsigned long long w[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) w[j] = (wi[j] >= 0) ? __ldg(b.bits + wi[j]) : 0ull;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) cnt += (int)((w[j] >> bit[j]) & 1ull);
+      cnt = mesh_count8(b, x, y, zg, ch * 8, L, G.wall);
     }
     if (cnt) atomicAdd(r.bandcnt + k, cnt);
   }

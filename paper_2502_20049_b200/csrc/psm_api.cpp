@@ -116,7 +116,7 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   c->nzl = (grid->nz * (c->rank + 1)) / world - c->z0;
   c->st = static_cast<cudaStream_t>(opt->cuda_stream);
   c->mst = c->st;
-  if (const char* e = std::getenv("PSM_AHEAD_BLOCKS")) c->ahead_blocks = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PSM_AHEAD_BLOCKS")) c->ahead_blocks_env = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PSM_P2P_TIMEOUT_S"))
     c->p2p_timeout_ns = (unsigned long long)(std::max(1.0, std::atof(e)) * 1e9);
   if (const char* e = std::getenv("PSM_BAND_CACHE")) c->no_cache = std::strcmp(e, "0") == 0;

@@ -114,7 +114,7 @@ struct psm_ctx {
   cudaStream_t mst = nullptr;        // stream the remap launches go to (st, or map_st ahead)
   cudaStream_t map_st = nullptr;     // remap-ahead stream (high priority)
   cudaEvent_t ev_map = nullptr, ev_coll = nullptr;
-  int ahead_blocks = 148;            // persistent remap blocks when overlapped with the collide
+  int ahead_blocks_env = 0;          // PSM_AHEAD_BLOCKS (persistent remap blocks when overlapped)
   int ahead_threads = 256;
   double* partial = nullptr;
   double* overflow = nullptr;

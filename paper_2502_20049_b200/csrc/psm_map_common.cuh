@@ -240,14 +240,19 @@ __device__ __forceinline__ int exact_count(const BodyGeo& b, int x, int y, int z
   return cnt;
 }
 
-// Word index / bit of 8 consecutive sub-samples (si0 .. si0+7, same cell, si0 % 8 == 0) of a mesh
+// Inside count of 8 consecutive sub-samples (si0 .. si0+7, same cell, si0 % 8 == 0) of a mesh
 // body.  Sample si0 is transformed with the exact A14 arithmetic; the others by adding the
 // rotated sub-sample offsets (error ~1e-13 cells).  A sample whose scaled coordinate lies within
-// 1e-9 of a geometry-cell face is recomputed exactly, so every floor() equals the exact one and the
-// result is bit-identical to mesh_word_index() per sample.
-__device__ __forceinline__ void mesh_word_index8(const BodyGeo& b, int x, int y, int zg, int si0,
-                                                 const double L[3], const int wall[3],
-                                                 long long wi[8], int bit[8]) {
+// 1e-9 of a geometry-cell face is recomputed exactly, so every floor() equals the exact one and
+// the count is bit-identical to mesh_word_index() per sample.  Each sample's geometry word is
+// loaded as soon as its index is known, U samples in flight: few live registers, so more warps
+// hide the load latency (measured faster than eight batched 64-bit indices).
+#ifndef PSM_REMAP_U
+#define PSM_REMAP_U 1
+#endif
+constexpr int kRemapU = PSM_REMAP_U;
+__device__ __forceinline__ int mesh_count8(const BodyGeo& b, int x, int y, int zg, int si0,
+                                           const double L[3], const int wall[3]) {
   const int n = 1 << b.s, msk = n - 1;
   const double h = ldexp(1.0, -b.s), hs = ldexp(1.0, b.s);
   const int gx0 = si0 & msk, gy0 = (si0 >> b.s) & msk, gz0 = si0 >> (2 * b.s);
@@ -255,7 +260,8 @@ __device__ __forceinline__ void mesh_word_index8(const BodyGeo& b, int x, int y,
                         (double)zg + (gz0 + 0.5) * h};
   double q0[3];
   body_frame(b, p0, L, wall, q0);
-#pragma unroll
+  int cnt = 0;
+#pragma unroll kRemapU
   for (int j = 0; j < 8; ++j) {
     const int si = si0 + j;
     const int gx = si & msk, gy = (si >> b.s) & msk, gz = si >> (2 * b.s);
@@ -269,33 +275,32 @@ __device__ __forceinline__ void mesh_word_index8(const BodyGeo& b, int x, int y,
       const double fr = f[a] - floor(f[a]);
       if (fr < 1e-9 || fr > 1.0 - 1e-9) safe = false;
     }
+    long long wi;
+    int bit;
     if (!safe) {
-      long long w;
-      int bp;
-      mesh_word_index(b, x, y, zg, si, L, wall, w, bp);
-      wi[j] = w;
-      bit[j] = bp;
-      continue;
-    }
-    int g[3];
-    bool in = true;
+      mesh_word_index(b, x, y, zg, si, L, wall, wi, bit);
+    } else {
+      int g[3];
+      bool in = true;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double xx = floor(f[a]);
-      if (!(xx >= 0.0) || xx >= (double)(b.dims_b[a] << b.s)) in = false;
-      g[a] = (int)xx;
+      for (int a = 0; a < 3; ++a) {
+        const double xx = floor(f[a]);
+        if (!(xx >= 0.0) || xx >= (double)(b.dims_b[a] << b.s)) in = false;
+        g[a] = (int)xx;
+      }
+      wi = -1;
+      bit = 0;
+      if (in) {
+        const long long brick = ((long long)(g[2] >> b.s) * b.dims_b[1] + (g[1] >> b.s)) *
+                                    b.dims_b[0] + (g[0] >> b.s);
+        const int bb = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
+        wi = brick * b.words + (bb >> 6);
+        bit = bb & 63;
+      }
     }
-    if (!in) {
-      wi[j] = -1;
-      bit[j] = 0;
-      continue;
-    }
-    const long long brick =
-        ((long long)(g[2] >> b.s) * b.dims_b[1] + (g[1] >> b.s)) * b.dims_b[0] + (g[0] >> b.s);
-    const int bb = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
-    wi[j] = brick * b.words + (bb >> 6);
-    bit[j] = bb & 63;
+    if (wi >= 0) cnt += (int)((__ldg(b.bits + wi) >> bit) & 1ull);
   }
+  return cnt;
 }
 
 }  // namespace psm
