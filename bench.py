@@ -371,8 +371,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5w64", choices=sorted(WORKLOADS))
     ap.add_argument("--extra", default=None,
-                    help="second workload measured in the same run and reported under its own "
-                         "key (default: c5w, the fp32 line, when --config is c5w64)")
+                    help="comma list of further workloads measured in the same run, each under "
+                         "its own key (default with c5w64: c5w -> 'f32', c5wpap -> "
+                         "'paper_config'); 'none' for none")
     ap.add_argument("--reps", type=int, default=5,
                     help="timed repetitions of exactly K steps; value = their median")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -407,13 +408,19 @@ def main():
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy().tobytes())
 
-    extra = args.extra if args.extra is not None else ("c5w" if args.config == "c5w64" else "")
-    extra = "" if extra == "none" else extra
+    # further workloads measured in the same run, each under its own key: by default the fp32
+    # twin of the fp64 line ("f32") and the paper's own performance configuration ("paper_config":
+    # D3Q19 cumulant AA fp64) on the same rotor-pair geometry
+    if args.extra is not None:
+        extras = [e for e in args.extra.split(",") if e and e != "none"]
+    else:
+        extras = ["c5w", "c5wpap"] if args.config == "c5w64" else []
+    extras = [e for e in extras if e != args.config]
     stream_gbs = stream_copy_gbs(torch) if rank == 0 else None
     res = measure(psm, torch, dist, wl, args, rank, world, local, nccl_id, e2e=not args.no_e2e,
                   config_name=args.config)
-    extra_res = None
-    if extra and extra != args.config:
+    extra_res = []
+    for extra in extras:
         nccl_id2 = None
         if world > 1:
             idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
@@ -422,8 +429,8 @@ def main():
                                            dtype=torch.uint8))
             dist.broadcast(idt, 0)
             nccl_id2 = bytes(idt.cpu().numpy().tobytes())
-        extra_res = measure(psm, torch, dist, dict(WORKLOADS[extra]), args, rank, world, local,
-                            nccl_id2, e2e=False, config_name=extra)
+        extra_res.append(measure(psm, torch, dist, dict(WORKLOADS[extra]), args, rank, world,
+                                 local, nccl_id2, e2e=False, config_name=extra))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -452,14 +459,16 @@ def main():
             "e2e": res["e2e"],
             "cpu_baseline": cpu,
         }
-        if extra_res is not None:
-            line[extra_res["prec"] if extra_res["prec"] != wl["prec"] else extra] = {
-                "config": extra, "workload": extra_res["config"]["workload"],
-                "value": extra_res["mlups"], "unit": UNIT, "ms_per_step": extra_res["ms_per_step"],
-                "reps": extra_res["reps"], "roofline_frac_step": extra_res["step_frac"],
-                "roofline": roofline_block(extra_res, stream_gbs),
-                "phases_ms": extra_res["phases_ms"], "gpu_launches": extra_res["launches"],
-                "clocks": extra_res["clocks"]}
+        for er in extra_res:
+            key = {"c5w": "f32", "c5wpap": "paper_config"}.get(er["name"], er["name"])
+            line[key] = {
+                "config": er["name"], "workload": er["config"]["workload"],
+                "dtype": er["prec"], "pattern": er["config"]["pattern"],
+                "value": er["mlups"], "unit": UNIT, "ms_per_step": er["ms_per_step"],
+                "reps": er["reps"], "roofline_frac_step": er["step_frac"],
+                "roofline": roofline_block(er, stream_gbs),
+                "phases_ms": er["phases_ms"], "gpu_launches": er["launches"],
+                "clocks": er["clocks"]}
         emit(line)
     if dist is not None:
         dist.barrier()
