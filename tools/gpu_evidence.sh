@@ -1,5 +1,6 @@
-# round-2 final evidence batch (1 GPU): tests, smoke, default bench, sweep, c3 table, NEXT-row
-# bench lines, Table I, ncu of the default collide, the paper configuration and c5wcum
+# Round evidence batch on one B200 (gpurun --timeout 5000 -- 'bash tools/gpu_evidence.sh'):
+# GPU tests, smoke, the default bench line (c5w64 + f32 + paper_config), the fluid-only
+# collide sweep, the c3 node-level table, every NEXT-row workload, ncu of three collides
 set -x
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/gputests.log 2>&1; echo rc=$? >> gpurun_out/gputests.log
