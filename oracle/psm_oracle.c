@@ -18,11 +18,12 @@
  *           the literal centre-only reading R2 selectable per mesh)
  * and the NEXT rows built on the same hot path:
  *   TRT fluid operator (listed; reading A27)
- *   cumulant fluid operator (readings A29, A31 with a body force)
+ *   cumulant fluid operator, D3Q27 and D3Q19 (readings A29, A32, A31 with a
+ *           body force)
  *   velocity inflow / pressure outflow on the x faces (reading A30)
  *   two-way coupling of dynamic bodies (reading A28, optional virtual mass)
  * The readings taken where the paper is silent or garbled are listed in DESIGN.md §3
- * (A1..A31); each use below names its reading.
+ * (A1..A34); each use below names its reading.
  *
  * State convention (A10): f holds the Eq.(4) state, i.e. the PRE-collision populations
  * f_i(x,t).  One step = collide every cell, then push f*_i(x) to x + c_i.
