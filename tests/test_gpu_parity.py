@@ -361,6 +361,57 @@ def test_two_way_coupled_bodies(world_bc):
     assert not np.allclose(g.body_state(1)[2], (0.0, 0.0, 0.01))  # it really was coupled
 
 
+def test_dynamic_body_back_to_prescribed_motion_with_remap_ahead():
+    """psm_set_dynamics(id, NULL) after coupled steps: the body continues in closed form from its
+    integrated state, the remap-ahead spare buffer (which followed the dynamic pose) is rebuilt,
+    and a pipelined psm_step(n) equals the oracle fed the closed-form poses from that state
+    (fractions bit-exact, PDFs <= 1e-12, F/T of the last step)."""
+    n = (40, 36, 32)
+    v, tr = pi.propeller_mesh(n_blades=3, scale=0.07, n_st=8, n_pts=16, hub_seg=16)
+    I_mesh = np.array([[900.0, 20.0, 0.0], [20.0, 700.0, 5.0], [0.0, 5.0, 800.0]])
+    Q0 = pi.rotation_about([1, 0, 1], 0.3)
+    t0 = (20.0, 18.0, 16.0)
+    o = oracle.Oracle(*n, 19, 0.7, (0, 0, 0), 1, 1)
+    g = _sim(nx=n[0], ny=n[1], nz=n[2], Q=19, tau=0.7, sc=1, bmode=1)
+    rho, u = pi.perturbed_flow(n[::-1], 31, u0=(0.02, 0.0, 0.0))
+    o.init_equilibrium(rho, u)
+    g.init_equilibrium(rho, u)
+    v0, w0 = (0.01, 0.0, 0.0), (0.0, 0.02, 0.0)
+    o.set_mesh(2, v, tr, 1)
+    g.set_mesh(2, v, tr, 1, Q0, t0, v0, w0)
+    # prescribed phase in one pipelined call: the spare word buffer is in use
+    g.step(5)
+    for k in range(5):
+        Qk, tk = oracle.pose_advance(Q0, t0, v0, w0, k, list(n), [1, 1, 1])
+        o.set_pose(2, Qk, tk, v0, w0)
+        o.map()
+        o.step(1)
+    Q5, t5 = oracle.pose_advance(Q0, t0, v0, w0, 5, list(n), [1, 1, 1])
+    o.set_pose(2, Q5, t5, v0, w0)
+    o.set_dynamics(2, 3000.0, I_mesh, (0.5, 0.0, 0.0), (0.0, 0.0, 0.3))
+    g.set_dynamics(2, 3000.0, I_mesh, (0.5, 0.0, 0.0), (0.0, 0.0, 0.3))
+    for _ in range(4):
+        o.map()
+        o.step(1)
+        o.integrate()
+        g.step(1)
+    g.set_dynamics(2, None)  # back to prescribed motion from the integrated state
+    Qs, ts, vs, ws = g.body_state(2)
+    so = o.body_state(2)
+    for a, c in zip(so, (Qs, ts, vs, ws)):
+        assert np.allclose(a, c, rtol=1e-11, atol=1e-14)
+    g.step(9)  # remap-ahead pipeline over the prescribed phase
+    for k in range(9):
+        Qk, tk = oracle.pose_advance(Qs, ts, vs, ws, k, list(n), [1, 1, 1])
+        o.set_pose(2, Qk, tk, vs, ws)
+        o.map()
+        o.step(1)
+    assert np.array_equal(o.fractions()[2], g.fractions()[2])
+    assert np.max(np.abs(o.pdfs() - g.pdfs())) <= F64_TOL
+    ok, info = _ft_close(g.force_torque(2), o.force_torque(2), 1e-9)
+    assert ok, info
+
+
 def test_neighbouring_bodies_sharing_tiles_keep_their_fractions():
     """Regression: two bodies whose cell boxes are disjoint but share 32x4x2 tiles; remapping
     one (single-body fast path) must not clear the other's words."""
