@@ -275,7 +275,7 @@ psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
     b.ms.cache = false;
     // the cached band pays off while the exact pass is cheap (8 sub-samples per cell); at
     // s >= 2 the radius-2 band's 64/512 samples per cell cost more than the L0-L2 pipeline
-    b.want_cache = !no_cache && !c->dbg && b.s <= 1;
+    b.want_cache = !no_cache && !c->dbg && b.s <= c->cache_max_s;
     remap_region(c, b, Q, t, boxes);
   }
   // an incremental body whose (build) box meets a box remapped now goes the full way
@@ -285,7 +285,7 @@ psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
       Body& b = c->bodies[incr[k]];
       if (!boxes_overlap(c, b, boxes)) continue;
       b.ms.cache = false;
-      b.want_cache = b.s <= 1;
+      b.want_cache = b.s <= c->cache_max_s;
       remap_region(c, b, b.ms.Qc, b.ms.tc, boxes);
       incr.erase(incr.begin() + (long)k);
       changed = true;

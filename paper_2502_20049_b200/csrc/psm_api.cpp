@@ -121,6 +121,7 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
     c->p2p_timeout_ns = (unsigned long long)(std::max(1.0, std::atof(e)) * 1e9);
   if (const char* e = std::getenv("PSM_BAND_CACHE")) c->no_cache = std::strcmp(e, "0") == 0;
   c->force_general = std::getenv("PSM_REMAP_GENERAL") != nullptr;
+  if (const char* e = std::getenv("PSM_CACHE_MAX_S")) c->cache_max_s = std::atoi(e);
   if (const char* e = std::getenv("PSM_SEG_CAP")) c->seg_cap_env = std::max(1ll, std::atoll(e));
   if (const char* e = std::getenv("PSM_BAND_CAP")) c->band_cap_env = std::max(1ll, std::atoll(e));
   if (const char* e = std::getenv("PSM_AHEAD_THREADS"))

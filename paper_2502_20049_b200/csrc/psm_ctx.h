@@ -136,6 +136,7 @@ struct psm_ctx {
   // PSM_BAND_CACHE=0, PSM_REMAP_GENERAL, PSM_SEG_CAP / PSM_BAND_CAP (cap the segment / band lists
   // of the full pipeline so that the in-kernel overflow paths run)
   bool no_cache = false, force_general = false;
+  int cache_max_s = 1;  // cached narrow band up to this s (PSM_CACHE_MAX_S)
   int64_t seg_cap_env = 0, band_cap_env = 0;
   double* pinned = nullptr;  // host staging (ft + err)
   // test-only dense fields
