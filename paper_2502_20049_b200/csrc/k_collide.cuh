@@ -592,8 +592,13 @@ __device__ __forceinline__ void stencil_offsets(const Geom& G, int xc, int yc, i
 
 // WALLS: 0 fully periodic; 1 runtime wall flags on every axis; 2 only x is non-periodic (open
 // x faces or x walls) with y, z periodic — the y/z flag logic compiles out
-template <int Q, typename T, int PAT, int WALLS, bool FORCE, bool DBG, int COLL>
-__global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COLL, WALLS>()))
+// OCC = 1: one block per SM more for the fp64 D3Q19 kernels (85 registers, a few spills):
+// measured +4 % when PSM tiles are frequent (c3 scenario A), -1.5 % fluid-only, so the host picks
+// it from the PSM-tile fraction of the previous psm_step call
+template <int Q, typename T, int PAT, int WALLS, bool FORCE, bool DBG, int COLL, int OCC = 0>
+__global__ void __launch_bounds__(kTileCells,
+                                  (collide_min_blocks<Q, T, PAT, COLL, WALLS>() +
+                                   ((OCC && sizeof(T) == 8 && Q == 19) ? 1 : 0)))
     k_collide(const __grid_constant__ CollideParams p) {
   const Geom& G = p.g;
   const int x = blockIdx.x * kTileX + threadIdx.x;
@@ -675,7 +680,9 @@ __global__ void __launch_bounds__(kTileCells, (collide_min_blocks<Q, T, PAT, COL
   // of the kernel, while the gathered loads are still in flight)
   __shared__ TileRed s_tred;
   if (solid_tile) {
-    if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) s_tred.cnt = 0u;
+    if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) {
+      s_tred.cnt = 0u;
+    }
     __syncthreads();
   }
 
@@ -1008,7 +1015,7 @@ cudaError_t launch_t(const CollideParams& p, int pat, bool force, bool dbg, int 
 
 // One kernel instantiation: dynamic shared memory for the PSM-cell stash (when the variant uses
 // it), with the > 48 KB opt-in set once per instantiation and device (bit per device ordinal).
-template <int Q, typename T, int PAT, int WALLS, bool FORCE, bool DBG, int COLL>
+template <int Q, typename T, int PAT, int WALLS, bool FORCE, bool DBG, int COLL, int OCC = 0>
 cudaError_t launch_k(const CollideParams& p, dim3 grid, dim3 block, cudaStream_t st) {
 #if defined(PSM_STASH_ALL)
   constexpr bool stash = true;
@@ -1023,13 +1030,13 @@ cudaError_t launch_k(const CollideParams& p, dim3 grid, dim3 block, cudaStream_t
     if (e != cudaSuccess) return e;
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(attr_devices & bit)) {
-      e = cudaFuncSetAttribute(k_collide<Q, T, PAT, WALLS, FORCE, DBG, COLL>,
+      e = cudaFuncSetAttribute(k_collide<Q, T, PAT, WALLS, FORCE, DBG, COLL, OCC>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) return e;
       attr_devices |= bit;
     }
   }
-  k_collide<Q, T, PAT, WALLS, FORCE, DBG, COLL><<<grid, block, sm, st>>>(p);
+  k_collide<Q, T, PAT, WALLS, FORCE, DBG, COLL, OCC><<<grid, block, sm, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -1043,6 +1050,13 @@ cudaError_t launch_coll(const CollideParams& p, int pat, bool force, bool dbg, d
   if (dbg && force) return launch_k<Q, T, 0, 1, true, true, COLL>(p, grid, block, st);
   if (dbg) return launch_k<Q, T, 0, 1, false, true, COLL>(p, grid, block, st);
   if (force) return launch_k<Q, T, 0, 1, true, false, COLL>(p, grid, block, st);
+  if constexpr (Q == 19 && sizeof(T) == 8) {  // periodic fast paths at higher occupancy
+    if (p.hiocc && !walls) {
+      if (pat == 0) return launch_k<Q, T, 0, 0, false, false, COLL, 1>(p, grid, block, st);
+      if (pat == 1) return launch_k<Q, T, 1, 0, false, false, COLL, 1>(p, grid, block, st);
+      return launch_k<Q, T, 2, 0, false, false, COLL, 1>(p, grid, block, st);
+    }
+  }
   if (pat == 0) {
     if (!walls) return launch_k<Q, T, 0, 0, false, false, COLL>(p, grid, block, st);
     if (xonly) return launch_k<Q, T, 0, 2, false, false, COLL>(p, grid, block, st);

@@ -122,6 +122,7 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   if (const char* e = std::getenv("PSM_BAND_CACHE")) c->no_cache = std::strcmp(e, "0") == 0;
   c->force_general = std::getenv("PSM_REMAP_GENERAL") != nullptr;
   if (const char* e = std::getenv("PSM_CACHE_MAX_S")) c->cache_max_s = std::atoi(e);
+  if (const char* e = std::getenv("PSM_HIOCC")) c->hiocc_env = std::atoi(e) != 0 ? 1 : 0;
   if (const char* e = std::getenv("PSM_SEG_CAP")) c->seg_cap_env = std::max(1ll, std::atoll(e));
   if (const char* e = std::getenv("PSM_BAND_CAP")) c->band_cap_env = std::max(1ll, std::atoll(e));
   if (const char* e = std::getenv("PSM_AHEAD_THREADS"))
@@ -594,6 +595,9 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
   p.partial = c->partial;
   p.overflow = c->overflow;
   p.err = c->err;
+  // fp64 D3Q19: the higher-occupancy collide when PSM tiles were frequent at the end of the
+  // previous call (more than 8 % of the tiles; PSM_HIOCC=0/1 forces it)
+  p.hiocc = c->hiocc_env >= 0 ? c->hiocc_env : (c->psm_tile_frac > 0.08 ? 1 : 0);
   p.dbg_B = c->dbg_B;
   p.dbg_us = c->dbg_us;
   p.dbg_id = c->dbg_id;
@@ -774,10 +778,18 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
     c->launches += 1;
   }
   CUDA_TRY(c, cudaMemcpyAsync(herr, c->err, 8, cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(c, launch_count_tiles(c->tile_flag, c->ntiles, c->flags + 5, c->st));
+  c->launches += 1;
+  CUDA_TRY(c, cudaMemcpyAsync(herr + 2, c->flags + 5, 8, cudaMemcpyDeviceToHost, c->st));
   if (c->p2p) CUDA_TRY(c, cudaMemcpyAsync(herr + 1, c->flags + 2, 8, cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
   (void)nb;
   ft_store(c, ids);
+  c->psm_tile_frac = (double)herr[2] / (double)c->ntiles;
+  static const bool stats_on = std::getenv("PSM_MAP_STATS") != nullptr;
+  if (stats_on)
+    std::fprintf(stderr, "[psm step] %lld steps, PSM tiles %.4f of the tiles, hiocc %d\n",
+                 (long long)n, c->psm_tile_frac, p.hiocc);
   if (c->p2p && herr[1] != 0)
     FAIL(c, PSM_E_NCCL, "fused halo: a neighbour did not signal its step in time (PSM_P2P_TIMEOUT_S)");
   if (*herr != ~0ull) {

@@ -137,6 +137,8 @@ struct psm_ctx {
   // of the full pipeline so that the in-kernel overflow paths run)
   bool no_cache = false, force_general = false;
   int cache_max_s = 1;  // cached narrow band up to this s (PSM_CACHE_MAX_S)
+  int hiocc_env = -1;   // PSM_HIOCC: force (1) / forbid (0) the higher-occupancy fp64 collide
+  double psm_tile_frac = 0.0;  // PSM tiles / tiles in the last psm_step call
   int64_t seg_cap_env = 0, band_cap_env = 0;
   double* pinned = nullptr;  // host staging (ft + err)
   // test-only dense fields

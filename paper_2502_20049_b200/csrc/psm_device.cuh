@@ -102,6 +102,7 @@ struct CollideParams {
   double* partial;        // [tile][2 slots][1 + kSlotVals] (slot id stored as double)
   double* overflow;       // [kMaxBodies+1][kSlotVals] atomics for a 3rd+ body in a tile
   unsigned long long* err;  // first (step, cell) with rho <= 0 or non-finite
+  int hiocc;              // host: launch the higher-occupancy instantiation (fp64 D3Q19)
   const double* dbg_B;    // DBG: B [cell]
   const double* dbg_us;   // DBG: u_s [3][cell]
   const uint8_t* dbg_id;  // DBG: id [cell]

@@ -13,6 +13,10 @@ namespace psm {
 cudaError_t launch_collide(int Q, bool fp64, const CollideParams& p, int pat, bool force,
                            bool dbg, int ntz, cudaStream_t st);
 
+// flagged tiles of a tile-flag buffer -> *out (k_collide.cu)
+cudaError_t launch_count_tiles(const uint8_t* flag, long long n, unsigned long long* out,
+                               cudaStream_t st);
+
 // fused-halo handshake (k_collide.cu)
 cudaError_t launch_p2p_signal(unsigned long long* up_flag, unsigned long long* dn_flag,
                               unsigned long long v, cudaStream_t st);
