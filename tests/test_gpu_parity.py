@@ -723,3 +723,45 @@ def test_paper_configuration_d3q19_cumulant_aa_rotating_100_steps(sc):
     assert d <= F64_TOL, d
     ok, info = _ft_close(g.force_torque(1), o.force_torque(1))
     assert ok, info
+
+
+@pytest.mark.parametrize("pattern,collision", [("two_array", "srt"), ("aa", "cumulant")])
+def test_fp64_occupancy_variants_bitwise_identical(pattern, collision):
+    """The fp64 D3Q19 collide exists at two occupancies (chosen at run time from the PSM-tile
+    fraction): both give the same bits, and equal the oracle."""
+    import os
+    n = (40, 36, 32)
+    v, tr = pi.propeller_mesh(n_blades=4, scale=0.1, n_st=8, n_pts=16, hub_seg=16)
+    rho, u = pi.perturbed_flow(n[::-1], 61, u0=(0.02, 0.0, 0.01))
+    w = (0.03, 0.0, 0.0)
+    runs = []
+    for h in ("0", "1"):
+        old = os.environ.get("PSM_HIOCC")
+        os.environ["PSM_HIOCC"] = h
+        try:
+            g = _sim(nx=n[0], ny=n[1], nz=n[2], Q=19, tau=0.6, prec="f64", pattern=pattern,
+                     collision=collision)
+        finally:
+            if old is None:
+                os.environ.pop("PSM_HIOCC", None)
+            else:
+                os.environ["PSM_HIOCC"] = old
+        g.init_equilibrium(rho, u)
+        g.set_mesh(1, v, tr, 1, np.eye(3), (20.0, 18.0, 16.0), (0, 0, 0), w)
+        for k in (1, 6, 9):
+            g.step(k)
+        runs.append((g.pdfs(), g.force_torque(1)[0]))
+        g.close()
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert np.array_equal(runs[0][1], runs[1][1])
+    o = oracle.Oracle(*n, 19, 0.6, (0, 0, 0), 1, 1)
+    o.set_collision(collision)
+    o.init_equilibrium(rho, u)
+    o.set_mesh(1, v, tr, 1)
+    for k in range(16):
+        Qk, tk = oracle.pose_advance(np.eye(3), (20.0, 18.0, 16.0), (0, 0, 0), w, k, list(n),
+                                     [1, 1, 1])
+        o.set_pose(1, Qk, tk, (0, 0, 0), w)
+        o.map()
+        o.step(1)
+    assert np.max(np.abs(o.pdfs() - runs[0][0])) <= F64_TOL
