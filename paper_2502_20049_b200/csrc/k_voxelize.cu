@@ -11,7 +11,8 @@
 //                bounding box; a covered row gets one toggle bit at the first sample index the
 //                crossing does not cover (atomicXor into a bit array, (NX+1) bits per row)
 //   k_vox_rows   one thread per row: suffix XOR of the toggles gives inside/outside per sample;
-//                each run of 2^s samples of one brick is OR-ed into the brick's bit words
+//                each run of 2^s samples of one brick is OR-ed into its bits of the linearly
+//                packed field
 //   k_vox_any    per brick: any sample inside / any sample outside
 //   k_box_pass   separable running-window OR (radius r along one axis, beyond the field = 0)
 //   k_vox_mask   the eight early-out bits
@@ -115,7 +116,8 @@ __global__ void k_vox_rows(const VoxParams p) {
       if (!bits) continue;
       const long long bxi = (gx0 + c) >> s;
       const long long b = (bzi * p.by + byi) * p.bx + bxi;
-      atomicOr(p.words + b * p.W + (off >> 6), (unsigned long long)bits << (off & 63));
+      const long long gb = (b << (3 * s)) + off;  // linear bit index (psm_device.cuh)
+      atomicOr(p.words + (gb >> 6), (unsigned long long)bits << (gb & 63));
     }
   }
 }
@@ -125,8 +127,13 @@ __global__ void k_vox_any(const VoxParams p, uint8_t* any_in, uint8_t* any_out) 
   const long long nb = p.bx * p.by * p.bz;
   if (b >= nb) return;
   const int nbits = 1 << (3 * p.s);
+  const long long gb0 = b << (3 * p.s);
   int ones = 0;
-  for (int k = 0; k < p.W; ++k) ones += __popcll(p.words[b * p.W + k]);
+  if (nbits >= 64) {
+    for (int k = 0; k < nbits / 64; ++k) ones += __popcll(p.words[(gb0 >> 6) + k]);
+  } else {
+    ones = __popcll((p.words[gb0 >> 6] >> (gb0 & 63)) & ((1ull << nbits) - 1ull));
+  }
   any_in[b] = ones > 0;
   any_out[b] = ones < nbits;
 }
@@ -199,7 +206,7 @@ cudaError_t launch_voxelize(VoxParams p, void* scratch, uint8_t* mask, cudaStrea
           *outS = f + 5 * nb, *in2 = f + 6 * nb, *out2 = f + 7 * nb, *tmp = f + 8 * nb;
   cudaError_t e = cudaMemsetAsync(p.tog, 0, (size_t)(p.NY * p.NZ * p.wpr) * 4, st);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(p.words, 0, nb * (size_t)p.W * 8, st);
+  e = cudaMemsetAsync(p.words, 0, (size_t)p.W * 8, st);
   if (e != cudaSuccess) return e;
   const int T = 256;
   if (p.nt > 0)

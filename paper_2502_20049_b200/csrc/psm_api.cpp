@@ -309,10 +309,11 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
       nb.rbound = rb;
       // geometry field (reading A15/A17): GPU voxeliser by default (k_voxelize.cu); the host
       // implementation with PSM_VOXELIZE=host; PSM_VOXELIZE_CHECK=1 runs both and compares
-      const int sl = shape->s, n = 1 << sl;
+      const int sl = shape->s;
       const size_t nbk = (size_t)(nb.dims[0] * nb.dims[1] * nb.dims[2]);
-      nb.words = std::max(1, (n * n * n) / 64);
-      CUDA_TRY(c, cudaMalloc(&nb.d_bits, nbk * nb.words * 8));
+      // linear bit index (psm_device.cuh BodyGeo::bits): ceil(bricks * 8^s / 64) words
+      nb.words = (int)(((nbk << (3 * sl)) + 63) / 64);
+      CUDA_TRY(c, cudaMalloc(&nb.d_bits, (size_t)nb.words * 8));
       CUDA_TRY(c, cudaMalloc(&nb.d_mask, nbk));
       const char* vx = std::getenv("PSM_VOXELIZE");
       const bool host_vox = vx && std::strcmp(vx, "host") == 0;

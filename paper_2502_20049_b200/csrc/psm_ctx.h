@@ -48,7 +48,7 @@ struct Body {
   // mesh geometry field (device)
   double o[3] = {0, 0, 0};
   int64_t dims[3] = {0, 0, 0};
-  int words = 1;
+  int words = 1;          // uint64 words of the packed geometry field
   unsigned long long* d_bits = nullptr;
   uint8_t* d_mask = nullptr;
   // prescribed motion: pose at step0, closed-form advance

@@ -73,11 +73,14 @@ struct BodyGeo {
   int dims_b[3];    // mesh: field extent in bricks (LBM cells)
   int kind;         // 0 sphere, 1 mesh
   int s;
-  int words;        // uint64 words per brick = max(1, 8^s / 64)
+  int words;        // uint64 words of the whole field
   int present;
   int mapping;      // 0 R1 (per sub-sample), 1 R2 (centre-only block average), meshes only
   int pad_;
-  const unsigned long long* bits;  // [brick][words]
+  // geometry bits packed linearly: bit (brick << 3s) + ((gz&m)*n + (gy&m))*n + (gx&m) of the
+  // uint64 array (a brick = the (2^s)^3 geometry cells of one LBM cell; at s = 0, 1 several
+  // bricks share a word instead of one word per brick, so the field stays cache-sized)
+  const unsigned long long* bits;
   const uint8_t* mask;             // [brick] flag bits, see pack_bricks (voxelize.cpp)
 };
 

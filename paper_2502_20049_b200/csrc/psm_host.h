@@ -15,6 +15,6 @@ void voxelize_mesh(const double* verts, int64_t nv, const int32_t* tris, int64_t
                    std::vector<uint8_t>& bits);
 void pack_bricks(const std::vector<uint8_t>& bits, int s, const int64_t dims_cells[3],
                  std::vector<unsigned long long>& words, std::vector<uint8_t>& mask,
-                 int* words_per_brick);
+                 int* total_words);
 
 }  // namespace psm

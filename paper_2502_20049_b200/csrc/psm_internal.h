@@ -32,8 +32,8 @@ struct VoxParams {
   int s;                     // super-sampling level: 2^s samples per LBM cell and axis
   long long NX, NY, NZ;      // geometry cells (= LBM cells << s)
   long long bx, by, bz;      // bricks (= LBM cells of the field)
-  int W;                     // uint64 words per brick
-  unsigned long long* words; // [bricks][W] output
+  int W;                     // uint64 words of the whole packed field
+  unsigned long long* words; // [W] output, linear bit index (brick << 3s) + bit in brick
   unsigned* tog;             // scratch: toggle bits, wpr words per (gy, gz) row
   long long wpr;
 };

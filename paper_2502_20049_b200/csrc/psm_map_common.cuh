@@ -42,8 +42,9 @@ __device__ __forceinline__ void mesh_word_index(const BodyGeo& b, int x, int y, 
   const long long brick =
       ((long long)(g[2] >> b.s) * b.dims_b[1] + (g[1] >> b.s)) * b.dims_b[0] + (g[0] >> b.s);
   const int bit = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
-  wi = brick * b.words + (bit >> 6);
-  bitpos = bit & 63;
+  const long long gb = (brick << (3 * b.s)) + bit;  // linear bit index (psm_device.cuh)
+  wi = gb >> 6;
+  bitpos = (int)(gb & 63);
 }
 
 __device__ __forceinline__ int mesh_bit(const BodyGeo& b, const double q[3]) {
@@ -58,9 +59,9 @@ __device__ __forceinline__ int mesh_bit(const BodyGeo& b, const double q[3]) {
   const int n = 1 << b.s, msk = n - 1;
   const long long brick =
       ((long long)(g[2] >> b.s) * b.dims_b[1] + (g[1] >> b.s)) * b.dims_b[0] + (g[0] >> b.s);
-  const int bit = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
-  const unsigned long long w = __ldg(b.bits + brick * b.words + (bit >> 6));
-  return (int)((w >> (bit & 63)) & 1ull);
+  const long long gb = (brick << (3 * b.s)) + ((((g[2] & msk) * n) + (g[1] & msk)) * n +
+                                                (g[0] & msk));
+  return (int)((__ldg(b.bits + (gb >> 6)) >> (gb & 63)) & 1ull);
 }
 
 // geometry bit g (in field range) of a mesh body
@@ -68,8 +69,8 @@ __device__ __forceinline__ int field_bit(const BodyGeo& b, int gx, int gy, int g
   const int n = 1 << b.s, msk = n - 1;
   const long long brick =
       ((long long)(gz >> b.s) * b.dims_b[1] + (gy >> b.s)) * b.dims_b[0] + (gx >> b.s);
-  const int bit = (((gz & msk) * n) + (gy & msk)) * n + (gx & msk);
-  return (int)((__ldg(b.bits + brick * b.words + (bit >> 6)) >> (bit & 63)) & 1ull);
+  const long long gb = (brick << (3 * b.s)) + ((((gz & msk) * n) + (gy & msk)) * n + (gx & msk));
+  return (int)((__ldg(b.bits + (gb >> 6)) >> (gb & 63)) & 1ull);
 }
 
 // R2 (paper-literal): only the cell centre is transformed (A14 arithmetic); the
@@ -293,9 +294,10 @@ __device__ __forceinline__ int mesh_count8(const BodyGeo& b, int x, int y, int z
       if (in) {
         const long long brick = ((long long)(g[2] >> b.s) * b.dims_b[1] + (g[1] >> b.s)) *
                                     b.dims_b[0] + (g[0] >> b.s);
-        const int bb = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
-        wi = brick * b.words + (bb >> 6);
-        bit = bb & 63;
+        const long long gb = (brick << (3 * b.s)) + ((((g[2] & msk) * n) + (g[1] & msk)) * n +
+                                                      (g[0] & msk));
+        wi = gb >> 6;
+        bit = (int)(gb & 63);
       }
     }
     if (wi >= 0) cnt += (int)((__ldg(b.bits + wi) >> bit) & 1ull);

@@ -167,7 +167,8 @@ void voxelize_mesh(const double* verts, int64_t nv, const int32_t* tris, int64_t
   }
 }
 
-// Pack into LBM-cell bricks of (2^s)^3 bits (words = max(1, 8^s/64) uint64 each) and build the
+// Pack into LBM-cell bricks of (2^s)^3 bits (linear bit index (brick << 3s) + bit, so bricks
+// share uint64 words at s = 0, 1) and build the
 // per-brick flags the remap kernel's exact early-outs use (cells beyond the field count as
 // all-outside):
 //   bit0: the brick and its 26 neighbours are all-outside   (one cell's sub-samples)
@@ -202,14 +203,15 @@ static void box_or(std::vector<uint8_t>& v, int64_t bx, int64_t by, int64_t bz, 
 
 void pack_bricks(const std::vector<uint8_t>& bits, int s, const int64_t dims_cells[3],
                  std::vector<unsigned long long>& words, std::vector<uint8_t>& mask,
-                 int* words_per_brick) {
+                 int* total_words) {
   const int n = 1 << s;
-  const int W = std::max(1, (n * n * n) / 64);
-  *words_per_brick = W;
   const int64_t bx = dims_cells[0], by = dims_cells[1], bz = dims_cells[2];
   const int64_t NX = bx << s, NY = by << s;
   const int64_t nb = bx * by * bz;
-  words.assign((size_t)(nb * W), 0ull);
+  // linear bit index (b << 3s) + bit: bricks share words at s = 0, 1
+  const int64_t W = ((nb << (3 * s)) + 63) / 64;
+  *total_words = (int)W;
+  words.assign((size_t)W, 0ull);
   std::vector<uint8_t> any_in((size_t)nb, 0), any_out((size_t)nb, 0);
 #pragma omp parallel for schedule(static)
   for (int64_t b = 0; b < nb; ++b) {
@@ -221,7 +223,9 @@ void pack_bricks(const std::vector<uint8_t>& bits, int s, const int64_t dims_cel
           const int64_t g = ((iz * n + sz) * NY + (iy * n + sy)) * NX + (ix * n + sx);
           if (bits[(size_t)g]) {
             const int bit = (sz * n + sy) * n + sx;
-            words[(size_t)(b * W + (bit >> 6))] |= 1ull << (bit & 63);
+            const int64_t gb = (b << (3 * s)) + bit;
+#pragma omp atomic
+            words[(size_t)(gb >> 6)] |= 1ull << (gb & 63);
             ++ones;
           }
         }
