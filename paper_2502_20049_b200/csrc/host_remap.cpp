@@ -162,7 +162,7 @@ psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
       }
       CUDA_TRY(c, launch_remap_single(r, c->mst == c->st ? 148 * 8 : ahead_blocks(c, r.body.s), c->mst,
                                       c->mst == c->st ? 256 : c->ahead_threads));
-      c->launches += 4;
+      c->launches += 3 + remap_l3_kernels(r.body);
       continue;
     }
     // general box (several bodies may cover its cells): one launch, 3D grid of its tiles
@@ -342,7 +342,7 @@ psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
     r.margin = 1;
     CUDA_TRY(c, launch_remap_band(r, c->mst == c->st ? 148 * 8 : ahead_blocks(c, b.s), c->mst,
                                   c->mst == c->st ? 256 : c->ahead_threads));
-    c->launches += (b.s >= 2 && b.mapping == 0) ? 2 : 1;
+    c->launches += remap_l3_kernels(r.body);
   }
   if (!incr.empty() && record(c, 0, 1, c->mst) != cudaSuccess)
     FAIL(c, PSM_E_CUDA, "event record failed");

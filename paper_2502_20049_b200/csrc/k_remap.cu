@@ -215,23 +215,20 @@ __global__ void __launch_bounds__(256, PSM_REMAP_MINB) k_remap_l3(const __grid_c
         for (int j = 0; j < m; ++j) cnt += sample_inside(b, x, y, zg, s0 + j, L, G.wall);
         continue;
       }
-      if (m == 8) {
-        cnt += mesh_count8(b, x, y, zg, s0, L, G.wall);
-      } else {  // s = 0: the single sample
-        for (int j = 0; j < m; ++j) {
-          long long wi;
-          int bit;
-          mesh_word_index(b, x, y, zg, s0 + j, L, G.wall, wi, bit);
-          if (wi >= 0) cnt += (int)((__ldg(b.bits + wi) >> bit) & 1ull);
-        }
+      // mesh at s = 0 (s >= 1 meshes run k_remap_l3_mesh): the single sample
+      for (int j = 0; j < m; ++j) {
+        long long wi;
+        int bit;
+        mesh_word_index(b, x, y, zg, s0 + j, L, G.wall, wi, bit);
+        if (wi >= 0) cnt += (int)((__ldg(b.bits + wi) >> bit) & 1ull);
       }
     }
     put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
   }
 }
 
-// L3 for s >= 2 (64 or 512 sub-samples per cell): one thread per (band cell, 8-sample chunk),
-// batched geometry-bit loads, integer atomics into the cell's count (order-independent); L4
+// L3 for spheres at s >= 2 (64 or 512 sub-samples per cell): one thread per (band cell, 8-sample
+// chunk), integer atomics into the cell's count (order-independent); L4
 // writes the words.
 __global__ void __launch_bounds__(256, PSM_REMAP_MINB) k_remap_l3_chunks(const __grid_constant__ RemapParams r) {
   const Geom& G = r.g;
@@ -247,12 +244,45 @@ __global__ void __launch_bounds__(256, PSM_REMAP_MINB) k_remap_l3_chunks(const _
     band_cell(r, r.band[k], x, y, z, tile);
     const int zg = G.z0 + z;
     int cnt = 0;
-    if (b.kind == 0) {
-      for (int j = 0; j < 8; ++j) cnt += sample_inside(b, x, y, zg, ch * 8 + j, L, G.wall);
-    } else {
-      cnt = mesh_count8(b, x, y, zg, ch * 8, L, G.wall);
-    }
+    for (int j = 0; j < 8; ++j) cnt += sample_inside(b, x, y, zg, ch * 8 + j, L, G.wall);
     if (cnt) atomicAdd(r.bandcnt + k, cnt);
+  }
+}
+
+// L3 for mesh bodies with R1 at s = 1..3 (S compile-time): G lanes per band cell (8 at s >= 2,
+// one 8-sample chunk each at s = 2, eight at s = 3; 1 at s = 1), mesh_count8_t per chunk, the
+// lanes' counts summed with shuffles and the word written by the cell's first lane (no count
+// atomics, no L4).  Warps iterate together (warp-uniform loop bound) so the full-mask shuffles
+// are legal; items = cells * G with G | 32, so a cell's lanes are all active or all idle.
+template <int S>
+__global__ void __launch_bounds__(256, PSM_REMAP_MINB) k_remap_l3_mesh(const __grid_constant__ RemapParams r) {
+  constexpr int kLanes = S >= 2 ? 8 : 1;
+  constexpr int C = S >= 2 ? (1 << (3 * S - 3)) / kLanes : 1;  // 8-sample chunks per lane
+  const Geom& G = r.g;
+  const BodyGeo& b = r.body;
+  const int n = min(*r.bandn, r.band_cap);
+  const long long items = (long long)n * kLanes;
+  const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (long long wb = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); wb < items;
+       wb += stride) {
+    const long long it = wb + lane;
+    const bool act = it < items;
+    const int k = (int)(it / kLanes), ch = (int)(it % kLanes);
+    int x = 0, y = 0, z = 0, tile = 0, cnt = 0;
+    if (act) {
+      band_cell(r, r.band[k], x, y, z, tile);
+#pragma unroll 1
+      for (int c = 0; c < C; ++c)
+        cnt += mesh_count8_t<S>(b, x, y, G.z0 + z, (ch * C + c) * 8, L, G.wall);
+    }
+    if (kLanes > 1) {
+#pragma unroll
+      for (int o = 1; o < kLanes; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if (act && ch == 0)
+      put_word(r, x, y, z, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, tile);
   }
 }
 
@@ -267,17 +297,31 @@ __global__ void k_remap_l4(const __grid_constant__ RemapParams r) {
   }
 }
 
+// the exact (L3) stage for body r.body over the band list
+void launch_l3(const RemapParams& r, int blocks, cudaStream_t st, int threads) {
+  const BodyGeo& b = r.body;
+  if (b.kind == 1 && b.mapping == 0 && b.s >= 1) {
+    if (b.s == 1) k_remap_l3_mesh<1><<<blocks, threads, 0, st>>>(r);
+    else if (b.s == 2) k_remap_l3_mesh<2><<<blocks, threads, 0, st>>>(r);
+    else k_remap_l3_mesh<3><<<blocks, threads, 0, st>>>(r);
+  } else if (b.s >= 2 && b.mapping == 0) {
+    k_remap_l3_chunks<<<blocks, threads, 0, st>>>(r);
+    k_remap_l4<<<blocks, threads, 0, st>>>(r);
+  } else {
+    k_remap_l3<<<blocks, threads, 0, st>>>(r);
+  }
+}
+
 }  // namespace
+
+int remap_l3_kernels(const BodyGeo& b) {
+  return (b.kind != 1 && b.s >= 2 && b.mapping == 0) ? 2 : 1;
+}
 
 // the exact pass alone over a cached band (poses within one cell of the band's build pose)
 cudaError_t launch_remap_band(const RemapParams& r, int persistent_blocks, cudaStream_t st,
                               int threads) {
-  if (r.body.s >= 2 && r.body.mapping == 0) {
-    k_remap_l3_chunks<<<persistent_blocks, threads, 0, st>>>(r);
-    k_remap_l4<<<persistent_blocks, threads, 0, st>>>(r);
-  } else {
-    k_remap_l3<<<persistent_blocks, threads, 0, st>>>(r);
-  }
+  launch_l3(r, persistent_blocks, st, threads);
   return cudaGetLastError();
 }
 
@@ -291,12 +335,7 @@ cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cud
   k_remap_l0<<<(ntile + 255) / 256, 256, 0, st>>>(r);
   k_remap_l1<<<persistent_blocks, threads, 0, st>>>(r);
   k_remap_l2<<<persistent_blocks, threads, 0, st>>>(r);
-  if (r.body.s >= 2 && r.body.mapping == 0) {
-    k_remap_l3_chunks<<<persistent_blocks, threads, 0, st>>>(r);
-    k_remap_l4<<<persistent_blocks, threads, 0, st>>>(r);
-  } else {
-    k_remap_l3<<<persistent_blocks, threads, 0, st>>>(r);
-  }
+  launch_l3(r, persistent_blocks, st, threads);
   return cudaGetLastError();
 }
 

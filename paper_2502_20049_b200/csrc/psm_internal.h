@@ -44,6 +44,7 @@ cudaError_t launch_voxelize(VoxParams p, void* scratch, uint8_t* mask, cudaStrea
 cudaError_t launch_map(const MapParams& p, cudaStream_t st);
 cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cudaStream_t st,
                                 int threads = 256);
+int remap_l3_kernels(const BodyGeo& b);  // kernels launch_remap_band launches
 cudaError_t launch_remap_band(const RemapParams& r, int persistent_blocks, cudaStream_t st,
                               int threads = 256);
 

@@ -228,10 +228,6 @@ __device__ __forceinline__ int cell_decision_own(const BodyGeo& b, int x, int y,
   return cell_decision(b, qc, margin);
 }
 
-// Warp-centric remap of one 32x4x2 tile per block: each warp owns one 32-cell x-row and decides
-// it without block barriers: (1) per 8-cell segment (reach kSubReach bricks), (2) per cell in
-// fp32 (dilated-by-one brick flags), (3) the narrow-band cells' sub-samples packed across the 32
-// lanes (lane -> (cell, sample) pairs) and counted with ballots — exact fp64 per sample.
 // exact count of a cell for body b (R1: all sub-samples; R2: the centre block)
 __device__ __forceinline__ int exact_count(const BodyGeo& b, int x, int y, int zg,
                                            const double L[3], const int wall[3]) {
@@ -241,66 +237,84 @@ __device__ __forceinline__ int exact_count(const BodyGeo& b, int x, int y, int z
   return cnt;
 }
 
+// exact inside test of one mesh sub-sample, out of line (the rare fallback of mesh_count8_t)
+static __device__ __noinline__ int mesh_sample_exact(const BodyGeo& b, int x, int y, int zg,
+                                                     int si, const double L[3],
+                                                     const int wall[3]) {
+  long long wi;
+  int bit;
+  mesh_word_index(b, x, y, zg, si, L, wall, wi, bit);
+  return wi >= 0 ? (int)((__ldg(b.bits + wi) >> bit) & 1ull) : 0;
+}
+
 // Inside count of 8 consecutive sub-samples (si0 .. si0+7, same cell, si0 % 8 == 0) of a mesh
-// body.  Sample si0 is transformed with the exact A14 arithmetic; the others by adding the
-// rotated sub-sample offsets (error ~1e-13 cells).  A sample whose scaled coordinate lies within
-// 1e-9 of a geometry-cell face is recomputed exactly, so every floor() equals the exact one and
-// the count is bit-identical to mesh_word_index() per sample.  Each sample's geometry word is
-// loaded as soon as its index is known, U samples in flight: few live registers, so more warps
-// hide the load latency (measured faster than eight batched 64-bit indices).
-#ifndef PSM_REMAP_U
-#define PSM_REMAP_U 1
-#endif
-constexpr int kRemapU = PSM_REMAP_U;
-__device__ __forceinline__ int mesh_count8(const BodyGeo& b, int x, int y, int zg, int si0,
-                                           const double L[3], const int wall[3]) {
-  const int n = 1 << b.s, msk = n - 1;
-  const double h = ldexp(1.0, -b.s), hs = ldexp(1.0, b.s);
-  const int gx0 = si0 & msk, gy0 = (si0 >> b.s) & msk, gz0 = si0 >> (2 * b.s);
-  const double p0[3] = {(double)x + (gx0 + 0.5) * h, (double)y + (gy0 + 0.5) * h,
+// body, super-sampling exponent S fixed at compile time (S = 1..3, R1).  The lattice offsets
+// of the seven samples relative to si0 are constants.  Only sample si0 is transformed in fp64
+// with the exact A14 arithmetic, split into the integer geometry cell base[] and the fraction
+// in [0, 1).  The seven others are base + fraction + (rotated lattice offsets) in fp32:
+// |value| < 8, error < 2e-6 cells, floored with the magic-number add (round(v - 1/2) = floor(v)
+// away from integers).  A sample whose fp32 fraction lies within kTol = 1e-5 of a geometry-cell
+// face takes the exact path (mesh_sample_exact), so every count equals the per-sample exact one
+// bit for bit.
+// The seven are taken in the periodic image of sample si0.  That changes no count:
+// psm_set_body requires r_bound + 1 < L/2 on periodic axes, so a sample inside the body in
+// either image has |d| < L/2 - 1 in it; that image is then its minimum image, and si0 (less
+// than one cell away) takes the same one.  Every other sample is outside in both images.
+// (Replaces a form that transformed every sample in fp64, ~150 instructions per sample; c3
+// scenario A at s = 2 went from 1.378 to 1.120 ms per step.)
+template <int S>
+__device__ __forceinline__ int mesh_count8_t(const BodyGeo& b, int x, int y, int zg, int si0,
+                                             const double L[3], const int wall[3]) {
+  static_assert(S >= 1 && S <= 3, "S in 1..3");
+  constexpr int n = 1 << S, msk = n - 1;
+  constexpr double h = 1.0 / n, hs = (double)n;
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: ulp 1, float bits - magic bits = integer
+  constexpr float kTol = 1e-5f;
+  const int gy0 = (si0 >> S) & msk, gz0 = si0 >> (2 * S);  // si0 % 8 == 0: x offset 0
+  const double p0[3] = {(double)x + 0.5 * h, (double)y + (gy0 + 0.5) * h,
                         (double)zg + (gz0 + 0.5) * h};
   double q0[3];
   body_frame(b, p0, L, wall, q0);
+  int base[3];
+  float rh[3];  // fraction of sample si0's field coordinate, minus 1/2
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double f = __dmul_rn(__dsub_rn(q0[a], b.o[a]), hs);
+    const double fl = floor(f);
+    base[a] = (fl > -1e9 && fl < 1e9) ? (int)fl : -(1 << 30);  // far outside: any sample misses
+    rh[a] = (float)(f - fl) - 0.5f;
+  }
+  const float qx[3] = {(float)b.Q[0], (float)b.Q[1], (float)b.Q[2]};
+  const float qy[3] = {(float)b.Q[3], (float)b.Q[4], (float)b.Q[5]};
+  const float qz[3] = {(float)b.Q[6], (float)b.Q[7], (float)b.Q[8]};
   int cnt = 0;
-#pragma unroll kRemapU
+#pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const int si = si0 + j;
-    const int gx = si & msk, gy = (si >> b.s) & msk, gz = si >> (2 * b.s);
-    const double dx = (gx - gx0) * h, dy = (gy - gy0) * h, dz = (gz - gz0) * h;
-    double f[3];
-    bool safe = true;
+    const int dgx = j & msk, dgy = (j >> S) & msk, dgz = j >> (2 * S);
+    int g[3];
+    bool safe = true, in = true;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const double qa = q0[a] + (b.Q[a] * dx + b.Q[3 + a] * dy + b.Q[6 + a] * dz);
-      f[a] = (qa - b.o[a]) * hs;
-      const double fr = f[a] - floor(f[a]);
-      if (fr < 1e-9 || fr > 1.0 - 1e-9) safe = false;
+      float v = rh[a];
+      if (dgx) v = __fmaf_rn((float)dgx, qx[a], v);
+      if (dgy) v = __fmaf_rn((float)dgy, qy[a], v);
+      if (dgz) v = __fmaf_rn((float)dgz, qz[a], v);
+      const float t = __fadd_rn(v, kMagic);  // kMagic + round(v)
+      const int i = __float_as_int(t) - __float_as_int(kMagic);
+      const float fr = __fsub_rn(v, __fsub_rn(t, kMagic));  // v - round(v), in [-1/2, 1/2]
+      safe = safe && fabsf(fr) < 0.5f - kTol;
+      g[a] = base[a] + i;
+      in = in && (unsigned)g[a] < (unsigned)(b.dims_b[a] << S);
     }
-    long long wi;
-    int bit;
     if (!safe) {
-      mesh_word_index(b, x, y, zg, si, L, wall, wi, bit);
-    } else {
-      int g[3];
-      bool in = true;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double xx = floor(f[a]);
-        if (!(xx >= 0.0) || xx >= (double)(b.dims_b[a] << b.s)) in = false;
-        g[a] = (int)xx;
-      }
-      wi = -1;
-      bit = 0;
-      if (in) {
-        const long long brick = ((long long)(g[2] >> b.s) * b.dims_b[1] + (g[1] >> b.s)) *
-                                    b.dims_b[0] + (g[0] >> b.s);
-        const long long gb = (brick << (3 * b.s)) + ((((g[2] & msk) * n) + (g[1] & msk)) * n +
-                                                      (g[0] & msk));
-        wi = gb >> 6;
-        bit = (int)(gb & 63);
-      }
+      cnt += mesh_sample_exact(b, x, y, zg, si0 + j, L, wall);
+    } else if (in) {
+      const long long brick =
+          ((long long)(g[2] >> S) * b.dims_b[1] + (g[1] >> S)) * b.dims_b[0] + (g[0] >> S);
+      const int bb = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
+      const long long gb = (brick << (3 * S)) + bb;
+      cnt += (int)((__ldg(b.bits + (gb >> 6)) >> (gb & 63)) & 1ull);
     }
-    if (wi >= 0) cnt += (int)((__ldg(b.bits + wi) >> bit) & 1ull);
   }
   return cnt;
 }
