@@ -240,6 +240,40 @@ def test_write_read_roundtrip_and_equilibrium():
     assert np.allclose(r2, rho, atol=1e-14) and np.allclose(u2, u, atol=1e-14)
 
 
+@pytest.mark.parametrize("s", [1, 2, 3])
+def test_mesh_band_pass_exact_on_geometry_cell_faces(s):
+    """The mesh band pass (k_remap_l3_mesh) transforms one sub-sample per 8 in fp64 and the
+    others in fp32, falling back to the exact per-sample arithmetic within 1e-5 of a
+    geometry-cell face.  Poses that put every sub-sample exactly on a face (identity rotation,
+    t offset by half a sub-sample spacing), within ~1e-4 of one (a 3e-6 rad rotation) and a
+    generic pose: counts bit-exact against the oracle's per-sample A14 arithmetic (reading R1)."""
+    import psm_inputs.meshgen as mg
+    n = 48
+    h = 0.5 ** s
+    meshes = [pi.box_mesh([-9.0, -7.0, -8.0], [8.0, 9.0, 7.0]), mg.uv_sphere_mesh(12.3, 24, 16),
+              pi.propeller_mesh(n_blades=4, scale=0.16, n_st=10, n_pts=16, hub_seg=24)]
+    c = np.array([24.0, 23.0, 25.0]) + h / 2
+    poses = [(np.eye(3), c), (pi.rotation_about([1.0, -2.0, 0.5], 3e-6), c),
+             (pi.rotation_about([0.3, 1.0, -0.7], 0.61), c + [0.17, -0.29, 0.05])]
+    g = _sim(nx=n, ny=n, nz=n, Q=19, tau=0.8, prec="f32")
+    for v, tr in meshes:
+        o = oracle.Oracle(n, n, n, 19, 0.8, (0, 0, 0), 1, 1)
+        o.set_mesh(1, v, tr, s)
+        for k, (Q, t) in enumerate(poses):
+            if k == 0:
+                g.set_mesh(1, v, tr, s, Q, t)
+            else:
+                g.set_pose(1, Q, t)
+            o.set_pose(1, Q, t)
+            o.map()
+            co = o.fractions()[2]
+            cg = g.fractions()[2]
+            assert co.sum() > 0
+            assert np.array_equal(co, cg), (s, k, int((co != cg).sum()))
+        g.remove_body(1)
+    g.close()
+
+
 @pytest.mark.parametrize("s", [1, 2])
 def test_cror_rotor_fractions_bit_exact_large(s):
     """A 12-blade rotor (tip 55 cells, coarse CROR recipe) rotating about x in a 128^3 box: the
