@@ -28,9 +28,10 @@ namespace {
 constexpr int kSegPerTile = (kTileX / kSubX) * kTileY * kTileZ;  // 32
 
 __device__ __forceinline__ void tile_coords(int t, const Geom& G, int& tx, int& ty, int& tz) {
-  tx = t % G.gx;
-  ty = (t / G.gx) % G.gy;
-  tz = t / (G.gx * G.gy);
+  const uint32_t u = (uint32_t)t, q = fast_div(u, G.fgx), z = fast_div(u, G.fgxy);
+  tx = (int)(u - q * (uint32_t)G.gx);
+  ty = (int)(q - z * (uint32_t)G.gy);
+  tz = (int)z;
 }
 
 // the cells a tile really holds (a ragged last tile is clamped to the grid): centre, half extents

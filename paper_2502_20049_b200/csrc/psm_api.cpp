@@ -143,6 +143,8 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   g.gx = (int)((grid->nx + kTileX - 1) / kTileX);
   g.gy = (int)((grid->ny + kTileY - 1) / kTileY);
   g.gz = (int)((c->nzl + kTileZ - 1) / kTileZ);
+  g.fgx = make_fastdiv((uint32_t)g.gx);
+  g.fgxy = make_fastdiv((uint32_t)g.gx * (uint32_t)g.gy);
   if (g.qstride >= (1ll << 31) || grid->nx >= (1 << 30) || grid->ny > 65535 * kTileY ||
       c->nzl > 65535 * kTileZ) {
     delete c;
@@ -312,6 +314,8 @@ psm_status psm_set_body(psm_ctx* c, int32_t id, const psm_shape* shape, const ps
       const int sl = shape->s;
       const size_t nbk = (size_t)(nb.dims[0] * nb.dims[1] * nb.dims[2]);
       // linear bit index (psm_device.cuh BodyGeo::bits): ceil(bricks * 8^s / 64) words
+      if (nbk >= (1ull << 31) || ((nbk << (3 * sl)) + 63) / 64 >= (1ull << 31))
+        FAIL(c, PSM_E_ARG, "mesh geometry field too large (32-bit brick and word indices)");
       nb.words = (int)(((nbk << (3 * sl)) + 63) / 64);
       CUDA_TRY(c, cudaMalloc(&nb.d_bits, (size_t)nb.words * 8));
       CUDA_TRY(c, cudaMalloc(&nb.d_mask, nbk));

@@ -73,6 +73,70 @@ __device__ __forceinline__ int field_bit(const BodyGeo& b, int gx, int gy, int g
   return (int)((__ldg(b.bits + (gb >> 6)) >> (gb & 63)) & 1ull);
 }
 
+// bits [lo, hi) of each of the R consecutive groups of W bits (a box's extent along one axis,
+// replicated over the slower axes); 0 <= lo <= hi <= W, R * W <= 64
+template <int W, int R>
+__device__ __forceinline__ unsigned long long rep_mask(int lo, int hi) {
+  const unsigned long long one = ((1ull << hi) - 1ull) & ~((1ull << lo) - 1ull);
+  unsigned long long m = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) m |= one << (r * W);
+  return m;
+}
+// bits [lo * W, hi * W) of a (R * W)-bit group
+template <int W>
+__device__ __forceinline__ unsigned long long range_mask(int lo, int hi) {
+  const unsigned long long h = (hi * W >= 64) ? ~0ull : ((1ull << (hi * W)) - 1ull);
+  return h & ~((1ull << (lo * W)) - 1ull);
+}
+
+// number of set geometry cells in the 2^S-cube block [g0, g0 + 2^S) (cells beyond the field
+// count 0): the block overlaps at most 2 x 2 x 2 bricks; per brick the overlapped cells form a
+// box whose bit mask is built from per-axis ranges, then one popcount per word (S = 1: a brick
+// is one byte of a word; S = 2: one word; S = 3: eight words, one per z layer)
+template <int S>
+__device__ __forceinline__ int r2_block_count(const BodyGeo& b, const long long g0[3]) {
+  constexpr int n = 1 << S;
+  long long B0[3];
+  int nb[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    B0[a] = g0[a] >> S;  // floor division (arithmetic shift)
+    nb[a] = ((g0[a] + n - 1) >> S) == B0[a] ? 1 : 2;
+  }
+  int cnt = 0;
+  for (int kz = 0; kz < nb[2]; ++kz) {
+    const long long Bz = B0[2] + kz;
+    if (Bz < 0 || Bz >= b.dims_b[2]) continue;
+    const int lz = (int)max(g0[2] - (Bz << S), 0ll), hz = (int)min(g0[2] + n - (Bz << S), (long long)n);
+    for (int ky = 0; ky < nb[1]; ++ky) {
+      const long long By = B0[1] + ky;
+      if (By < 0 || By >= b.dims_b[1]) continue;
+      const int ly = (int)max(g0[1] - (By << S), 0ll), hy = (int)min(g0[1] + n - (By << S), (long long)n);
+      for (int kx = 0; kx < nb[0]; ++kx) {
+        const long long Bx = B0[0] + kx;
+        if (Bx < 0 || Bx >= b.dims_b[0]) continue;
+        const int lx = (int)max(g0[0] - (Bx << S), 0ll), hx = (int)min(g0[0] + n - (Bx << S), (long long)n);
+        const unsigned long long brick = ((unsigned long long)Bz * b.dims_b[1] + By) * b.dims_b[0] + Bx;
+        if constexpr (S == 1) {  // bit z*4 + y*2 + x of byte (brick & 7) of word brick >> 3
+          const unsigned long long m =
+              rep_mask<2, 4>(lx, hx) & rep_mask<4, 2>(2 * ly, 2 * hy) & range_mask<4>(lz, hz);
+          const unsigned long long w = __ldg(b.bits + (brick >> 3)) >> ((brick & 7ull) * 8);
+          cnt += __popcll(w & m);
+        } else if constexpr (S == 2) {  // bit z*16 + y*4 + x of word brick
+          const unsigned long long m =
+              rep_mask<4, 16>(lx, hx) & rep_mask<16, 4>(4 * ly, 4 * hy) & range_mask<16>(lz, hz);
+          cnt += __popcll(__ldg(b.bits + brick) & m);
+        } else {  // S = 3: bit y*8 + x of word brick*8 + z
+          const unsigned long long m = rep_mask<8, 8>(lx, hx) & range_mask<8>(ly, hy);
+          for (int z = lz; z < hz; ++z) cnt += __popcll(__ldg(b.bits + brick * 8 + z) & m);
+        }
+      }
+    }
+  }
+  return cnt;
+}
+
 // R2 (paper-literal): only the cell centre is transformed (A14 arithmetic); the
 // count is the number of set geometry cells in the 2^s-cube block whose lower corner is
 // g0 = floor((q_c - o) 2^s - 2^(s-1) + 1/2); cells beyond the field count 0.
@@ -88,7 +152,13 @@ static __device__ __noinline__ int r2_count(const BodyGeo& b, int x, int y, int 
   for (int a = 0; a < 3; ++a)
     g0[a] = (long long)floor(__dadd_rn(__dsub_rn(__dmul_rn(__dsub_rn(q[a], b.o[a]), hs), half),
                                        0.5));
-  int cnt = 0;
+  switch (b.s) {
+    case 1: return r2_block_count<1>(b, g0);
+    case 2: return r2_block_count<2>(b, g0);
+    case 3: return r2_block_count<3>(b, g0);
+    default: break;
+  }
+  int cnt = 0;  // s = 0: the single geometry cell
   for (int k = 0; k < n; ++k)
     for (int j = 0; j < n; ++j)
       for (int i = 0; i < n; ++i) {
@@ -309,11 +379,20 @@ __device__ __forceinline__ int mesh_count8_t(const BodyGeo& b, int x, int y, int
     if (!safe) {
       cnt += mesh_sample_exact(b, x, y, zg, si0 + j, L, wall);
     } else if (in) {
-      const long long brick =
-          ((long long)(g[2] >> S) * b.dims_b[1] + (g[1] >> S)) * b.dims_b[0] + (g[0] >> S);
-      const int bb = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
-      const long long gb = (brick << (3 * S)) + bb;
-      cnt += (int)((__ldg(b.bits + (gb >> 6)) >> (gb & 63)) & 1ull);
+      // 32-bit: the field's word count fits an int (BodyGeo::words), and so does bricks * 8^S / 64
+      const uint32_t brick =
+          ((uint32_t)(g[2] >> S) * (uint32_t)b.dims_b[1] + (uint32_t)(g[1] >> S)) *
+              (uint32_t)b.dims_b[0] + (uint32_t)(g[0] >> S);
+      const uint32_t bb = (((g[2] & msk) * n) + (g[1] & msk)) * n + (g[0] & msk);
+      uint32_t wi, bit;
+      if constexpr (S == 1) {
+        wi = brick >> 3;
+        bit = ((brick & 7u) << 3) | bb;
+      } else {
+        wi = (brick << (3 * S - 6)) | (bb >> 6);
+        bit = bb & 63u;
+      }
+      cnt += (int)((__ldg(b.bits + wi) >> bit) & 1ull);
     }
   }
   return cnt;

@@ -240,13 +240,17 @@ def test_write_read_roundtrip_and_equilibrium():
     assert np.allclose(r2, rho, atol=1e-14) and np.allclose(u2, u, atol=1e-14)
 
 
+@pytest.mark.parametrize("mapping", ["R1", "R2"])
 @pytest.mark.parametrize("s", [1, 2, 3])
-def test_mesh_band_pass_exact_on_geometry_cell_faces(s):
+def test_mesh_band_pass_exact_on_geometry_cell_faces(s, mapping):
     """The mesh band pass (k_remap_l3_mesh) transforms one sub-sample per 8 in fp64 and the
     others in fp32, falling back to the exact per-sample arithmetic within 1e-5 of a
     geometry-cell face.  Poses that put every sub-sample exactly on a face (identity rotation,
     t offset by half a sub-sample spacing), within ~1e-4 of one (a 3e-6 rad rotation) and a
-    generic pose: counts bit-exact against the oracle's per-sample A14 arithmetic (reading R1)."""
+    generic pose: counts bit-exact against the oracle's per-sample A14 arithmetic (reading R1).
+    R2 (reading A12): the centre-only block count, by per-brick popcount masks in the library
+    (r2_block_count) and cell by cell in the oracle; the identity pose puts every block exactly on
+    one brick, the others make blocks straddle up to 2 x 2 x 2 bricks."""
     import psm_inputs.meshgen as mg
     n = 48
     h = 0.5 ** s
@@ -259,9 +263,10 @@ def test_mesh_band_pass_exact_on_geometry_cell_faces(s):
     for v, tr in meshes:
         o = oracle.Oracle(n, n, n, 19, 0.8, (0, 0, 0), 1, 1)
         o.set_mesh(1, v, tr, s)
+        o.set_mapping(1, mapping)
         for k, (Q, t) in enumerate(poses):
             if k == 0:
-                g.set_mesh(1, v, tr, s, Q, t)
+                g.set_mesh(1, v, tr, s, Q, t, mapping=mapping)
             else:
                 g.set_pose(1, Q, t)
             o.set_pose(1, Q, t)

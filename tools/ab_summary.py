@@ -25,7 +25,7 @@ for line in open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/ab.log"):
         if "f32" in r:
             res[cur]["f32 MLUPS"].append(r["f32"]["value"])
     elif "op" in r:
-        res[cur][f"{r['op']} {r['scen']} {r['var']} ms"].append(r["ms_per_step"])
+        res[cur][f"{r['op']} {r['scen']} {r['var']} {r.get('mapping', 'R1')} ms"].append(r["ms_per_step"])
 keys = sorted({k for v in res.values() for k in v})
 libs = list(res)
 print("| | " + " | ".join(libs) + " |")
