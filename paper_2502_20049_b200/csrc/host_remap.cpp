@@ -9,6 +9,14 @@ namespace psm {
 // s >= 2 where the 64-register chunked sample kernel fits twice into the registers one collide
 // block frees (measured: c3 scenario A at s = 2, 9963 -> 10183 MLUPS; one per SM is better for
 // the s = 1 band of c5w).  PSM_AHEAD_BLOCKS overrides.
+// the cached band pays off while its exact pass is cheap: R1 up to s = 1 (8 sub-samples per
+// cell; at s >= 2 the radius-2 band's 64/512 samples per cell cost more than the L0-L2
+// pipeline), R2 at every s (one block popcount per cell: c3 scenario A at s = 2, 1.014 ->
+// 0.924 ms per step)
+static bool cache_pays(const psm_ctx* c, const Body& b) {
+  return b.mapping == 1 ? b.s <= c->cache_max_s_r2 : b.s <= c->cache_max_s;
+}
+
 static int ahead_blocks(const psm_ctx* c, int s) {
   if (c->ahead_blocks_env > 0) return c->ahead_blocks_env;
   return s >= 2 ? 2 * 148 : 148;
@@ -273,9 +281,7 @@ psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
       continue;
     }
     b.ms.cache = false;
-    // the cached band pays off while the exact pass is cheap (8 sub-samples per cell); at
-    // s >= 2 the radius-2 band's 64/512 samples per cell cost more than the L0-L2 pipeline
-    b.want_cache = !no_cache && !c->dbg && b.s <= c->cache_max_s;
+    b.want_cache = !no_cache && !c->dbg && cache_pays(c, b);
     remap_region(c, b, Q, t, boxes);
   }
   // an incremental body whose (build) box meets a box remapped now goes the full way
@@ -285,7 +291,7 @@ psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
       Body& b = c->bodies[incr[k]];
       if (!boxes_overlap(c, b, boxes)) continue;
       b.ms.cache = false;
-      b.want_cache = b.s <= c->cache_max_s;
+      b.want_cache = cache_pays(c, b);
       remap_region(c, b, b.ms.Qc, b.ms.tc, boxes);
       incr.erase(incr.begin() + (long)k);
       changed = true;

@@ -136,7 +136,8 @@ struct psm_ctx {
   // PSM_BAND_CACHE=0, PSM_REMAP_GENERAL, PSM_SEG_CAP / PSM_BAND_CAP (cap the segment / band lists
   // of the full pipeline so that the in-kernel overflow paths run)
   bool no_cache = false, force_general = false;
-  int cache_max_s = 1;  // cached narrow band up to this s (PSM_CACHE_MAX_S)
+  int cache_max_s = 1;     // cached narrow band up to this s, R1 (PSM_CACHE_MAX_S)
+  int cache_max_s_r2 = 3;  // the same for R2 bodies (PSM_CACHE_MAX_S_R2)
   int hiocc_env = -1;   // PSM_HIOCC: force (1) / forbid (0) the higher-occupancy fp64 collide
   double psm_tile_frac = 0.0;  // PSM tiles / tiles in the last psm_step call
   int64_t seg_cap_env = 0, band_cap_env = 0;
