@@ -145,6 +145,8 @@ psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
       RemapParams r;
       std::memset(&r, 0, sizeof(r));
       r.g = c->geom;
+      r.fgx = make_fastdiv((uint32_t)r.g.gx);
+      r.fgxy = make_fastdiv((uint32_t)r.g.gx * (uint32_t)r.g.gy);
       r.box = tb[i];
       r.id = __builtin_ctz(tb[i].bodymask);
       r.body = mp.bodies[r.id];
@@ -321,6 +323,8 @@ psm_status remap(psm_ctx* c, const std::vector<int>& ids, int64_t step) {
     RemapParams r;
     std::memset(&r, 0, sizeof(r));
     r.g = c->geom;
+    r.fgx = make_fastdiv((uint32_t)r.g.gx);
+    r.fgxy = make_fastdiv((uint32_t)r.g.gx * (uint32_t)r.g.gy);
     r.id = id;
     BodyGeo& g = r.body;
     std::memcpy(g.Q, b.ms.Qc, sizeof(g.Q));

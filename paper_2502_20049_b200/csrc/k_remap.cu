@@ -27,8 +27,10 @@ namespace {
 
 constexpr int kSegPerTile = (kTileX / kSubX) * kTileY * kTileZ;  // 32
 
-__device__ __forceinline__ void tile_coords(int t, const Geom& G, int& tx, int& ty, int& tz) {
-  const uint32_t u = (uint32_t)t, q = fast_div(u, G.fgx), z = fast_div(u, G.fgxy);
+__device__ __forceinline__ void tile_coords(int t, const RemapParams& r, int& tx, int& ty,
+                                            int& tz) {
+  const Geom& G = r.g;
+  const uint32_t u = (uint32_t)t, q = fast_div(u, r.fgx), z = fast_div(u, r.fgxy);
   tx = (int)(u - q * (uint32_t)G.gx);
   ty = (int)(q - z * (uint32_t)G.gy);
   tz = (int)z;
@@ -91,7 +93,7 @@ __global__ void k_remap_l1(const __grid_constant__ RemapParams r) {
     const int tile = r.tiles[i / kSegPerTile];
     const int sg = i % kSegPerTile;
     int tx, ty, tz;
-    tile_coords(tile, G, tx, ty, tz);
+    tile_coords(tile, r, tx, ty, tz);
     const int sx = sg % (kTileX / kSubX), row = sg / (kTileX / kSubX);
     const int y = ty * kTileY + row % kTileY, z = tz * kTileZ + row / kTileY;
     if (y >= G.ny || z >= G.nzl) continue;
@@ -149,7 +151,7 @@ __global__ void k_remap_l2(const __grid_constant__ RemapParams r) {
     const uint32_t sgw = r.segs[si];
     const int tile = (int)(sgw >> 5), sg = (int)(sgw & 31u);
     int tx, ty, tz;
-    tile_coords(tile, G, tx, ty, tz);
+    tile_coords(tile, r, tx, ty, tz);
     const int sx = sg % (kTileX / kSubX), row = sg / (kTileX / kSubX);
     const int y = ty * kTileY + row % kTileY, z = tz * kTileZ + row / kTileY;
     const int x = tx * kTileX + sx * kSubX + c;
@@ -181,7 +183,7 @@ __device__ __forceinline__ void band_cell(const RemapParams& r, uint32_t e, int&
   tile = (int)(e >> 8);
   const int c = (int)(e & 255u);
   int tx, ty, tz;
-  tile_coords(tile, r.g, tx, ty, tz);
+  tile_coords(tile, r, tx, ty, tz);
   x = tx * kTileX + c % kTileX;
   y = ty * kTileY + (c / kTileX) % kTileY;
   z = tz * kTileZ + c / (kTileX * kTileY);

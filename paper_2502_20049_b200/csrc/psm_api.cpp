@@ -144,8 +144,6 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   g.gx = (int)((grid->nx + kTileX - 1) / kTileX);
   g.gy = (int)((grid->ny + kTileY - 1) / kTileY);
   g.gz = (int)((c->nzl + kTileZ - 1) / kTileZ);
-  g.fgx = make_fastdiv((uint32_t)g.gx);
-  g.fgxy = make_fastdiv((uint32_t)g.gx * (uint32_t)g.gy);
   if (g.qstride >= (1ll << 31) || grid->nx >= (1 << 30) || grid->ny > 65535 * kTileY ||
       c->nzl > 65535 * kTileZ) {
     delete c;

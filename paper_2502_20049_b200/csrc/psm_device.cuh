@@ -112,7 +112,6 @@ struct Geom {
   int open_x;             // x faces are inflow (x = 0) / outflow (x = nx-1), reading A30
   long long qstride;      // elements between consecutive direction planes
   int gx, gy, gz;         // tile grid
-  FastDiv fgx, fgxy;      // division by gx and gx * gy (tile index -> tile coordinates)
 };
 
 struct CollideParams {
@@ -188,6 +187,7 @@ struct RemapParams {
   int* bandn;           // number of band cells (counters + 2, or a cached band's count)
   int seg_cap, band_cap;
   int margin;           // 1: decisions valid for any pose within one cell (cached band)
+  FastDiv fgx, fgxy;    // division by g.gx and g.gx * g.gy (tile index -> tile coordinates)
 };
 
 #if defined(__CUDACC__)
