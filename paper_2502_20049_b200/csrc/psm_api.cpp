@@ -126,8 +126,9 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   if (const char* e = std::getenv("PSM_HIOCC")) c->hiocc_env = std::atoi(e) != 0 ? 1 : 0;
   if (const char* e = std::getenv("PSM_SEG_CAP")) c->seg_cap_env = std::max(1ll, std::atoll(e));
   if (const char* e = std::getenv("PSM_BAND_CAP")) c->band_cap_env = std::max(1ll, std::atoll(e));
-  if (const char* e = std::getenv("PSM_AHEAD_THREADS"))
-    c->ahead_threads = std::min(1024, std::max(32, std::atoi(e)));
+  if (const char* e = std::getenv("PSM_AHEAD_THREADS"))  // whole warps (the band pass sums a
+    // cell's 8 lanes with full-warp shuffles), at most the remap kernels' launch bound of 256
+    c->ahead_threads = std::min(256, std::max(32, std::atoi(e))) / 32 * 32;
   Geom& g = c->geom;
   g.nx = (int)grid->nx;
   g.ny = (int)grid->ny;
