@@ -147,6 +147,7 @@ psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
       r.g = c->geom;
       r.fgx = make_fastdiv((uint32_t)r.g.gx);
       r.fgxy = make_fastdiv((uint32_t)r.g.gx * (uint32_t)r.g.gy);
+      r.fused12 = c->remap_fused12;
       r.box = tb[i];
       r.id = __builtin_ctz(tb[i].bodymask);
       r.body = mp.bodies[r.id];
@@ -172,7 +173,7 @@ psm_status run_map(psm_ctx* c, const std::vector<Box>& boxes) {
       }
       CUDA_TRY(c, launch_remap_single(r, c->mst == c->st ? 148 * 8 : ahead_blocks(c, r.body.s), c->mst,
                                       c->mst == c->st ? 256 : c->ahead_threads));
-      c->launches += 3 + remap_l3_kernels(r.body);
+      c->launches += remap_single_kernels(r);
       continue;
     }
     // general box (several bodies may cover its cells): one launch, 3D grid of its tiles

@@ -178,6 +178,91 @@ __global__ void k_remap_l2(const __grid_constant__ RemapParams r) {
   }
 }
 
+// L1 + L2 fused: one thread per segment takes the L1 decision; the warp then decides the cells
+// of its undecided segments together, four segments (eight lanes each) per pass, instead of
+// listing them for a separate L2 launch.  Same decisions and writes as k_remap_l1/k_remap_l2
+// (whose segment list is bounded by seg_cap; here there is no segment list to overflow).
+__global__ void k_remap_l12(const __grid_constant__ RemapParams r) {
+  const Geom& G = r.g;
+  const int nseg = r.counters[0] * kSegPerTile;
+  const double L[3] = {(double)G.nx, (double)G.ny, (double)G.nz_global};
+  const BodyGeo& b = r.body;
+  const uint32_t full = ((uint32_t)1 << (3 * b.s)) | ((uint32_t)r.id << 16);
+  const int lane = threadIdx.x & 31;
+  const int stride = gridDim.x * blockDim.x;
+  // warp-uniform loop bound: the ballots and shuffles below need every lane
+  for (int wb = blockIdx.x * blockDim.x + (threadIdx.x & ~31); wb < nseg; wb += stride) {
+    const int i = wb + lane;
+    bool und = false;
+    int tile = 0, sg = 0, y = 0, z = 0, x0 = 0, x1 = 0;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < nseg) {
+      tile = r.tiles[i / kSegPerTile];
+      sg = i % kSegPerTile;
+      int tx, ty, tz;
+      tile_coords(tile, r, tx, ty, tz);
+      const int sx = sg % (kTileX / kSubX), row = sg / (kTileX / kSubX);
+      y = ty * kTileY + row % kTileY;
+      z = tz * kTileZ + row / kTileY;
+      x0 = tx * kTileX + sx * kSubX;
+      if (y < G.ny && z < G.nzl && x0 < G.nx) {
+        x1 = min(x0 + kSubX, G.nx);  // ragged last segment: clamped to the grid
+        const double ps[3] = {0.5 * (x0 + x1), y + 0.5, G.z0 + z + 0.5};
+        const double half[3] = {0.5 * (x1 - x0), 0.5, 0.5};
+        double qs[3];
+        const int dec = tile_decision<kSubReach, 16, 32>(b, ps, half, L, G.wall, qs, r.margin);
+        if (dec == 2) {
+          // straddling segments (seam): every cell transforms its own centre (q.w = 1)
+          const bool own = region_straddles(b, ps, half, L, G.wall, r.margin);
+          q = make_float4((float)qs[0], (float)qs[1], (float)qs[2], own ? 1.f : 0.f);
+          und = true;
+        } else {
+          const uint32_t w = dec == 1 ? full : 0u;
+          for (int c = 0; c < x1 - x0; ++c) put_word(r, x0 + c, y, z, w, tile);
+        }
+      }
+    }
+    unsigned m = __ballot_sync(0xffffffffu, und);
+    while (m) {
+      const int slot = lane >> 3, c = lane & 7;
+      unsigned mm = m;  // the (slot + 1)-th undecided segment of the warp
+      for (int k = 0; k < slot && mm; ++k) mm &= mm - 1;
+      const int src = mm ? __ffs(mm) - 1 : 0;
+      const bool have = mm != 0u;
+      const int t_ = __shfl_sync(0xffffffffu, tile, src);
+      const int sg_ = __shfl_sync(0xffffffffu, sg, src);
+      const int y_ = __shfl_sync(0xffffffffu, y, src);
+      const int z_ = __shfl_sync(0xffffffffu, z, src);
+      const int x0_ = __shfl_sync(0xffffffffu, x0, src);
+      const int x1_ = __shfl_sync(0xffffffffu, x1, src);
+      const float qx = __shfl_sync(0xffffffffu, q.x, src), qy = __shfl_sync(0xffffffffu, q.y, src);
+      const float qz = __shfl_sync(0xffffffffu, q.z, src), qw = __shfl_sync(0xffffffffu, q.w, src);
+      const int x = x0_ + c;
+      if (have && x < x1_) {
+        const float off = (float)x + 0.5f - 0.5f * (float)(x0_ + x1_);
+        const float qc[3] = {qx + (float)b.Q[0] * off, qy + (float)b.Q[1] * off,
+                             qz + (float)b.Q[2] * off};
+        const int cd = qw != 0.f ? cell_decision_own(b, x, y_, G.z0 + z_, L, G.wall, r.margin)
+                                 : cell_decision(b, qc, r.margin);
+        if (cd == 2) {
+          const int k = atomicAdd(r.bandn, 1);
+          if (k < r.band_cap) {
+            const int sx = sg_ % (kTileX / kSubX), row = sg_ / (kTileX / kSubX);
+            r.band[k] = ((uint32_t)t_ << 8) | (uint32_t)(row * kTileX + sx * kSubX + c);
+            r.bandcnt[k] = 0;
+          } else {  // list full: count here
+            const int cnt = exact_count(b, x, y_, G.z0 + z_, L, G.wall);
+            put_word(r, x, y_, z_, cnt ? ((uint32_t)cnt | ((uint32_t)r.id << 16)) : 0u, t_);
+          }
+        } else {
+          put_word(r, x, y_, z_, cd == 1 ? full : 0u, t_);
+        }
+      }
+      for (int k = 0; k < 4 && m; ++k) m &= m - 1;  // the four segments just done
+    }
+  }
+}
+
 __device__ __forceinline__ void band_cell(const RemapParams& r, uint32_t e, int& x, int& y,
                                           int& z, int& tile) {
   tile = (int)(e >> 8);
@@ -321,6 +406,10 @@ int remap_l3_kernels(const BodyGeo& b) {
   return (b.kind != 1 && b.s >= 2 && b.mapping == 0) ? 2 : 1;
 }
 
+int remap_single_kernels(const RemapParams& r) {
+  return (r.fused12 ? 2 : 3) + remap_l3_kernels(r.body);
+}
+
 // the exact pass alone over a cached band (poses within one cell of the band's build pose)
 cudaError_t launch_remap_band(const RemapParams& r, int persistent_blocks, cudaStream_t st,
                               int threads) {
@@ -336,8 +425,12 @@ cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cud
   if (e != cudaSuccess) return e;
   // (a cached band's count is reset by the host once per rebuild, before the body's first box)
   k_remap_l0<<<(ntile + 255) / 256, 256, 0, st>>>(r);
-  k_remap_l1<<<persistent_blocks, threads, 0, st>>>(r);
-  k_remap_l2<<<persistent_blocks, threads, 0, st>>>(r);
+  if (r.fused12) {
+    k_remap_l12<<<persistent_blocks, threads, 0, st>>>(r);
+  } else {
+    k_remap_l1<<<persistent_blocks, threads, 0, st>>>(r);
+    k_remap_l2<<<persistent_blocks, threads, 0, st>>>(r);
+  }
   launch_l3(r, persistent_blocks, st, threads);
   return cudaGetLastError();
 }

@@ -123,6 +123,7 @@ psm_status psm_create(const psm_grid* grid, psm_stencil stencil, double tau,
   c->force_general = std::getenv("PSM_REMAP_GENERAL") != nullptr;
   if (const char* e = std::getenv("PSM_CACHE_MAX_S")) c->cache_max_s = std::atoi(e);
   if (const char* e = std::getenv("PSM_CACHE_MAX_S_R2")) c->cache_max_s_r2 = std::atoi(e);
+  if (const char* e = std::getenv("PSM_REMAP_L12")) c->remap_fused12 = std::atoi(e) != 0;
   if (const char* e = std::getenv("PSM_HIOCC")) c->hiocc_env = std::atoi(e) != 0 ? 1 : 0;
   if (const char* e = std::getenv("PSM_SEG_CAP")) c->seg_cap_env = std::max(1ll, std::atoll(e));
   if (const char* e = std::getenv("PSM_BAND_CAP")) c->band_cap_env = std::max(1ll, std::atoll(e));

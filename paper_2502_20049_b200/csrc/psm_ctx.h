@@ -138,6 +138,7 @@ struct psm_ctx {
   bool no_cache = false, force_general = false;
   int cache_max_s = 1;     // cached narrow band up to this s, R1 (PSM_CACHE_MAX_S)
   int cache_max_s_r2 = 3;  // the same for R2 bodies (PSM_CACHE_MAX_S_R2)
+  int remap_fused12 = 1;   // L1 + L2 in one launch (PSM_REMAP_L12=0: two)
   int hiocc_env = -1;   // PSM_HIOCC: force (1) / forbid (0) the higher-occupancy fp64 collide
   double psm_tile_frac = 0.0;  // PSM tiles / tiles in the last psm_step call
   int64_t seg_cap_env = 0, band_cap_env = 0;

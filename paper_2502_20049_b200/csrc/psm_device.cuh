@@ -188,6 +188,7 @@ struct RemapParams {
   int seg_cap, band_cap;
   int margin;           // 1: decisions valid for any pose within one cell (cached band)
   FastDiv fgx, fgxy;    // division by g.gx and g.gx * g.gy (tile index -> tile coordinates)
+  int fused12;          // L1 and L2 in one warp-cooperative launch (k_remap_l12)
 };
 
 #if defined(__CUDACC__)

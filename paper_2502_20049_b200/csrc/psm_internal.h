@@ -44,7 +44,8 @@ cudaError_t launch_voxelize(VoxParams p, void* scratch, uint8_t* mask, cudaStrea
 cudaError_t launch_map(const MapParams& p, cudaStream_t st);
 cudaError_t launch_remap_single(const RemapParams& r, int persistent_blocks, cudaStream_t st,
                                 int threads = 256);
-int remap_l3_kernels(const BodyGeo& b);  // kernels launch_remap_band launches
+int remap_l3_kernels(const BodyGeo& b);        // kernels launch_remap_band launches
+int remap_single_kernels(const RemapParams& r);  // kernels launch_remap_single launches
 cudaError_t launch_remap_band(const RemapParams& r, int persistent_blocks, cudaStream_t st,
                               int threads = 256);
 
