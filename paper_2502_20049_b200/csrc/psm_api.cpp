@@ -602,8 +602,12 @@ psm_status psm_step(psm_ctx* c, int64_t n) {
   p.overflow = c->overflow;
   p.err = c->err;
   // fp64 D3Q19: the higher-occupancy collide when PSM tiles were frequent at the end of the
-  // previous call (more than 8 % of the tiles; PSM_HIOCC=0/1 forces it)
-  p.hiocc = c->hiocc_env >= 0 ? c->hiocc_env : (c->psm_tile_frac > 0.08 ? 1 : 0);
+  // previous call (PSM_HIOCC=0/1 forces it).  Break-even measured per operator: fluid-only it
+  // costs 0.8-2 %; the AA cumulant's PSM tiles gain enough from 2.5 % of the tiles on (c5wpap,
+  // 3.2 %: +0.45 %), the other operators from 8 % (c3 scenario A, 15 %: +4-7 %)
+  const bool aa_cum = c->opt.pattern == PSM_AA && c->opt.collision == PSM_CUMULANT;
+  p.hiocc = c->hiocc_env >= 0 ? c->hiocc_env
+                              : (c->psm_tile_frac > (aa_cum ? 0.025 : 0.08) ? 1 : 0);
   p.dbg_B = c->dbg_B;
   p.dbg_us = c->dbg_us;
   p.dbg_id = c->dbg_id;
