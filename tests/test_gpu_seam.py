@@ -105,6 +105,10 @@ SEAM_CASES = {
     "mesh_s2_overflow": ("mesh", 2, 1, {"PSM_SEG_CAP": "9", "PSM_BAND_CAP": "17"}),
     "sphere_s1_band": ("sphere", 1, 1, {}),
     "sphere_s2_general": ("sphere", 2, 1, {"PSM_REMAP_GENERAL": "1"}),
+    # the two-launch L1/L2 form (PSM_REMAP_L12=0) and the R2 mapping's cached band at s = 2, 3
+    "mesh_s2_l1l2": ("mesh", 2, 1, {"PSM_REMAP_L12": "0"}),
+    "mesh_s2_r2_band": ("mesh", 2, 1, {}, "R2"),
+    "mesh_s3_r2_ahead": ("mesh", 3, 2, {}, "R2"),
 }
 
 
@@ -115,7 +119,8 @@ def test_large_body_at_periodic_seam(case):
     boundary, remapped by the library's own closed-form advance (psm_step, rows a1/a2): the
     library's pose equals oracle.pose_advance bit for bit and the counts are bit-exact against
     the oracle at every checked step."""
-    kind, s, chunk, env = SEAM_CASES[case]
+    kind, s, chunk, env = SEAM_CASES[case][:4]
+    mapping = SEAM_CASES[case][4] if len(SEAM_CASES[case]) > 4 else "R1"
     nx, ny, nz = GRID
     Q0 = pi.rotation_about([0.3, -1.0, 0.5], 0.7)
     t0 = [66.3, 2.1, 36.7]
@@ -132,7 +137,8 @@ def test_large_body_at_periodic_seam(case):
     if kind == "mesh":
         mv, mt = _seam_propeller()
         o.set_mesh(1, mv, mt, s)
-        g.set_mesh(1, mv, mt, s, Q0, t0, v, w)
+        o.set_mapping(1, mapping)
+        g.set_mesh(1, mv, mt, s, Q0, t0, v, w, mapping=mapping)
     else:
         o.set_sphere(1, 17.5, s)
         g.set_sphere(1, 17.5, s, Q0, t0, v, w)
